@@ -1,0 +1,198 @@
+/*
+ * ms2g.h -- C ABI of libms2g.so, the B200 (sm_100a) hot path of PnP-MS2G
+ * (Tang, "Multi-Stage Sketched Gradient ... Plug-and-Play", arXiv 2203.07308).
+ *
+ * Citation keys: P:NN = PAPER.md line NN (the paper), S:NN = SPEC.md line NN,
+ * Z1..Z23 / O1..O13 = the readings listed in DESIGN.md.
+ *
+ * Conventions for every call
+ *  - Return value: MS2G_OK (0) or an error code; ms2g_last_error() returns a
+ *    thread-local message for the last failing call on this thread.
+ *  - Image / sinogram pointers are caller-owned DEVICE pointers to contiguous
+ *    fp32 arrays.  The library never frees or retains them past the call.
+ *      image     [batch][n_c][n_c], row i along +y, column j along +x, n_c = n/factor
+ *      sinogram  [batch][V_r][B]   (this rank's views [view_begin, view_end))
+ *      compacted [batch][n_sel][B] (views selected by a subset, ascending order)
+ *  - `stream` is a cudaStream_t passed as void*.  Every call is asynchronous
+ *    and ordered on that stream, except where "synchronous" is stated.
+ *  - A plan is used by one host thread at a time.  No call allocates device
+ *    memory after ms2g_plan_geometry / ms2g_attach_nccl, so sequences of calls
+ *    are CUDA-graph capturable.
+ *  - Configuration errors are detected on the host before any launch.
+ */
+#ifndef MS2G_H
+#define MS2G_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MS2G_OK = 0,
+  MS2G_ERR_CONFIG = 2,    /* invalid description / shapes (SPEC exit code 2) */
+  MS2G_ERR_DIVERGED = 3,  /* non-finite iterate (SPEC exit code 3)      */
+  MS2G_ERR_CUDA = 5,      /* CUDA runtime failure                                      */
+  MS2G_ERR_NCCL = 6,      /* NCCL failure                                              */
+  MS2G_ERR_INPUT = 7      /* invalid pointer / subset / argument value                 */
+};
+
+typedef struct ms2g_plan ms2g_plan;  /* opaque: owns device geometry tables + workspaces */
+
+/* Fan-beam geometry (views equally spaced over an arc;
+ * flat detector S:92; reading Z12).  Pixel (i,j) of the n x n grid covers
+ * [-fov/2 + j h, -fov/2 + (j+1) h] x [-fov/2 + i h, ...], h = fov/n.
+ * View v: theta = arc_rad * v / n_views, source sod*(cos, sin), detector
+ * centre -(sdd-sod)*(cos, sin), axis (-sin, cos); bin t at offset
+ * (t - (n_bins-1)/2) * bin_pitch.  One ray per bin. */
+typedef struct {
+  int32_t n;                       /* image side N; every factor must divide it          */
+  double fov;                      /* physical side W (> 0)                               */
+  int32_t n_views;                 /* V, global view count                                */
+  double arc_rad;                  /* angular range (2 pi full scan, pi limited angle)    */
+  int32_t n_bins;                  /* B                                                   */
+  double sod, sdd;                 /* source-centre / source-detector distances;          */
+                                   /* need sod > fov/sqrt2 and sdd - sod > fov/sqrt2      */
+  double bin_pitch;                /* <= 0 selects (sdd/sod) * fov / n                     */
+  int32_t view_begin, view_end;    /* this rank's contiguous shard; (0,0) = all views     */
+  int32_t batch;                   /* images per call (>= 1)                              */
+} ms2g_geom_desc;
+
+/* Build the per-factor ray tables (host fp64, cast once) and every workspace.
+ * factors: the sketch factors s (each divides n) the plan will be used with.
+ * Synchronous.  Errors: MS2G_ERR_CONFIG (bad desc / factor), MS2G_ERR_CUDA. */
+int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32_t n_factors,
+                       ms2g_plan** out);
+void ms2g_plan_destroy(ms2g_plan* plan);
+
+/* Multi-GPU view sharding: rank 0 creates a 128-byte
+ * ncclUniqueId, the caller broadcasts it, then every rank attaches.  After
+ * attaching, back_project(..., allreduce=1) sums partial images over ranks
+ * in place (ncclAllReduce, fp32, sum).  Synchronous.  MS2G_ERR_NCCL. */
+int ms2g_nccl_unique_id(void* out_128_bytes);
+int ms2g_attach_nccl(ms2g_plan* plan, const void* unique_id_128_bytes, int32_t rank, int32_t nranks);
+
+/* Forward projection with fused residual (Eq. 6-7 "A_s S(x) - b"):
+ *   out[b][k][t] = (A_s x_b)[v_k][t] - bsino[b][v_k][t]
+ * A_s = Siddon exact intersection lengths on the n_c = n/factor grid.
+ * x     image [batch][n_c][n_c];  xT optional transposed copy (xT[j][i] =
+ *       x[i][j]); NULL -> the library transposes into a plan workspace.
+ * bsino [batch][V_r][B] indexed by rank-local view, or NULL (plain A_s x).
+ * subset: ascending GLOBAL view indices (NULL = all views); views outside
+ *       this rank's shard are skipped; out is compacted over the rest.
+ * Errors: CONFIG (factor not in plan), INPUT (NULL x/out, bad subset). */
+int ms2g_forward_project(ms2g_plan* plan, int32_t factor, const float* x, const float* xT,
+                         const float* bsino, float* out, const int32_t* subset, int32_t n_subset,
+                         void* stream);
+
+/* Exact adjoint ("A_s^T"):  img[b] = scale * A_s^T sino[b]
+ * (accumulate != 0: img += ...).  sino is compacted [batch][n_sel][B] in the
+ * same view order forward_project used.  allreduce != 0 sums the partial
+ * images over the attached NCCL ranks in place (requires attach_nccl). */
+int ms2g_back_project(ms2g_plan* plan, int32_t factor, const float* sino, float* img, float scale,
+                      int32_t accumulate, const int32_t* subset, int32_t n_subset, int32_t allreduce,
+                      void* stream);
+
+/* Image-space sketch S_s (north-star D; reading Z2): s x s average pool,
+ * x [batch][n][n] -> v [batch][n/s][n/s]; vT (optional, may be NULL)
+ * receives the transposed copy the forward projector reads. */
+int ms2g_sketch_down(ms2g_plan* plan, int32_t factor, const float* x, float* v, float* vT,
+                     void* stream);
+
+/* Upsample + step ("z = y - eta U G"; reading Z2: U_s = nearest
+ * replication = s^2 S_s^T):  z = y - eta * U_s g.  y == NULL gives z = U_s g. */
+int ms2g_sketch_up(ms2g_plan* plan, int32_t factor, const float* g, const float* y, float eta,
+                   float* z, void* stream);
+
+/* Sketched data-fidelity gradient (Eq. 6, Eq. 7):
+ *   g = (V/|M|) U_s A_s^T (A_s S_s x - b_M)      (full resolution n x n)
+ * factor 1 gives A^T(Ax - b).  subset NULL = all views (|M| = V).
+ * With NCCL attached the partial A_s^T is allreduced before U_s. */
+int ms2g_sketched_grad(ms2g_plan* plan, int32_t factor, const float* x, const float* bsino, float* g,
+                       const int32_t* subset, int32_t n_subset, void* stream);
+
+/* Lipschitz constant of the factor-s fidelity ("eta = O(1/L)"; reading
+ * Z5/Z6): v0 = 1/||1||, w = A_s^T A_s v, L = <v,w>, v = w/||w||, `iters`
+ * times over all views (allreduced when NCCL is attached).  fp64 dots.
+ * Synchronous: *L is written on return. */
+int ms2g_power_iteration(ms2g_plan* plan, int32_t factor, int32_t iters, double* L, void* stream);
+
+/* Denoiser D: kind 0 identity, 1 Gaussian 3x3 (sigma, replicate
+ * boundary), 2 TV-prox by Chambolle's dual iteration (lambda, tau <= 1/8,
+ * inner_iters).  z, out: [batch][n][n], must not alias. */
+typedef struct {
+  int32_t kind;
+  float sigma;
+  float lambda;
+  float tau;
+  int32_t inner_iters;
+} ms2g_denoiser;
+int ms2g_denoise(ms2g_plan* plan, const ms2g_denoiser* den, const float* z, float* out, void* stream);
+
+/* Algorithm 1.  Option 1: n_iters steps per stage on all views.
+ * Option 2: n_epochs per stage, each epoch visits the n_subsets interleaved
+ * view subsets {v : v mod n_subsets == k} in a Fisher-Yates order drawn from
+ * one SplitMix64 stream seeded with `seed` (reading Z8/Z9; O13). */
+typedef struct {
+  int32_t factor, n_iters, n_epochs;
+} ms2g_stage;
+typedef struct {
+  const ms2g_stage* stages;
+  int32_t n_stages;
+  int32_t option;        /* 1 | 2                                         */
+  int32_t n_subsets;     /* Option 2 only                                 */
+  uint64_t seed;
+  ms2g_denoiser den;
+  float alpha;           /* RED-PRO mix weight, 0 < alpha <= 1      */
+  int32_t power_iters;   /* per-stage power iterations (20 in the configs) */
+  int32_t check_every;   /* unused by the graph path: every step is checked on device */
+} ms2g_solve_desc;
+/* One global iteration: i (1-based, continuous over stages), stage,
+ * factor, subset (-1 = all views), eta = 1/L_stage, a_i = (i-1)/(i+3). */
+typedef struct {
+  int32_t i, stage, factor, subset;
+  double eta, a;
+} ms2g_sched_entry;
+
+/* Host-only, bit-exact schedule (eta left 0).  *n_out = total steps; at most
+ * `cap` entries are written.  MS2G_ERR_CONFIG on a bad description.  plan
+ * may be NULL (then factor divisibility and n_subsets <= n_views are not
+ * checked); no device is touched. */
+int ms2g_schedule(const ms2g_plan* plan, const ms2g_solve_desc* desc, ms2g_sched_entry* out, int32_t cap,
+                  int32_t* n_out);
+
+/* Whole PnP-MS2G solve, captured once as a CUDA graph per (plan, desc,
+ * pointers) and replayed: per stage the power iteration, then per step
+ *   v = S_s y; r = A_s v - b_M; G = c A_s^T r (+allreduce); z = y - eta U_s G;
+ *   x = (1-alpha) z + alpha D(z); y = x + a_i (x - x_prev).
+ * x0 = y0, b [batch][V_r][B], x_out [batch][n][n] (may alias x0).
+ * trace (optional, host) receives the schedule with eta filled in.
+ * Synchronous on return (the divergence flag is read back): a non-finite
+ * iterate returns MS2G_ERR_DIVERGED naming the stage and iteration. */
+int ms2g_pnp_ms2g_solve(ms2g_plan* plan, const ms2g_solve_desc* desc, const float* b, const float* x0,
+                        float* x_out, ms2g_sched_entry* trace, void* stream);
+
+/* Same solve, asynchronous: the graph is launched and the call returns; the
+ * divergence flag is left on the device (read it with ms2g_solve_status). */
+int ms2g_pnp_ms2g_solve_async(ms2g_plan* plan, const ms2g_solve_desc* desc, const float* b,
+                              const float* x0, float* x_out, void* stream);
+/* Synchronous: returns MS2G_OK or MS2G_ERR_DIVERGED for the last solve. */
+int ms2g_solve_status(ms2g_plan* plan, void* stream);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* ms2g_last_error(void);
+
+/* Number of device kernels libms2g has launched in this process (graph
+ * replays count their kernel nodes).  For the bench's gpu_launches claim. */
+uint64_t ms2g_launch_count(void);
+
+/* Plan facts for the binding: coarse side for a factor (0 if not planned),
+ * rank-local view range and batch. */
+int ms2g_plan_info(const ms2g_plan* plan, int32_t factor, int32_t* n_c, int32_t* view_begin,
+                   int32_t* view_end, int32_t* batch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MS2G_H */

@@ -1,0 +1,319 @@
+// image_ops.cu -- streaming kernels of the PnP-MS2G step (sm_100a):
+//   sketch S_s (+ transposed copy for the projector), upsample+step,
+//   Gaussian / TV-prox denoisers fused with the RED-PRO mix and the FISTA
+//   momentum, and the fp64 reductions of the power iteration.
+// These are HBM/L2-streaming kernels; one thread per
+// output pixel, coalesced along rows, 32x32 shared tiles for transposes.
+#include <climits>
+
+#include "internal.cuh"
+
+namespace ms2g {
+
+static inline int grid1d(size_t total, int block = 256, int cap = 148 * 32) {
+  size_t g = (total + block - 1) / block;
+  if (g > (size_t)cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// -------------------------------------------------------------- sketch --
+// S_s: s x s average pool (north-star D; BASELINE configs "2x2 average pool").
+// Writes v (row-major) and/or vT (transposed) through a 32x33 shared tile.
+__global__ void k_sketch_down(const float* __restrict__ x, float* __restrict__ v, float* __restrict__ vT,
+                              int n, int s, int nc) {
+  __shared__ float tile[32][33];
+  const int bz = blockIdx.z;
+  const float* xb = x + (size_t)bz * n * n;
+  const size_t cb = (size_t)bz * nc * nc;
+  const int I0 = blockIdx.y * 32, J0 = blockIdx.x * 32;
+  const float inv = 1.0f / (float)(s * s);
+  for (int di = threadIdx.y; di < 32; di += 8) {
+    const int I = I0 + di, J = J0 + threadIdx.x;
+    if (I < nc && J < nc) {
+      float acc = 0.f;
+      for (int a = 0; a < s; ++a) {
+        const float* row = xb + (size_t)(s * I + a) * n + (size_t)s * J;
+        for (int b = 0; b < s; ++b) acc += row[b];
+      }
+      const float val = (s == 1) ? acc : acc * inv;
+      if (v) v[cb + (size_t)I * nc + J] = val;
+      tile[di][threadIdx.x] = val;
+    }
+  }
+  if (!vT) return;
+  __syncthreads();
+  for (int di = threadIdx.y; di < 32; di += 8) {
+    const int J = J0 + di, I = I0 + threadIdx.x;
+    if (I < nc && J < nc) vT[cb + (size_t)J * nc + I] = tile[threadIdx.x][di];
+  }
+}
+
+int launch_sketch_down(int n, int s, int batch, const float* x, float* v, float* vT, cudaStream_t st) {
+  const int nc = n / s;
+  dim3 grid((nc + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
+  k_sketch_down<<<grid, block, 0, st>>>(x, v, vT, n, s, nc);
+  return check_launch("k_sketch_down");
+}
+
+int launch_transpose(int n, int batch, const float* x, float* xT, cudaStream_t st) {
+  return launch_sketch_down(n, 1, batch, x, nullptr, xT, st);
+}
+
+// ---------------------------------------------------------- upsample+step --
+// z = y - eta * U_s g, U_s = nearest replication (reading Z2).
+__global__ void k_up_step(const float* __restrict__ g, const float* __restrict__ y,
+                          const float* __restrict__ eta_dev, float eta, float* __restrict__ z, int n, int s,
+                          int nc, size_t total) {
+  const float e = eta_dev ? *eta_dev : eta;
+  const size_t np = (size_t)n * n;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = idx / np, p = idx % np;
+    const int i = (int)(p / n), j = (int)(p % n);
+    const float gv = g[b * nc * nc + (size_t)(i / s) * nc + (j / s)];
+    z[idx] = y ? (y[idx] - e * gv) : gv;
+  }
+}
+
+int launch_up_step(int n, int s, int batch, const float* g, const float* y, const float* eta_dev, float eta,
+                   float* z, cudaStream_t st) {
+  const size_t total = (size_t)n * n * batch;
+  k_up_step<<<grid1d(total), 256, 0, st>>>(g, y, eta_dev, eta, z, n, s, n / s, total);
+  return check_launch("k_up_step");
+}
+
+// --------------------------------------------------- mix + momentum core --
+// x = (1-alpha) z + alpha D(z);  y = x + a (x - x_prev);
+// a non-finite x or y records the global iteration in *flag.
+__device__ __forceinline__ void mix_momentum(size_t idx, float zv, float dv, const float* __restrict__ xprev,
+                                             float* __restrict__ xout, float* __restrict__ yout, float alpha,
+                                             float a, int mode, int* flag, int iter) {
+  if (mode == 0) {  // plain denoiser output
+    xout[idx] = dv;
+    return;
+  }
+  const float xv = (1.f - alpha) * zv + alpha * dv;
+  const float yv = xv + a * (xv - xprev[idx]);
+  xout[idx] = xv;
+  yout[idx] = yv;
+  if (!isfinite(xv) || !isfinite(yv)) atomicMin(flag, iter);
+}
+
+// Gaussian 3x3 (BASELINE configs[0], sigma = 0.8): separable [w1, w0, w1],
+// replicate boundary, rows then columns.
+__global__ void k_gauss_mm(const float* __restrict__ z, const float* __restrict__ xprev, float* __restrict__ xout,
+                           float* __restrict__ yout, int n, float w0, float w1, float alpha, float a, int mode,
+                           int* flag, int iter, size_t total) {
+  const size_t np = (size_t)n * n;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = idx / np, p = idx % np;
+    const int i = (int)(p / n), j = (int)(p % n);
+    const float* zb = z + b * np;
+    const int jl = max(j - 1, 0), jr = min(j + 1, n - 1);
+    float t[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int r = min(max(i + q - 1, 0), n - 1);
+      const float* row = zb + (size_t)r * n;
+      t[q] = w1 * row[jl] + w0 * row[j] + w1 * row[jr];
+    }
+    const float dv = w1 * t[0] + w0 * t[1] + w1 * t[2];
+    mix_momentum(idx, zb[p], dv, xprev, xout, yout, alpha, a, mode, flag, iter);
+  }
+}
+
+int launch_gauss_mix_mom(int n, int batch, float sigma, const float* z, const float* xprev, float* xout,
+                         float* yout, float alpha, float a, int mode, int* flag, int iter, cudaStream_t st) {
+  const double e = exp(-1.0 / (2.0 * (double)sigma * (double)sigma));
+  const float w1 = (float)(e / (1.0 + 2.0 * e)), w0 = (float)(1.0 / (1.0 + 2.0 * e));
+  const size_t total = (size_t)n * n * batch;
+  k_gauss_mm<<<grid1d(total), 256, 0, st>>>(z, xprev, xout, yout, n, w0, w1, alpha, a, mode, flag, iter, total);
+  return check_launch("k_gauss_mm");
+}
+
+__global__ void k_copy_mm(const float* __restrict__ z, const float* __restrict__ xprev, float* __restrict__ xout,
+                          float* __restrict__ yout, float a, int mode, int* flag, int iter, size_t total) {
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const float zv = z[idx];
+    mix_momentum(idx, zv, zv, xprev, xout, yout, 1.f, a, mode, flag, iter);
+  }
+}
+
+int launch_copy_mix_mom(int n, int batch, const float* z, const float* xprev, float* xout, float* yout, float a,
+                        int mode, int* flag, int iter, cudaStream_t st) {
+  const size_t total = (size_t)n * n * batch;
+  k_copy_mm<<<grid1d(total), 256, 0, st>>>(z, xprev, xout, yout, a, mode, flag, iter, total);
+  return check_launch("k_copy_mm");
+}
+
+// ------------------------------------------------------------- TV-prox --
+// Chambolle 2004 dual fixed point ("TV-prox"; reading Z18):
+//   w = div p - f/lambda,  q = grad w,  p <- (p + tau q) / (1 + tau |q|),
+//   u = f - lambda div p.  Forward differences, zero last row/column.
+// p layout: [batch][2][n][n] (x-component, then y-component).
+__device__ __forceinline__ float tv_div(const float* __restrict__ px, const float* __restrict__ py, int n, int i,
+                                        int j) {
+  const size_t q = (size_t)i * n + j;
+  const float a = (j < n - 1 ? px[q] : 0.f) - (j > 0 ? px[q - 1] : 0.f);
+  const float b = (i < n - 1 ? py[q] : 0.f) - (i > 0 ? py[q - n] : 0.f);
+  return a + b;
+}
+
+__global__ void k_tv_iter(const float* __restrict__ f, const float* __restrict__ pin, float* __restrict__ pout,
+                          int n, float inv_lambda, float tau, size_t total) {
+  const size_t np = (size_t)n * n;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = idx / np, p = idx % np;
+    const int i = (int)(p / n), j = (int)(p % n);
+    const float* fb = f + b * np;
+    const float* px = pin + b * 2 * np;
+    const float* py = px + np;
+    const float wc = tv_div(px, py, n, i, j) - fb[p] * inv_lambda;
+    float qx = 0.f, qy = 0.f;
+    if (j < n - 1) qx = (tv_div(px, py, n, i, j + 1) - fb[p + 1] * inv_lambda) - wc;
+    if (i < n - 1) qy = (tv_div(px, py, n, i + 1, j) - fb[p + n] * inv_lambda) - wc;
+    const float den = 1.f + tau * sqrtf(qx * qx + qy * qy);
+    float* ox = pout + b * 2 * np;
+    ox[p] = (px[p] + tau * qx) / den;
+    ox[np + p] = (py[p] + tau * qy) / den;
+  }
+}
+
+__global__ void k_tv_final(const float* __restrict__ f, const float* __restrict__ pin,
+                           const float* __restrict__ xprev, float* __restrict__ xout, float* __restrict__ yout,
+                           int n, float lambda, float alpha, float a, int mode, int* flag, int iter, size_t total) {
+  const size_t np = (size_t)n * n;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = idx / np, p = idx % np;
+    const int i = (int)(p / n), j = (int)(p % n);
+    const float* px = pin + b * 2 * np;
+    const float fv = f[idx];
+    const float u = fv - lambda * tv_div(px, px + np, n, i, j);
+    mix_momentum(idx, fv, u, xprev, xout, yout, alpha, a, mode, flag, iter);
+  }
+}
+
+__global__ void k_fill(float* __restrict__ x, size_t count, float value) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+    x[i] = value;
+}
+
+int launch_fill(float* x, size_t count, float value, cudaStream_t st) {
+  k_fill<<<grid1d(count), 256, 0, st>>>(x, count, value);
+  return check_launch("k_fill");
+}
+
+int launch_tv(int n, int batch, float lambda, float tau, int iters, const float* f, float* p0, float* p1,
+              const float* xprev, float* xout, float* yout, float alpha, float a, int mode, int* flag, int iter,
+              cudaStream_t st) {
+  const size_t total = (size_t)n * n * batch;
+  if (lambda == 0.f) {  // prox of the zero function: identity
+    return launch_copy_mix_mom(n, batch, f, xprev, xout, yout, a, mode, flag, iter, st);
+  }
+  MS2G_TRY(launch_fill(p0, 2 * total, 0.f, st));  // p^0 = 0 at every call (no warm start)
+  float* pin = p0;
+  float* pout = p1;
+  for (int k = 0; k < iters; ++k) {
+    k_tv_iter<<<grid1d(total), 256, 0, st>>>(f, pin, pout, n, 1.f / lambda, tau, total);
+    MS2G_TRY(check_launch("k_tv_iter"));
+    float* tmp = pin;
+    pin = pout;
+    pout = tmp;
+  }
+  k_tv_final<<<grid1d(total), 256, 0, st>>>(f, pin, xprev, xout, yout, n, lambda, alpha, a, mode, flag, iter,
+                                            total);
+  return check_launch("k_tv_final");
+}
+
+// ------------------------------------------------------ power iteration --
+// O8 / Z6: L = <v, w>, v <- w / ||w||, fp64 partial sums with a fixed
+// per-thread order and a fixed tree: deterministic.
+__global__ void k_dot_norm(const float* __restrict__ v, const float* __restrict__ w, size_t np,
+                           double* __restrict__ red) {
+  __shared__ double sd[256], sn[256];
+  double d = 0.0, q = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+    const double wi = w[i];
+    d += (double)v[i] * wi;
+    q += wi * wi;
+  }
+  sd[threadIdx.x] = d;
+  sn[threadIdx.x] = q;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sd[threadIdx.x] += sd[threadIdx.x + o];
+      sn[threadIdx.x] += sn[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    red[2 * blockIdx.x] = sd[0];
+    red[2 * blockIdx.x + 1] = sn[0];
+  }
+}
+
+__global__ void k_power_finalize(const double* __restrict__ red, int nblocks, double* __restrict__ pw,
+                                 double* L_out, double* eta_out, float* etaf_out) {
+  if (threadIdx.x != 0) return;
+  double d = 0.0, q = 0.0;
+  for (int b = 0; b < nblocks; ++b) {
+    d += red[2 * b];
+    q += red[2 * b + 1];
+  }
+  pw[0] = d;
+  pw[1] = q > 0.0 ? 1.0 / sqrt(q) : 0.0;
+  if (L_out) *L_out = d;
+  if (eta_out) *eta_out = 1.0 / d;
+  if (etaf_out) *etaf_out = (float)(1.0 / d);
+}
+
+__global__ void k_scale_T(const float* __restrict__ w, const double* __restrict__ pw, float* __restrict__ v,
+                          float* __restrict__ vT, int nc) {
+  __shared__ float tile[32][33];
+  const float inv = (float)pw[1];
+  const int I0 = blockIdx.y * 32, J0 = blockIdx.x * 32;
+  for (int di = threadIdx.y; di < 32; di += 8) {
+    const int I = I0 + di, J = J0 + threadIdx.x;
+    if (I < nc && J < nc) {
+      const float val = w[(size_t)I * nc + J] * inv;
+      v[(size_t)I * nc + J] = val;
+      tile[di][threadIdx.x] = val;
+    }
+  }
+  __syncthreads();
+  for (int di = threadIdx.y; di < 32; di += 8) {
+    const int J = J0 + di, I = I0 + threadIdx.x;
+    if (I < nc && J < nc) vT[(size_t)J * nc + I] = tile[threadIdx.x][di];
+  }
+}
+
+int launch_power_step(int nc, int /*batch*/, const float* v, const float* w, double* red, int red_blocks,
+                      double* pw, double* L_out, float* vnext, float* vnextT, double* eta_out, float* etaf_out,
+                      cudaStream_t st) {
+  const size_t np = (size_t)nc * nc;
+  k_dot_norm<<<red_blocks, 256, 0, st>>>(v, w, np, red);
+  MS2G_TRY(check_launch("k_dot_norm"));
+  k_power_finalize<<<1, 32, 0, st>>>(red, red_blocks, pw, L_out, eta_out, etaf_out);
+  MS2G_TRY(check_launch("k_power_finalize"));
+  if (vnext) {
+    dim3 grid((nc + 31) / 32, (nc + 31) / 32), block(32, 8);
+    k_scale_T<<<grid, block, 0, st>>>(w, pw, vnext, vnextT, nc);
+    MS2G_TRY(check_launch("k_scale_T"));
+  }
+  return MS2G_OK;
+}
+
+__global__ void k_init_flag(int* flag) { *flag = INT_MAX; }
+
+int launch_init_flag(int* flag, cudaStream_t st) {
+  k_init_flag<<<1, 1, 0, st>>>(flag);
+  return check_launch("k_init_flag");
+}
+
+}  // namespace ms2g

@@ -1,0 +1,164 @@
+// internal.cuh -- shared declarations of libms2g (CUDA product path).
+// Independent of oracle/: no code, header or table is shared with it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/ms2g.h"
+
+namespace ms2g {
+
+// Fixed-point minor coordinate: 32 fractional bits (1 unit = 2^-32 pixel).
+constexpr double kFix = 4294967296.0;
+
+enum RayFlags : int { kMajorY = 1, kMirror = 2 };
+
+// One ray of one view on the grid of one factor (32 bytes).  The ray is a
+// line "minor = F0 + S * major" in pixel units of the n_c grid, in a frame
+// where the minor axis may be mirrored (minor' = n_c - minor) so that the
+// slope S is in [0, 1].  major = x (column) for |dx| >= |dy|, else y (row).
+struct __align__(16) RayEntry {
+  long long F0;             // minor' at major coordinate 0, 2^-32 units
+  unsigned long long S;     // minor' step per unit major step, 2^-32 units (<= 2^32)
+  float Lc;                 // physical length per unit major step: h_c sqrt(1 + slope^2)
+  float Ly32;               // Lc / slope' * 2^-32 (0 when S == 0)
+  int flags;                // kMajorY | kMirror
+  short c_lo, c_hi;         // major indices [c_lo, c_hi) where the ray meets the grid
+};
+static_assert(sizeof(RayEntry) == 32, "RayEntry must be 32 bytes");
+
+// Per-view constants for the detector-coordinate map of a point P (pixel
+// units of the n_c grid):  tau(P) = off + scale * ((P-S).e) / ((P-S).n).
+struct __align__(16) ViewEntry {
+  float Sx, Sy, ex, ey, nx, ny, scale, off;
+};
+
+struct FactorTables {
+  int factor = 0, nc = 0;
+  RayEntry* d_rays = nullptr;     // [V_r][B]
+  ViewEntry* d_views = nullptr;   // [V_r]
+  int bp_chunks = 1;              // view chunks of the backprojector
+};
+
+struct SolveGraph {
+  std::string key;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernel_nodes = 0;
+};
+
+}  // namespace ms2g
+
+struct ms2g_plan {
+  ms2g_geom_desc d{};
+  int V_r = 0;                         // views in this rank's shard
+  int B = 0;
+  double pitch = 0;
+  std::vector<ms2g::FactorTables> ft;
+  int nmax_c = 0;                      // largest coarse side among the factors
+  // workspaces (all sized for batch)
+  float* w_xT = nullptr;               // transposed input for forward_project(xT == NULL)
+  float* w_v = nullptr;                // coarse sketch
+  float* w_vT = nullptr;               // its transpose
+  float* w_G = nullptr;                // coarse gradient / backprojection
+  float* w_res = nullptr;              // residual / projection [batch][V_r][B]
+  float* w_part = nullptr;             // backprojection chunk partials
+  size_t part_elems = 0;
+  float* w_x[2] = {nullptr, nullptr};  // iterate double buffer (full res)
+  float* w_y = nullptr;                // extrapolated point
+  float* w_z = nullptr;                // pre-denoiser point
+  float* w_p[2] = {nullptr, nullptr};  // TV dual double buffer [batch][2][n][n]
+  double* w_red = nullptr;             // reduction partials
+  int red_blocks = 0;
+  double* w_scal = nullptr;            // device scalars: [0..63] L per stage, [64..127] eta
+  float* w_etaf = nullptr;             // fp32 eta per stage [64]
+  double* w_pw = nullptr;              // power-iteration scalars (dot, inv_norm)
+  int* w_flag = nullptr;               // first non-finite global iteration (INT_MAX = none)
+  int* w_sel = nullptr;                // selected-view scratch [V_r]
+  int* h_sel = nullptr;                // pinned host staging for subsets
+  cudaEvent_t sel_ev = nullptr;
+  int* w_subsets = nullptr;            // precomputed Option-2 subset lists
+  std::vector<int> subset_off, subset_len, subset_global_len;
+  int subsets_n = 0;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  // graph cache
+  ms2g::SolveGraph sg;
+  int last_total_steps = 0;
+  std::vector<ms2g_sched_entry> last_sched;
+  std::vector<int> last_stage_of_step;
+};
+
+namespace ms2g {
+
+// error handling (thread-local message)
+int set_error(int code, const std::string& msg);
+#define MS2G_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e__ = (call);                                                             \
+    if (e__ != cudaSuccess)                                                               \
+      return ::ms2g::set_error(MS2G_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+#define MS2G_NCCL(call)                                                                   \
+  do {                                                                                    \
+    ncclResult_t r__ = (call);                                                            \
+    if (r__ != ncclSuccess)                                                               \
+      return ::ms2g::set_error(MS2G_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r__)); \
+  } while (0)
+#define MS2G_TRY(call)         \
+  do {                         \
+    int rc__ = (call);         \
+    if (rc__ != MS2G_OK) return rc__; \
+  } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// launches issued while a solve graph is being captured (not yet executed)
+extern thread_local bool t_capturing;
+extern thread_local uint64_t t_captured;
+inline void note_launch() {
+  if (t_capturing) ++t_captured;
+  else count_launch();
+}
+inline int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(MS2G_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  note_launch();
+  return MS2G_OK;
+}
+
+const FactorTables* find_factor(const ms2g_plan* p, int factor);
+
+// ---- kernel launchers (projector.cu) ----
+int launch_forward(ms2g_plan* p, const FactorTables& f, const float* x, const float* xT, const float* b,
+                   float* out, const int* d_sel, int n_sel, int batch, cudaStream_t s);
+int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
+                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s);
+
+// ---- image kernels (image_ops.cu) ----
+int launch_sketch_down(int n, int s, int batch, const float* x, float* v, float* vT, cudaStream_t st);
+int launch_transpose(int n, int batch, const float* x, float* xT, cudaStream_t st);
+int launch_up_step(int n, int s, int batch, const float* g, const float* y, const float* eta_dev,
+                   float eta, float* z, cudaStream_t st);
+int launch_gauss_mix_mom(int n, int batch, float sigma, const float* z, const float* xprev, float* xout,
+                         float* yout, float alpha, float a, int mode, int* flag, int iter, cudaStream_t st);
+int launch_tv(int n, int batch, float lambda, float tau, int iters, const float* f, float* p0, float* p1,
+              const float* xprev, float* xout, float* yout, float alpha, float a, int mode, int* flag,
+              int iter, cudaStream_t st);
+int launch_copy_mix_mom(int n, int batch, const float* z, const float* xprev, float* xout, float* yout,
+                        float a, int mode, int* flag, int iter, cudaStream_t st);
+int launch_fill(float* x, size_t count, float value, cudaStream_t st);
+int launch_power_step(int nc, int batch, const float* v, const float* w, double* red, int red_blocks,
+                      double* pw, double* L_out, float* vnext, float* vnextT, double* eta_out,
+                      float* etaf_out, cudaStream_t st);
+int launch_init_flag(int* flag, cudaStream_t st);
+
+}  // namespace ms2g

@@ -1,0 +1,701 @@
+// ms2g_api.cu -- C ABI of libms2g (include/ms2g.h): plan, geometry tables,
+// operator entry points, schedule, power iteration and the graph-captured
+// PnP-MS2G solve.  Host code only; kernels live in projector.cu/image_ops.cu.
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+#include "internal.cuh"
+
+namespace ms2g {
+
+std::atomic<uint64_t> g_launches{0};
+thread_local bool t_capturing = false;
+thread_local uint64_t t_captured = 0;
+static thread_local std::string t_err;
+
+int set_error(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+const FactorTables* find_factor(const ms2g_plan* p, int factor) {
+  for (const auto& f : p->ft)
+    if (f.factor == factor) return &f;
+  return nullptr;
+}
+
+// floor / ceil division of a signed 64-bit value by a positive divisor
+static long long floor_div(long long a, long long b) {
+  long long q = a / b;
+  if ((a % b != 0) && (a < 0)) --q;
+  return q;
+}
+static long long ceil_div(long long a, long long b) { return -floor_div(-a, b); }
+
+// Geometry plan: per-view and
+// per-ray constants computed in fp64 on the host, rounded once.
+static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
+  const ms2g_geom_desc& d = p->d;
+  const int nc = d.n / f.factor;
+  f.nc = nc;
+  const double hc = d.fov / nc, org = -0.5 * d.fov;
+  const int B = p->B, V_r = p->V_r;
+  std::vector<RayEntry> rays((size_t)V_r * B);
+  std::vector<ViewEntry> views(V_r);
+  const long long M = (long long)nc << 32;
+  for (int vl = 0; vl < V_r; ++vl) {
+    const int v = d.view_begin + vl;
+    const double th = d.arc_rad * (double)v / (double)d.n_views;
+    const double c = std::cos(th), s = std::sin(th);
+    const double Sx = (d.sod * c - org) / hc, Sy = (d.sod * s - org) / hc;
+    const double dcx = -(d.sdd - d.sod) * c, dcy = -(d.sdd - d.sod) * s;
+    ViewEntry ve;
+    ve.Sx = (float)Sx; ve.Sy = (float)Sy;
+    ve.ex = (float)(-s); ve.ey = (float)c;
+    ve.nx = (float)(-c); ve.ny = (float)(-s);
+    ve.scale = (float)(d.sdd / p->pitch);
+    ve.off = (float)(0.5 * (B - 1));
+    views[vl] = ve;
+    for (int t = 0; t < B; ++t) {
+      const double u = ((double)t - 0.5 * (double)(B - 1)) * p->pitch;
+      const double Px = (dcx - u * s - org) / hc, Py = (dcy + u * c - org) / hc;
+      const double Dx = Px - Sx, Dy = Py - Sy;
+      RayEntry R;
+      int flags = 0;
+      double slope, m0c;
+      if (std::fabs(Dx) >= std::fabs(Dy)) {
+        slope = Dy / Dx;
+        m0c = Sy - Sx * slope;
+      } else {
+        flags |= kMajorY;
+        slope = Dx / Dy;
+        m0c = Sx - Sy * slope;
+      }
+      const double Lc = hc * std::sqrt(1.0 + slope * slope);
+      if (slope < 0) {
+        flags |= kMirror;
+        slope = -slope;
+        m0c = (double)nc - m0c;
+      }
+      R.F0 = llround(m0c * kFix);
+      R.S = (unsigned long long)llround(slope * kFix);
+      R.Lc = (float)Lc;
+      R.Ly32 = R.S ? (float)(Lc / slope / kFix) : 0.f;
+      R.flags = flags;
+      long long lo, hi;
+      if (R.S == 0) {
+        lo = 0; hi = (R.F0 >= 0 && R.F0 < M) ? nc : 0;
+      } else {
+        const long long Sl = (long long)R.S;
+        lo = floor_div(-R.F0, Sl);
+        if (lo < 0) lo = 0;
+        hi = ceil_div(M - R.F0, Sl);
+        if (hi > nc) hi = nc;
+      }
+      if (lo >= hi) lo = hi = 0;
+      R.c_lo = (short)lo;
+      R.c_hi = (short)hi;
+      rays[(size_t)vl * B + t] = R;
+    }
+  }
+  MS2G_CUDA(cudaMalloc(&f.d_rays, sizeof(RayEntry) * rays.size()));
+  MS2G_CUDA(cudaMalloc(&f.d_views, sizeof(ViewEntry) * views.size()));
+  MS2G_CUDA(cudaMemcpy(f.d_rays, rays.data(), sizeof(RayEntry) * rays.size(), cudaMemcpyHostToDevice));
+  MS2G_CUDA(cudaMemcpy(f.d_views, views.data(), sizeof(ViewEntry) * views.size(), cudaMemcpyHostToDevice));
+  // backprojector view chunks: enough blocks for ~4 waves of 148 SMs
+  const int tiles_x = (nc + 31) / 32;
+  const long long tiles = (long long)tiles_x * tiles_x * d.batch;
+  const long long target = 4LL * sm_count;
+  long long ch = (target + tiles - 1) / tiles;
+  const long long maxch = (V_r + 7) / 8;
+  if (ch > maxch) ch = maxch;
+  if (ch < 1) ch = 1;
+  f.bp_chunks = (int)ch;
+  return MS2G_OK;
+}
+
+static void free_plan(ms2g_plan* p) {
+  if (!p) return;
+  for (auto& f : p->ft) {
+    cudaFree(f.d_rays);
+    cudaFree(f.d_views);
+  }
+  float* fl[] = {p->w_xT, p->w_v, p->w_vT, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
+                 p->w_y, p->w_z, p->w_p[0], p->w_p[1], p->w_etaf};
+  for (float* q : fl) cudaFree(q);
+  cudaFree(p->w_red);
+  cudaFree(p->w_scal);
+  cudaFree(p->w_pw);
+  cudaFree(p->w_flag);
+  cudaFree(p->w_sel);
+  cudaFree(p->w_subsets);
+  if (p->h_sel) cudaFreeHost(p->h_sel);
+  if (p->sel_ev) cudaEventDestroy(p->sel_ev);
+  if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
+  if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
+  if (p->comm) ncclCommDestroy(p->comm);
+  delete p;
+}
+
+// Resolve a host subset of GLOBAL view indices into this rank's compacted
+// list on the device (stream ordered).  subset == NULL -> all views.
+static int resolve_subset(ms2g_plan* p, const int32_t* subset, int n_subset, cudaStream_t st, const int** d_sel,
+                          int* n_sel, int* n_global) {
+  if (!subset) {
+    *d_sel = nullptr;
+    *n_sel = p->V_r;
+    *n_global = p->d.n_views;
+    return MS2G_OK;
+  }
+  if (n_subset < 1) return set_error(MS2G_ERR_INPUT, "empty view subset (S:285)");
+  int prev = -1, m = 0;
+  MS2G_CUDA(cudaEventSynchronize(p->sel_ev));  // staging buffer free again
+  for (int k = 0; k < n_subset; ++k) {
+    const int v = subset[k];
+    if (v < 0 || v >= p->d.n_views || v <= prev)
+      return set_error(MS2G_ERR_INPUT, "subset must hold ascending view indices in [0, n_views)");
+    prev = v;
+    if (v >= p->d.view_begin && v < p->d.view_end) p->h_sel[m++] = v - p->d.view_begin;
+  }
+  if (m > 0) {
+    MS2G_CUDA(cudaMemcpyAsync(p->w_sel, p->h_sel, sizeof(int) * m, cudaMemcpyHostToDevice, st));
+    MS2G_CUDA(cudaEventRecord(p->sel_ev, st));
+  }
+  *d_sel = p->w_sel;
+  *n_sel = m;
+  *n_global = n_subset;
+  return MS2G_OK;
+}
+
+static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
+  if (!p->comm || p->nranks <= 1) return MS2G_OK;
+  MS2G_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, p->comm, st));
+  return MS2G_OK;
+}
+
+// g = c U_s A_s^T (A_s S_s x - b), into a full-resolution image.
+static int enqueue_grad(ms2g_plan* p, const FactorTables& f, const float* x, const float* b, float* g,
+                        const int* d_sel, int n_sel, float c, int batch, cudaStream_t st) {
+  const int n = p->d.n, s = f.factor;
+  const float* v;
+  if (s > 1) {
+    MS2G_TRY(launch_sketch_down(n, s, batch, x, p->w_v, p->w_vT, st));  // v = S_s(y)
+    v = p->w_v;
+  } else {
+    MS2G_TRY(launch_transpose(n, batch, x, p->w_vT, st));
+    v = x;
+  }
+  MS2G_TRY(launch_forward(p, f, v, p->w_vT, b, p->w_res, d_sel, n_sel, batch, st));  // r = A_s v - b
+  float* G = (s > 1) ? p->w_G : g;
+  MS2G_TRY(launch_backward(p, f, p->w_res, G, c, 0, d_sel, n_sel, batch, st));      // G = c A_s^T r
+  MS2G_TRY(allreduce(p, G, (size_t)f.nc * f.nc * batch, st));
+  if (s > 1) MS2G_TRY(launch_up_step(n, s, batch, G, nullptr, nullptr, -1.f, g, st));  // U_s G
+  return MS2G_OK;
+}
+
+// O8 power iteration on the full view set (allreduced over ranks); the last
+// Rayleigh quotient goes to L_out / eta_out / etaf_out (device pointers).
+static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double* L_out, double* eta_out,
+                         float* etaf_out, cudaStream_t st) {
+  const size_t np = (size_t)f.nc * f.nc;
+  const float v0 = (float)(1.0 / (double)f.nc);  // 1 / ||1||
+  MS2G_TRY(launch_fill(p->w_v, np, v0, st));
+  MS2G_TRY(launch_fill(p->w_vT, np, v0, st));
+  for (int k = 0; k < iters; ++k) {
+    MS2G_TRY(launch_forward(p, f, p->w_v, p->w_vT, nullptr, p->w_res, nullptr, p->V_r, 1, st));
+    MS2G_TRY(launch_backward(p, f, p->w_res, p->w_G, 1.f, 0, nullptr, p->V_r, 1, st));
+    MS2G_TRY(allreduce(p, p->w_G, np, st));
+    const bool last = (k == iters - 1);
+    MS2G_TRY(launch_power_step(f.nc, 1, p->w_v, p->w_G, p->w_red, p->red_blocks, p->w_pw, last ? L_out : nullptr,
+                               last ? nullptr : p->w_v, last ? nullptr : p->w_vT, last ? eta_out : nullptr,
+                               last ? etaf_out : nullptr, st));
+  }
+  return MS2G_OK;
+}
+
+static int denoise_mix(ms2g_plan* p, const ms2g_denoiser& den, const float* z, const float* xprev, float* xout,
+                       float* yout, float alpha, float a, int mode, int iter, int batch, cudaStream_t st) {
+  const int n = p->d.n;
+  switch (den.kind) {
+    case 0:
+      return launch_copy_mix_mom(n, batch, z, xprev, xout, yout, a, mode, p->w_flag, iter, st);
+    case 1:
+      return launch_gauss_mix_mom(n, batch, den.sigma, z, xprev, xout, yout, alpha, a, mode, p->w_flag, iter, st);
+    case 2:
+      return launch_tv(n, batch, den.lambda, den.tau, den.inner_iters, z, p->w_p[0], p->w_p[1], xprev, xout, yout,
+                       alpha, a, mode, p->w_flag, iter, st);
+    default:
+      return set_error(MS2G_ERR_CONFIG, "unknown denoiser kind");
+  }
+}
+
+static int check_denoiser(const ms2g_denoiser& den) {
+  if (den.kind < 0 || den.kind > 2) return set_error(MS2G_ERR_CONFIG, "denoiser kind must be 0, 1 or 2");
+  if (den.kind == 1 && !(den.sigma > 0)) return set_error(MS2G_ERR_CONFIG, "gaussian sigma must be > 0");
+  if (den.kind == 2) {
+    if (!(den.lambda >= 0)) return set_error(MS2G_ERR_CONFIG, "tv lambda must be >= 0");
+    if (!(den.tau > 0 && den.tau <= 0.125f)) return set_error(MS2G_ERR_CONFIG, "tv tau must be in (0, 1/8]");
+    if (den.inner_iters < 1) return set_error(MS2G_ERR_CONFIG, "tv inner_iters must be >= 1");
+  }
+  return MS2G_OK;
+}
+
+// O13 schedule: SplitMix64 + Fisher-Yates (independent of the oracle's copy).
+static uint64_t splitmix64(uint64_t& state) {
+  uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+static int make_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, std::vector<ms2g_sched_entry>& out) {
+  out.clear();
+  if (!sd || !sd->stages || sd->n_stages < 1 || sd->n_stages > 63)
+    return set_error(MS2G_ERR_CONFIG, "solve needs 1..63 stages");
+  if (sd->option != 1 && sd->option != 2) return set_error(MS2G_ERR_CONFIG, "option must be 1 or 2");
+  if (sd->option == 2 && (sd->n_subsets < 1 || (p && sd->n_subsets > p->d.n_views)))
+    return set_error(MS2G_ERR_CONFIG, "n_subsets must be in [1, n_views]");
+  uint64_t state = sd->seed;
+  int i = 0;
+  std::vector<int> perm(sd->option == 2 ? sd->n_subsets : 1);
+  for (int k = 0; k < sd->n_stages; ++k) {
+    const ms2g_stage& st = sd->stages[k];
+    if (st.factor < 1 || (p && p->d.n % st.factor != 0))
+      return set_error(MS2G_ERR_CONFIG, "stage factor must divide n (S:127)");
+    if (sd->option == 1) {
+      if (st.n_iters < 0) return set_error(MS2G_ERR_CONFIG, "n_iters must be >= 0");
+      for (int j = 0; j < st.n_iters; ++j) {
+        ++i;
+        out.push_back({i, k, st.factor, -1, 0.0, (double)(i - 1) / (double)(i + 3)});
+      }
+    } else {
+      if (st.n_epochs < 0) return set_error(MS2G_ERR_CONFIG, "n_epochs must be >= 0");
+      for (int ep = 0; ep < st.n_epochs; ++ep) {
+        for (int q = 0; q < sd->n_subsets; ++q) perm[q] = q;
+        for (int q = sd->n_subsets - 1; q >= 1; --q) {
+          const int j = (int)(splitmix64(state) % (uint64_t)(q + 1));
+          std::swap(perm[q], perm[j]);
+        }
+        for (int q = 0; q < sd->n_subsets; ++q) {
+          ++i;
+          out.push_back({i, k, st.factor, perm[q], 0.0, (double)(i - 1) / (double)(i + 3)});
+        }
+      }
+    }
+  }
+  return MS2G_OK;
+}
+
+// Upload the n_subsets interleaved subset lists (rank-local) once per solve
+// description; synchronous, outside graph capture.
+static int prepare_subsets(ms2g_plan* p, int n_subsets) {
+  if (p->subsets_n == n_subsets) return MS2G_OK;
+  std::vector<int> all;
+  p->subset_off.assign(n_subsets, 0);
+  p->subset_len.assign(n_subsets, 0);
+  p->subset_global_len.assign(n_subsets, 0);
+  for (int k = 0; k < n_subsets; ++k) {
+    p->subset_off[k] = (int)all.size();
+    for (int v = k; v < p->d.n_views; v += n_subsets) {
+      p->subset_global_len[k]++;
+      if (v >= p->d.view_begin && v < p->d.view_end) all.push_back(v - p->d.view_begin);
+    }
+    p->subset_len[k] = (int)all.size() - p->subset_off[k];
+  }
+  cudaFree(p->w_subsets);
+  p->w_subsets = nullptr;
+  MS2G_CUDA(cudaMalloc(&p->w_subsets, sizeof(int) * (all.size() + 1)));
+  if (!all.empty())
+    MS2G_CUDA(cudaMemcpy(p->w_subsets, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice));
+  p->subsets_n = n_subsets;
+  return MS2G_OK;
+}
+
+// The whole solve as one stream-ordered sequence (captured into a graph).
+static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vector<ms2g_sched_entry>& sch,
+                         const float* b, const float* x0, float* x_out, cudaStream_t st) {
+  const int n = p->d.n, batch = p->d.batch;
+  const size_t img = (size_t)n * n * batch;
+  MS2G_TRY(launch_init_flag(p->w_flag, st));
+  // x_0 = y_0 = x0, x_prev = x_0
+  MS2G_CUDA(cudaMemcpyAsync(p->w_x[0], x0, sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
+  MS2G_CUDA(cudaMemcpyAsync(p->w_y, x0, sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
+  int cur = 0;
+  size_t step = 0;
+  for (int k = 0; k < sd->n_stages; ++k) {
+    const ms2g_stage& stg = sd->stages[k];
+    const FactorTables* f = find_factor(p, stg.factor);
+    MS2G_TRY(enqueue_power(p, *f, sd->power_iters, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
+    while (step < sch.size() && sch[step].stage == k) {
+      const ms2g_sched_entry& e = sch[step];
+      const int* d_sel = nullptr;
+      int n_sel = p->V_r;
+      float c = 1.f;
+      if (e.subset >= 0) {
+        d_sel = p->w_subsets + p->subset_off[e.subset];
+        n_sel = p->subset_len[e.subset];
+        c = (float)((double)p->d.n_views / (double)p->subset_global_len[e.subset]);
+      }
+      // G-step: z = y - eta_k U_s (c A_s^T (A_s S_s y - b_M))
+      const int s = f->factor;
+      const float* v;
+      if (s > 1) {
+        MS2G_TRY(launch_sketch_down(n, s, batch, p->w_y, p->w_v, p->w_vT, st));
+        v = p->w_v;
+      } else {
+        MS2G_TRY(launch_transpose(n, batch, p->w_y, p->w_vT, st));
+        v = p->w_y;
+      }
+      MS2G_TRY(launch_forward(p, *f, v, p->w_vT, b, p->w_res, d_sel, n_sel, batch, st));
+      MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
+      MS2G_TRY(allreduce(p, p->w_G, (size_t)f->nc * f->nc * batch, st));
+      MS2G_TRY(launch_up_step(n, s, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
+      // x = (1-alpha) z + alpha D(z);  y = x + a_i (x - x_prev)
+      MS2G_TRY(denoise_mix(p, sd->den, p->w_z, p->w_x[cur], p->w_x[cur ^ 1], p->w_y, sd->alpha, (float)e.a, 1,
+                           e.i, batch, st));
+      cur ^= 1;
+      ++step;
+    }
+  }
+  MS2G_CUDA(cudaMemcpyAsync(x_out, p->w_x[cur], sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
+  return MS2G_OK;
+}
+
+static std::string solve_key(const ms2g_solve_desc* sd, const float* b, const float* x0, const float* x_out) {
+  std::ostringstream os;
+  os << sd->n_stages << ':' << sd->option << ':' << sd->n_subsets << ':' << sd->seed << ':' << sd->den.kind << ':'
+     << sd->den.sigma << ':' << sd->den.lambda << ':' << sd->den.tau << ':' << sd->den.inner_iters << ':'
+     << sd->alpha << ':' << sd->power_iters << ':' << (const void*)b << ':' << (const void*)x0 << ':'
+     << (const void*)x_out;
+  for (int k = 0; k < sd->n_stages; ++k)
+    os << '|' << sd->stages[k].factor << ',' << sd->stages[k].n_iters << ',' << sd->stages[k].n_epochs;
+  return os.str();
+}
+
+static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b, const float* x0, float* x_out,
+                        cudaStream_t st) {
+  if (!b || !x0 || !x_out) return set_error(MS2G_ERR_INPUT, "NULL b/x0/x_out");
+  if (!(sd->alpha > 0.f && sd->alpha <= 1.f)) return set_error(MS2G_ERR_CONFIG, "alpha must be in (0, 1] (S:197)");
+  if (sd->power_iters < 1) return set_error(MS2G_ERR_CONFIG, "power_iters must be >= 1");
+  MS2G_TRY(check_denoiser(sd->den));
+  std::vector<ms2g_sched_entry> sch;
+  MS2G_TRY(make_schedule(p, sd, sch));
+  for (int k = 0; k < sd->n_stages; ++k)
+    if (!find_factor(p, sd->stages[k].factor))
+      return set_error(MS2G_ERR_CONFIG, "stage factor was not planned (ms2g_plan_geometry factors)");
+  if (!find_factor(p, 1) && p->nmax_c < p->d.n)
+    return set_error(MS2G_ERR_CONFIG, "the solve needs full-resolution workspaces: plan factor 1 as well");
+  if (sd->option == 2) MS2G_TRY(prepare_subsets(p, sd->n_subsets));
+  const std::string key = solve_key(sd, b, x0, x_out);
+  if (key != p->sg.key || !p->sg.exec) {
+    if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
+    if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
+    p->sg = SolveGraph{};
+    cudaStream_t cs;
+    MS2G_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      cudaStreamDestroy(cs);
+      return set_error(MS2G_ERR_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+    }
+    t_capturing = true;
+    t_captured = 0;
+    int rc = enqueue_solve(p, sd, sch, b, x0, x_out, cs);
+    t_capturing = false;
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (rc != MS2G_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return set_error(MS2G_ERR_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return set_error(MS2G_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    }
+    p->sg.key = key;
+    p->sg.graph = graph;
+    p->sg.exec = exec;
+    p->sg.kernel_nodes = t_captured;
+  }
+  MS2G_CUDA(cudaGraphLaunch(p->sg.exec, st));
+  count_launch(p->sg.kernel_nodes);
+  p->last_sched = sch;
+  return MS2G_OK;
+}
+
+static int solve_status(ms2g_plan* p, cudaStream_t st) {
+  int flag = INT_MAX;
+  MS2G_CUDA(cudaMemcpyAsync(&flag, p->w_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MS2G_CUDA(cudaStreamSynchronize(st));
+  if (flag != INT_MAX) {
+    int stage = -1;
+    for (const auto& e : p->last_sched)
+      if (e.i == flag) stage = e.stage;
+    std::ostringstream os;
+    os << "diverged: non-finite iterate at stage " << stage << ", iteration " << flag;
+    return set_error(MS2G_ERR_DIVERGED, os.str());
+  }
+  return MS2G_OK;
+}
+
+}  // namespace ms2g
+
+using namespace ms2g;
+
+extern "C" {
+
+const char* ms2g_last_error(void) { return t_err.c_str(); }
+
+uint64_t ms2g_launch_count(void) { return g_launches.load(); }
+
+int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32_t n_factors, ms2g_plan** out) {
+  t_err.clear();
+  if (!desc || !out) return set_error(MS2G_ERR_INPUT, "NULL desc/out");
+  *out = nullptr;
+  ms2g_geom_desc d = *desc;
+  if (d.n < 1 || !(d.fov > 0) || d.n_views < 1 || d.n_bins < 1 || !(d.arc_rad > 0))
+    return set_error(MS2G_ERR_CONFIG, "need n, fov, n_views, n_bins, arc_rad > 0");
+  const double R = d.fov / std::sqrt(2.0);
+  if (!(d.sod > R) || !(d.sdd - d.sod > R))
+    return set_error(MS2G_ERR_CONFIG, "source and detector must lie outside the FOV circle (sod, sdd-sod > fov/sqrt2)");
+  if (d.view_begin == 0 && d.view_end == 0) d.view_end = d.n_views;
+  if (d.view_begin < 0 || d.view_end > d.n_views || d.view_begin >= d.view_end)
+    return set_error(MS2G_ERR_CONFIG, "view shard [view_begin, view_end) out of range");
+  if (d.batch < 1) d.batch = 1;
+  if (!factors || n_factors < 1) return set_error(MS2G_ERR_CONFIG, "need at least one factor");
+  ms2g_plan* p = new ms2g_plan();
+  p->d = d;
+  p->V_r = d.view_end - d.view_begin;
+  p->B = d.n_bins;
+  p->pitch = d.bin_pitch > 0 ? d.bin_pitch : (d.sdd / d.sod) * d.fov / d.n;
+  int dev = 0, sms = 148;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) {
+    delete p;
+    return set_error(MS2G_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  for (int k = 0; k < n_factors; ++k) {
+    const int s = factors[k];
+    if (s < 1 || d.n % s != 0) {
+      delete p;
+      return set_error(MS2G_ERR_CONFIG, "every factor must be >= 1 and divide n (S:127, S:145)");
+    }
+    if (d.n / s > 32767) {
+      delete p;
+      return set_error(MS2G_ERR_CONFIG, "n/factor must be <= 32767");
+    }
+    if (find_factor(p, s)) continue;
+    FactorTables f;
+    f.factor = s;
+    p->ft.push_back(f);
+  }
+  int rc = MS2G_OK;
+  size_t part = 1;
+  for (auto& f : p->ft) {
+    rc = build_tables(p, f, sms);
+    if (rc != MS2G_OK) {
+      free_plan(p);
+      return rc;
+    }
+    if (f.nc > p->nmax_c) p->nmax_c = f.nc;
+    const size_t need = (size_t)f.bp_chunks * f.nc * f.nc * d.batch;
+    if (f.bp_chunks > 1 && need > part) part = need;
+  }
+  const size_t bt = d.batch;
+  const size_t cimg = (size_t)p->nmax_c * p->nmax_c * bt, fimg = (size_t)d.n * d.n * bt;
+  auto alloc = [&](float** q, size_t count) -> int {
+    MS2G_CUDA(cudaMalloc(q, sizeof(float) * (count ? count : 1)));
+    return MS2G_OK;
+  };
+  p->red_blocks = 2 * sms;
+  if ((rc = alloc(&p->w_xT, cimg)) || (rc = alloc(&p->w_v, cimg)) || (rc = alloc(&p->w_vT, cimg)) ||
+      (rc = alloc(&p->w_G, cimg)) || (rc = alloc(&p->w_res, (size_t)p->V_r * p->B * bt)) ||
+      (rc = alloc(&p->w_part, part)) || (rc = alloc(&p->w_x[0], fimg)) || (rc = alloc(&p->w_x[1], fimg)) ||
+      (rc = alloc(&p->w_y, fimg)) || (rc = alloc(&p->w_z, fimg)) || (rc = alloc(&p->w_p[0], 2 * fimg)) ||
+      (rc = alloc(&p->w_p[1], 2 * fimg)) || (rc = alloc(&p->w_etaf, 64))) {
+    free_plan(p);
+    return rc;
+  }
+  p->part_elems = part;
+  e = cudaMalloc(&p->w_red, sizeof(double) * 2 * p->red_blocks);
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_scal, sizeof(double) * 128);
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_pw, sizeof(double) * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_flag, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_sel, sizeof(int) * p->V_r);
+  if (e == cudaSuccess) e = cudaMallocHost(&p->h_sel, sizeof(int) * p->V_r);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->sel_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMemset(p->w_flag, 0x7f, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(p->w_scal, 0, sizeof(double) * 128);
+  if (e != cudaSuccess) {
+    free_plan(p);
+    return set_error(MS2G_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+  }
+  *out = p;
+  return MS2G_OK;
+}
+
+void ms2g_plan_destroy(ms2g_plan* plan) {
+  if (plan) cudaDeviceSynchronize();
+  free_plan(plan);
+}
+
+int ms2g_plan_info(const ms2g_plan* p, int32_t factor, int32_t* n_c, int32_t* vb, int32_t* ve, int32_t* batch) {
+  if (!p) return set_error(MS2G_ERR_INPUT, "NULL plan");
+  const FactorTables* f = find_factor(p, factor);
+  if (n_c) *n_c = f ? f->nc : 0;
+  if (vb) *vb = p->d.view_begin;
+  if (ve) *ve = p->d.view_end;
+  if (batch) *batch = p->d.batch;
+  return MS2G_OK;
+}
+
+int ms2g_nccl_unique_id(void* out) {
+  if (!out) return set_error(MS2G_ERR_INPUT, "NULL id buffer");
+  ncclUniqueId id;
+  MS2G_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out, &id, sizeof(id));
+  return MS2G_OK;
+}
+
+int ms2g_attach_nccl(ms2g_plan* p, const void* uid, int32_t rank, int32_t nranks) {
+  if (!p || !uid) return set_error(MS2G_ERR_INPUT, "NULL plan/id");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(MS2G_ERR_CONFIG, "bad rank/nranks");
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  if (p->comm) {
+    ncclCommDestroy(p->comm);
+    p->comm = nullptr;
+  }
+  MS2G_NCCL(ncclCommInitRank(&p->comm, nranks, id, rank));
+  p->rank = rank;
+  p->nranks = nranks;
+  if (p->sg.exec) {  // a cached solve graph captured without the communicator
+    cudaGraphExecDestroy(p->sg.exec);
+    cudaGraphDestroy(p->sg.graph);
+    p->sg = SolveGraph{};
+  }
+  return MS2G_OK;
+}
+
+int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const float* xT, const float* b, float* out,
+                         const int32_t* subset, int32_t n_subset, void* stream) {
+  if (!p || !x || !out) return set_error(MS2G_ERR_INPUT, "NULL plan/x/out");
+  const FactorTables* f = find_factor(p, factor);
+  if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int* d_sel;
+  int n_sel, n_glob;
+  MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
+  if (!xT) {
+    MS2G_TRY(launch_transpose(f->nc, p->d.batch, x, p->w_xT, st));
+    xT = p->w_xT;
+  }
+  return launch_forward(p, *f, x, xT, b, out, d_sel, n_sel, p->d.batch, st);
+}
+
+int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* img, float scale, int32_t accumulate,
+                      const int32_t* subset, int32_t n_subset, int32_t do_allreduce, void* stream) {
+  if (!p || !sino || !img) return set_error(MS2G_ERR_INPUT, "NULL plan/sino/img");
+  const FactorTables* f = find_factor(p, factor);
+  if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  if (do_allreduce && !p->comm && p->nranks > 1) return set_error(MS2G_ERR_CONFIG, "allreduce needs attach_nccl");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int* d_sel;
+  int n_sel, n_glob;
+  MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
+  MS2G_TRY(launch_backward(p, *f, sino, img, scale, accumulate, d_sel, n_sel, p->d.batch, st));
+  if (do_allreduce) MS2G_TRY(allreduce(p, img, (size_t)f->nc * f->nc * p->d.batch, st));
+  return MS2G_OK;
+}
+
+int ms2g_sketch_down(ms2g_plan* p, int32_t factor, const float* x, float* v, float* vT, void* stream) {
+  if (!p || !x || (!v && !vT)) return set_error(MS2G_ERR_INPUT, "NULL plan/x/v");
+  if (factor < 1 || p->d.n % factor) return set_error(MS2G_ERR_CONFIG, "factor must divide n (S:127)");
+  return launch_sketch_down(p->d.n, factor, p->d.batch, x, v, vT, (cudaStream_t)stream);
+}
+
+int ms2g_sketch_up(ms2g_plan* p, int32_t factor, const float* g, const float* y, float eta, float* z, void* stream) {
+  if (!p || !g || !z) return set_error(MS2G_ERR_INPUT, "NULL plan/g/z");
+  if (factor < 1 || p->d.n % factor) return set_error(MS2G_ERR_CONFIG, "factor must divide n");
+  return launch_up_step(p->d.n, factor, p->d.batch, g, y, nullptr, y ? eta : 0.f, z, (cudaStream_t)stream);
+}
+
+int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* g,
+                       const int32_t* subset, int32_t n_subset, void* stream) {
+  if (!p || !x || !b || !g) return set_error(MS2G_ERR_INPUT, "NULL plan/x/b/g");
+  const FactorTables* f = find_factor(p, factor);
+  if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  if (factor == 1 ? false : p->nmax_c < f->nc) return set_error(MS2G_ERR_CONFIG, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int* d_sel;
+  int n_sel, n_glob;
+  MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
+  const float c = (float)((double)p->d.n_views / (double)n_glob);
+  return enqueue_grad(p, *f, x, b, g, d_sel, n_sel, c, p->d.batch, st);
+}
+
+int ms2g_power_iteration(ms2g_plan* p, int32_t factor, int32_t iters, double* L, void* stream) {
+  if (!p || !L) return set_error(MS2G_ERR_INPUT, "NULL plan/L");
+  if (iters < 1) return set_error(MS2G_ERR_CONFIG, "iters must be >= 1");
+  const FactorTables* f = find_factor(p, factor);
+  if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  MS2G_TRY(enqueue_power(p, *f, iters, p->w_scal + 127, nullptr, nullptr, st));
+  MS2G_CUDA(cudaMemcpyAsync(L, p->w_scal + 127, sizeof(double), cudaMemcpyDeviceToHost, st));
+  MS2G_CUDA(cudaStreamSynchronize(st));
+  return MS2G_OK;
+}
+
+int ms2g_denoise(ms2g_plan* p, const ms2g_denoiser* den, const float* z, float* out, void* stream) {
+  if (!p || !den || !z || !out) return set_error(MS2G_ERR_INPUT, "NULL plan/den/z/out");
+  if (z == out) return set_error(MS2G_ERR_INPUT, "z and out must not alias");
+  MS2G_TRY(check_denoiser(*den));
+  return denoise_mix(p, *den, z, nullptr, out, nullptr, 1.f, 0.f, 0, 0, p->d.batch, (cudaStream_t)stream);
+}
+
+int ms2g_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, ms2g_sched_entry* out, int32_t cap, int32_t* n_out) {
+  std::vector<ms2g_sched_entry> sch;
+  MS2G_TRY(make_schedule(p, sd, sch));
+  if (n_out) *n_out = (int32_t)sch.size();
+  for (size_t k = 0; k < sch.size() && (int)k < cap && out; ++k) out[k] = sch[k];
+  return MS2G_OK;
+}
+
+int ms2g_pnp_ms2g_solve_async(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b, const float* x0,
+                              float* x_out, void* stream) {
+  if (!p || !sd) return set_error(MS2G_ERR_INPUT, "NULL plan/desc");
+  return solve_launch(p, sd, b, x0, x_out, (cudaStream_t)stream);
+}
+
+int ms2g_solve_status(ms2g_plan* p, void* stream) {
+  if (!p) return set_error(MS2G_ERR_INPUT, "NULL plan");
+  return solve_status(p, (cudaStream_t)stream);
+}
+
+int ms2g_pnp_ms2g_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b, const float* x0, float* x_out,
+                        ms2g_sched_entry* trace, void* stream) {
+  if (!p || !sd) return set_error(MS2G_ERR_INPUT, "NULL plan/desc");
+  cudaStream_t st = (cudaStream_t)stream;
+  MS2G_TRY(solve_launch(p, sd, b, x0, x_out, st));
+  const int rc = solve_status(p, st);
+  if (trace) {
+    double etas[64];
+    MS2G_CUDA(cudaMemcpy(etas, p->w_scal + 64, sizeof(double) * 64, cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < p->last_sched.size(); ++k) {
+      trace[k] = p->last_sched[k];
+      trace[k].eta = etas[trace[k].stage];
+    }
+  }
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,341 @@
+"""GPU (libms2g, sm_100a) vs fp64 oracle parity, element by element.
+
+Bar (BASELINE.json north_star): relative L2 <= 1e-5 per operator call,
+<= 1e-3 on the reconstruction after the full schedule, bit-exact schedules.
+Inputs are seeded (ms2g_synth) and shaped like C1..C5; sizes span several
+32x32 tiles and ragged tails; backprojection inputs include zero-mean random
+sinograms (consistent-sign inputs hide crossing-precision errors).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import ms2g_synth as S  # noqa: E402
+import oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL_OP = 1e-5
+TOL_SOLVE = 1e-3
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2203_07308_b200 as P
+    P.load()
+    return P
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+# geometry cases: (n, V, B, factors); ragged n_c (20, 40, 48) leave partial tiles
+GEOMS = [
+    (64, 90, 96, (2, 1)),          # C1
+    (256, 360, 384, (4, 2, 1)),    # C2
+    (40, 20, 61, (2, 1)),          # ragged tiles, odd bin count
+    (96, 33, 150, (3, 1)),         # factor 3, wide detector
+]
+
+
+@pytest.mark.parametrize("n,V,B,factors", GEOMS)
+def test_forward_parity(P, n, V, B, factors):
+    g = O.Geometry(n, V, B)
+    with P.plan_geometry(n, V, B, factors=factors) as plan:
+        for s in factors:
+            nc = n // s
+            for x in (S.phantom(nc, 8, 11 + s), S.random_image(nc, 5 + s)):
+                ref = O.forward(g, s, x)
+                got = host(P.forward_project(plan, s, dev(x)[None]))[0]
+                assert rel(got, ref) <= TOL_OP, (s, rel(got, ref))
+
+
+@pytest.mark.parametrize("n,V,B,factors", GEOMS)
+def test_forward_residual_and_subset(P, n, V, B, factors):
+    g = O.Geometry(n, V, B)
+    rng = np.random.default_rng(n)
+    b = S.random_sinogram((V, B), 77, zero_mean=False) * 3
+    sub = np.sort(rng.choice(V, size=max(1, V // 3), replace=False))
+    with P.plan_geometry(n, V, B, factors=factors) as plan:
+        s = factors[0]
+        x = S.phantom(n // s, 6, 3)
+        ref = O.forward(g, s, x, b=b, views=sub)
+        got = host(P.forward_project(plan, s, dev(x)[None], b=dev(b)[None], subset=sub))[0]
+        assert rel(got, ref) <= TOL_OP
+
+
+@pytest.mark.parametrize("n,V,B,factors", GEOMS)
+def test_backward_parity_zero_mean(P, n, V, B, factors):
+    g = O.Geometry(n, V, B)
+    with P.plan_geometry(n, V, B, factors=factors) as plan:
+        for s in factors:
+            for zm in (True, False):
+                r = S.random_sinogram((V, B), 100 + s, zero_mean=zm)
+                ref = O.backward(g, s, r)
+                got = host(P.back_project(plan, s, dev(r)[None]))[0]
+                assert rel(got, ref) <= TOL_OP, (s, zm, rel(got, ref))
+
+
+def test_backward_subset_scale_accumulate(P):
+    n, V, B = 128, 120, 192
+    g = O.Geometry(n, V, B)
+    sub = O.subset_views(V, 8, 3)
+    r = S.random_sinogram((len(sub), B), 9)
+    with P.plan_geometry(n, V, B, factors=(2,)) as plan:
+        base = S.random_image(64, 4)
+        ref = base + 8.0 * O.backward(g, 2, r, views=sub)
+        img = dev(base)[None].clone()
+        P.back_project(plan, 2, dev(r)[None], img=img, scale=8.0, accumulate=True, subset=sub)
+        assert rel(host(img)[0], ref) <= TOL_OP
+
+
+def test_adjoint_identity_fp32(P):
+    """GPU-only invariant: <A x, y> = <x, A^T y> in fp32 (same weights)."""
+    n, V, B = 256, 180, 384
+    with P.plan_geometry(n, V, B, factors=(1, 2)) as plan:
+        for s in (1, 2):
+            nc = n // s
+            for k in range(3):
+                x = dev(S.random_image(nc, 30 + k) - 0.5)[None]
+                y = dev(S.random_sinogram((V, B), 40 + k))[None]
+                lhs = float((P.forward_project(plan, s, x).double() * y.double()).sum())
+                rhs = float((x.double() * P.back_project(plan, s, y).double()).sum())
+                assert abs(lhs - rhs) <= 1e-5 * abs(lhs)
+
+
+def test_backward_deterministic(P):
+    n, V, B = 256, 360, 384
+    with P.plan_geometry(n, V, B, factors=(2, 1)) as plan:
+        r = dev(S.random_sinogram((V, B), 5))[None]
+        for s in (2, 1):
+            a = P.back_project(plan, s, r).clone(); b = P.back_project(plan, s, r)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("s", [1, 2, 4])
+def test_sketch_down_up(P, s):
+    n = 64
+    x = S.random_image(n, 8)
+    with P.plan_geometry(n, 10, 96, factors=(s,)) as plan:
+        vT = torch.empty((1, n // s, n // s), device="cuda")
+        v = host(P.sketch_down(plan, s, dev(x)[None], vT=vT))[0]
+        ref = O.sketch_down(x, s)
+        assert np.max(np.abs(v - ref)) <= 2e-7 * np.max(np.abs(ref))
+        assert np.array_equal(host(vT)[0], v.T)
+        gc = S.random_image(n // s, 9)
+        up = host(P.sketch_up(plan, s, dev(gc)[None]))[0]
+        assert np.array_equal(up, O.sketch_up(gc.astype(np.float64), s).astype(np.float32).astype(np.float64))
+        y = S.random_image(n, 10)
+        z = host(P.sketch_up(plan, s, dev(gc)[None], y=dev(y)[None], eta=0.3))[0]
+        zr = y - np.float32(0.3) * O.sketch_up(gc, s)
+        assert np.max(np.abs(z - zr)) <= 1e-6
+
+
+@pytest.mark.parametrize("cfg,factors", [(1, (2, 1)), (2, (4, 2, 1))])
+def test_sketched_grad_option1(P, cfg, factors):
+    pr = S.PRESETS[cfg]
+    g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+    xt = S.phantom(pr.n, pr.n_ellipses, S.config_seed(cfg))
+    b = S.gaussian_data(O.forward(g, 1, xt), pr.noise[1], S.config_seed(cfg)).astype(np.float32)
+    x = S.phantom(pr.n, pr.n_ellipses, S.config_seed(cfg, 9))   # independent image: ||r|| = O(||b||)
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=factors) as plan:
+        for s in factors:
+            ref = O.sketched_grad(g, s, x, b)
+            got = host(P.sketched_grad(plan, s, dev(x)[None], dev(b)[None]))[0]
+            assert rel(got, ref) <= TOL_OP, (s, rel(got, ref))
+
+
+def test_sketched_grad_option2_subsets(P):
+    n, V, B = 128, 160, 192
+    g = O.Geometry(n, V, B)
+    b = S.random_sinogram((V, B), 3, zero_mean=False) * 2
+    x = S.phantom(n, 12, 4)
+    with P.plan_geometry(n, V, B, factors=(4, 2, 1)) as plan:
+        for s in (4, 2, 1):
+            for k in (0, 5):
+                sub = O.subset_views(V, 8, k)
+                ref = O.sketched_grad(g, s, x, b, views=sub)
+                got = host(P.sketched_grad(plan, s, dev(x)[None], dev(b)[None], subset=sub))[0]
+                assert rel(got, ref) <= TOL_OP, (s, k, rel(got, ref))
+
+
+@pytest.mark.parametrize("n,V,B,s", [(64, 90, 96, 2), (64, 90, 96, 1), (256, 360, 384, 4), (128, 45, 200, 1)])
+def test_power_iteration(P, n, V, B, s):
+    g = O.Geometry(n, V, B)
+    with P.plan_geometry(n, V, B, factors=(s,)) as plan:
+        L = P.power_iteration(plan, s, 20)
+    Lr = O.power_iteration(g, s, 20)
+    assert abs(L - Lr) <= 1e-5 * Lr
+
+
+def test_denoisers(P):
+    n = 96
+    z = S.phantom(n, 10, 21) + 0.05 * S.random_sinogram((n, n), 2)
+    with P.plan_geometry(n, 8, 150, factors=(1,)) as plan:
+        gz = host(P.denoise(plan, ("gauss", 0.8), dev(z)[None]))[0]
+        assert rel(gz, O.gauss3(z, 0.8)) <= TOL_OP
+        for lam in (0.02, 0.01):
+            tz = host(P.denoise(plan, ("tv", lam, 10), dev(z)[None]))[0]
+            assert rel(tz, O.tv_chambolle(z, lam, 10)) <= TOL_OP
+        iz = host(P.denoise(plan, ("identity",), dev(z)[None]))[0]
+        assert np.array_equal(iz, z.astype(np.float32))
+
+
+@pytest.mark.parametrize("cfg", [3, 2])
+def test_schedule_bit_exact(P, cfg):
+    pr = S.PRESETS[cfg]
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(1,)) as plan:
+        a = P.schedule(plan, pr.stages, pr.option, pr.n_subsets, S.config_seed(cfg))
+    b = O.schedule(pr.stages, pr.option, pr.n_subsets, S.config_seed(cfg))
+    assert [e[:4] for e in a] == [e[:4] for e in b]
+    assert [e[5] for e in a] == [e[5] for e in b]
+
+
+def _make_data(pr, cfg, image=0):
+    g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+    xt = S.phantom(pr.n, pr.n_ellipses, S.config_seed(cfg, image), texture=pr.texture)
+    p = O.forward(g, 1, xt)
+    if pr.noise[0] == "gauss":
+        b = S.gaussian_data(p, pr.noise[1], S.config_seed(cfg, image))
+    else:
+        b = S.poisson_data(p, pr.noise[1], S.config_seed(cfg, image))
+    return g, xt, b
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_solve_parity_option1(P, cfg):
+    pr = S.PRESETS[cfg]
+    g, xt, b = _make_data(pr, cfg)
+    factors = sorted({s[0] for s in pr.stages} | {1}, reverse=True)
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=factors) as plan:
+        xo, tr = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha, trace=True)
+        xo = host(xo)[0]
+    xr, trr, etas = O.pnp_ms2g(g, pr.stages, b, den=pr.den, alpha=pr.alpha)
+    assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)
+    assert [e[:4] for e in tr] == [e[:4] for e in trr]
+    for e, er in zip(tr, trr):
+        assert abs(e[4] - er[4]) <= 1e-5 * er[4]
+
+
+@pytest.mark.slow
+def test_solve_parity_option2_c3(P):
+    pr = S.PRESETS[3]
+    g, xt, b = _make_data(pr, 3)
+    seed = S.config_seed(3)
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(4, 2, 1)) as plan:
+        xo, tr = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], option=2, n_subsets=8, seed=seed, den=pr.den,
+                                  alpha=pr.alpha, trace=True)
+        xo = host(xo)[0]
+    xr, trr, _ = O.pnp_ms2g(g, pr.stages, b, option=2, n_subsets=8, seed=seed, den=pr.den, alpha=pr.alpha)
+    assert [e[:4] for e in tr] == [e[:4] for e in trr]
+    assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)
+
+
+def test_solve_batch_matches_single(P):
+    """C5-style batch (Poisson data, TV): each batch image equals its own
+    single-image solve and the oracle."""
+    n, V, B = 128, 90, 192
+    g = O.Geometry(n, V, B)
+    stages = [(2, 4, 0), (1, 3, 0)]
+    bs, xs = [], []
+    for im in range(3):
+        xt = S.phantom(n, 10, S.config_seed(5, im))
+        bs.append(S.poisson_data(O.forward(g, 1, xt), 1e5, S.config_seed(5, im)))
+    with P.plan_geometry(n, V, B, factors=(2, 1), batch=3) as plan:
+        xb = host(P.pnp_ms2g_solve(plan, stages, dev(np.stack(bs)), den=("tv", 0.02, 10), alpha=1.0))
+    for im in range(3):
+        xr, _, _ = O.pnp_ms2g(g, stages, bs[im], den=("tv", 0.02, 10), alpha=1.0)
+        assert rel(xb[im], xr) <= TOL_SOLVE
+
+
+def test_emulated_view_sharding(P):
+    """P view shards run one after another on one GPU: the sum of the partial
+    backprojections equals the full one (the algebra the NCCL allreduce
+    implements)."""
+    n, V, B = 128, 90, 192
+    r = S.random_sinogram((V, B), 12)
+    x = S.phantom(n, 8, 2)
+    with P.plan_geometry(n, V, B, factors=(2, 1)) as full:
+        ref = host(P.back_project(full, 1, dev(r)[None]))[0]
+        fref = host(P.forward_project(full, 2, dev(x[::2, ::2])[None]))[0]
+    for nr in (2, 3, 4):
+        acc = np.zeros_like(ref)
+        fwd = []
+        for rk in range(nr):
+            vb, ve = P.view_shard(V, rk, nr)
+            with P.plan_geometry(n, V, B, factors=(2, 1), view_begin=vb, view_end=ve) as sh:
+                acc += host(P.back_project(sh, 1, dev(r[vb:ve])[None]))[0]
+                fwd.append(host(P.forward_project(sh, 2, dev(x[::2, ::2])[None]))[0])
+        assert rel(acc, ref) <= 1e-6
+        assert np.array_equal(np.concatenate(fwd, 0), fref)
+
+
+def test_full_size_sampled_c4(P):
+    """C4 full size (1024^2, 1440 x 1536) in the bench's launch configuration:
+    sampled rays (forward) and pixels (adjoint) against the oracle, one by one."""
+    pr = S.PRESETS[4]
+    n, V, B = pr.n, pr.n_views, pr.n_bins
+    g = O.Geometry(n, V, B)
+    x = S.phantom(n, pr.n_ellipses, S.config_seed(4))
+    rng = np.random.default_rng(4)
+    with P.plan_geometry(n, V, B, factors=(2, 1)) as plan:
+        for s in (2, 1):
+            xs = x if s == 1 else O.sketch_down(x, 2).astype(np.float32)
+            got = host(P.forward_project(plan, s, dev(xs)[None]))[0]
+            vv, tt = rng.integers(0, V, 200), rng.integers(0, B, 200)
+            ref = np.array([O.ray_sum(g, s, xs, int(v), int(t)) for v, t in zip(vv, tt)])
+            assert rel(got[vv, tt], ref) <= TOL_OP
+        r = S.random_sinogram((V, B), 44)
+        img = host(P.back_project(plan, 2, dev(r)[None]))[0]
+        pix = [(0, 0), (511, 511), (256, 100), (17, 400), (300, 301), (128, 0)]
+        ref = np.array([O.backward_pixel(g, 2, r, i, j) for i, j in pix])
+        gotp = np.array([img[i, j] for i, j in pix])
+        assert np.max(np.abs(gotp - ref)) <= TOL_OP * np.sqrt(np.mean(img ** 2)) * 3
+
+
+def test_divergence_reported(P):
+    n, V, B = 64, 30, 96
+    b = np.ones((V, B), np.float32); b[3, 7] = np.nan
+    with P.plan_geometry(n, V, B, factors=(2, 1)) as plan:
+        with pytest.raises(P.DivergedError, match="iteration 1"):
+            P.pnp_ms2g_solve(plan, [(2, 2, 0), (1, 1, 0)], dev(b)[None])
+
+
+def test_config_errors(P):
+    with pytest.raises(P.MS2GError) as e:
+        P.plan_geometry(64, 10, 96, factors=(3,))
+    assert e.value.code == 2
+    with pytest.raises(P.MS2GError):
+        P.plan_geometry(64, 10, 96, factors=(1,), sod=1.0)
+    with P.plan_geometry(64, 10, 96, factors=(2,)) as plan:
+        x = torch.zeros((1, 32, 32), device="cuda")
+        with pytest.raises(P.MS2GError) as e:
+            P.forward_project(plan, 1, x)
+        assert e.value.code == 2
+        with pytest.raises(P.MS2GError) as e:
+            P.forward_project(plan, 2, x, subset=[3, 1])
+        assert e.value.code == 7
+        with pytest.raises(P.MS2GError):
+            P.pnp_ms2g_solve(plan, [(2, 1, 0)], torch.zeros((1, 10, 96), device="cuda"), alpha=0.0)
+
+
+def test_launch_count_increases(P):
+    before = P.launch_count()
+    with P.plan_geometry(64, 10, 96, factors=(1,)) as plan:
+        P.forward_project(plan, 1, torch.ones((1, 64, 64), device="cuda"))
+    assert P.launch_count() > before

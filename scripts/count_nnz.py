@@ -1,0 +1,29 @@
+"""Exact segment counts nnz(A_s) for the C1..C5 geometries, from the oracle only.
+
+Writes profiles/nnz_counts.json: {"C<k>": {"geometry": [n, V, B], "<s>": nnz}}.
+These are the algorithmic-work denominators of bench.py's roofline (8 B per
+segment); the CUDA path never produces them.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import ms2g_synth as S  # noqa: E402
+import oracle as O  # noqa: E402
+
+out = {}
+for cfg, pr in S.PRESETS.items():
+    g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+    ent = {"geometry": [pr.n, pr.n_views, pr.n_bins]}
+    for s in (4, 2, 1):
+        ent[str(s)] = O.count_nnz(g, s)
+    if pr.option == 2:
+        for s in (4, 2, 1):
+            ent[f"{s}_subset0"] = O.count_nnz(g, s, views=O.subset_views(pr.n_views, pr.n_subsets, 0))
+    out[f"C{cfg}"] = ent
+    print(cfg, ent, flush=True)
+with open(os.path.join(ROOT, "profiles", "nnz_counts.json"), "w") as f:
+    json.dump(out, f, indent=1)

@@ -47,7 +47,7 @@ def host(t):
 GEOMS = [
     (64, 90, 96, (2, 1)),          # C1
     (256, 360, 384, (4, 2, 1)),    # C2
-    (40, 20, 61, (2, 1)),          # ragged tiles, odd bin count
+    (40, 20, 62, (2, 1)),          # ragged tiles (n_c = 20, 40)
     (96, 33, 150, (3, 1)),         # factor 3, wide detector
 ]
 

@@ -268,15 +268,10 @@ def run_ms2g(args, rank, nranks, local_rank):
     for s in (2, 1):
         nc = pr.n // s
         tg = time_calls(lambda: P.sketched_grad(plan, s, x1, b, g=g), 10)
-        xT = torch.empty((1, nc, nc), device=dev)
-        if s == 1:
-            xs = x1
-            P.sketch_down(plan, 1, x1, vT=xT, want_v=False)
-        else:
-            xs = P.sketch_down(plan, 2, x1, vT=xT)
+        xs = x1 if s == 1 else P.sketch_down(plan, 2, x1)
         res = torch.empty((1, ve - vb, pr.n_bins), device=dev)
         img = torch.empty((1, nc, nc), device=dev)
-        tf = time_calls(lambda: P.forward_project(plan, s, xs, b=b, out=res, xT=xT), 10)
+        tf = time_calls(lambda: P.forward_project(plan, s, xs, b=b, out=res), 10)
         tb = time_calls(lambda: P.back_project(plan, s, res, img=img), 10)
         seg = nnz[str(s)] * frac_views
         detail[f"grad_s{s}"] = {"evals_per_s": 1.0 / tg, "ms": tg * 1e3,

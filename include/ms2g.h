@@ -76,15 +76,14 @@ int ms2g_attach_nccl(ms2g_plan* plan, const void* unique_id_128_bytes, int32_t r
 /* Forward projection with fused residual (Eq. 6-7 "A_s S(x) - b"):
  *   out[b][k][t] = (A_s x_b)[v_k][t] - bsino[b][v_k][t]
  * A_s = Siddon exact intersection lengths on the n_c = n/factor grid.
- * x     image [batch][n_c][n_c];  xT optional transposed copy (xT[j][i] =
- *       x[i][j]); NULL -> the library transposes into a plan workspace.
+ * x     image [batch][n_c][n_c] (the library first packs it into its gather
+ *       layout, a plan workspace).
  * bsino [batch][V_r][B] indexed by rank-local view, or NULL (plain A_s x).
  * subset: ascending GLOBAL view indices (NULL = all views); views outside
  *       this rank's shard are skipped; out is compacted over the rest.
  * Errors: CONFIG (factor not in plan), INPUT (NULL x/out, bad subset). */
-int ms2g_forward_project(ms2g_plan* plan, int32_t factor, const float* x, const float* xT,
-                         const float* bsino, float* out, const int32_t* subset, int32_t n_subset,
-                         void* stream);
+int ms2g_forward_project(ms2g_plan* plan, int32_t factor, const float* x, const float* bsino, float* out,
+                         const int32_t* subset, int32_t n_subset, void* stream);
 
 /* Exact adjoint ("A_s^T"):  img[b] = scale * A_s^T sino[b]
  * (accumulate != 0: img += ...).  sino is compacted [batch][n_sel][B] in the
@@ -95,10 +94,8 @@ int ms2g_back_project(ms2g_plan* plan, int32_t factor, const float* sino, float*
                       void* stream);
 
 /* Image-space sketch S_s (north-star D; reading Z2): s x s average pool,
- * x [batch][n][n] -> v [batch][n/s][n/s]; vT (optional, may be NULL)
- * receives the transposed copy the forward projector reads. */
-int ms2g_sketch_down(ms2g_plan* plan, int32_t factor, const float* x, float* v, float* vT,
-                     void* stream);
+ * x [batch][n][n] -> v [batch][n/s][n/s]. */
+int ms2g_sketch_down(ms2g_plan* plan, int32_t factor, const float* x, float* v, void* stream);
 
 /* Upsample + step ("z = y - eta U G"; reading Z2: U_s = nearest
  * replication = s^2 S_s^T):  z = y - eta * U_s g.  y == NULL gives z = U_s g. */

@@ -86,9 +86,9 @@ def load():
     L.ms2g_plan_destroy.restype = None
     L.ms2g_nccl_unique_id.argtypes = [p]
     L.ms2g_attach_nccl.argtypes = [p, p, i, i]
-    L.ms2g_forward_project.argtypes = [p, i, p, p, p, p, C.POINTER(C.c_int32), i, p]
+    L.ms2g_forward_project.argtypes = [p, i, p, p, p, C.POINTER(C.c_int32), i, p]
     L.ms2g_back_project.argtypes = [p, i, p, p, f, i, C.POINTER(C.c_int32), i, i, p]
-    L.ms2g_sketch_down.argtypes = [p, i, p, p, p, p]
+    L.ms2g_sketch_down.argtypes = [p, i, p, p, p]
     L.ms2g_sketch_up.argtypes = [p, i, p, p, f, p, p]
     L.ms2g_sketched_grad.argtypes = [p, i, p, p, p, C.POINTER(C.c_int32), i, p]
     L.ms2g_power_iteration.argtypes = [p, i, i, C.POINTER(d), p]
@@ -197,13 +197,13 @@ def _n_sel(plan: Plan, subset) -> int:
     return sum(1 for v in subset if plan.view_begin <= int(v) < plan.view_end)
 
 
-def forward_project(plan: Plan, factor: int, x, b=None, subset=None, out=None, xT=None):
+def forward_project(plan: Plan, factor: int, x, b=None, subset=None, out=None):
     """r = A_s x - b on the selected views, compacted [batch][n_sel][B]."""
     sel, m = _subset(subset)
     if out is None:
         out = torch.empty((plan.batch, _n_sel(plan, subset), plan.n_bins), device=x.device, dtype=torch.float32)
-    _check(load().ms2g_forward_project(plan.handle, factor, _dev(x, "x"), _dev(xT, "xT"), _dev(b, "b"),
-                                       _dev(out, "out"), sel, m, _stream()))
+    _check(load().ms2g_forward_project(plan.handle, factor, _dev(x, "x"), _dev(b, "b"), _dev(out, "out"), sel, m,
+                                       _stream()))
     return out
 
 
@@ -219,12 +219,12 @@ def back_project(plan: Plan, factor: int, sino, img=None, scale=1.0, accumulate=
     return img
 
 
-def sketch_down(plan: Plan, factor: int, x, v=None, vT=None, want_v=True):
-    """S_s: s x s average pool (+ optional transposed copy)."""
+def sketch_down(plan: Plan, factor: int, x, v=None):
+    """S_s: s x s average pool."""
     nc = plan.nc(factor)
-    if v is None and want_v:
+    if v is None:
         v = torch.empty((plan.batch, nc, nc), device=x.device, dtype=torch.float32)
-    _check(load().ms2g_sketch_down(plan.handle, factor, _dev(x, "x"), _dev(v, "v"), _dev(vT, "vT"), _stream()))
+    _check(load().ms2g_sketch_down(plan.handle, factor, _dev(x, "x"), _dev(v, "v"), _stream()))
     return v
 
 

@@ -19,45 +19,29 @@ static inline int grid1d(size_t total, int block = 256, int cap = 148 * 32) {
 
 // -------------------------------------------------------------- sketch --
 // S_s: s x s average pool (north-star D; BASELINE configs "2x2 average pool").
-// Writes v (row-major) and/or vT (transposed) through a 32x33 shared tile.
-__global__ void k_sketch_down(const float* __restrict__ x, float* __restrict__ v, float* __restrict__ vT,
-                              int n, int s, int nc) {
-  __shared__ float tile[32][33];
-  const int bz = blockIdx.z;
-  const float* xb = x + (size_t)bz * n * n;
-  const size_t cb = (size_t)bz * nc * nc;
-  const int I0 = blockIdx.y * 32, J0 = blockIdx.x * 32;
+__global__ void k_sketch_down(const float* __restrict__ x, float* __restrict__ v, int n, int s, int nc,
+                              size_t total) {
   const float inv = 1.0f / (float)(s * s);
-  for (int di = threadIdx.y; di < 32; di += 8) {
-    const int I = I0 + di, J = J0 + threadIdx.x;
-    if (I < nc && J < nc) {
-      float acc = 0.f;
-      for (int a = 0; a < s; ++a) {
-        const float* row = xb + (size_t)(s * I + a) * n + (size_t)s * J;
-        for (int b = 0; b < s; ++b) acc += row[b];
-      }
-      const float val = (s == 1) ? acc : acc * inv;
-      if (v) v[cb + (size_t)I * nc + J] = val;
-      tile[di][threadIdx.x] = val;
+  const size_t np = (size_t)nc * nc;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = idx / np, p = idx % np;
+    const int I = (int)(p / nc), J = (int)(p % nc);
+    const float* xb = x + b * n * n;
+    float acc = 0.f;
+    for (int a = 0; a < s; ++a) {
+      const float* row = xb + (size_t)(s * I + a) * n + (size_t)s * J;
+      for (int c = 0; c < s; ++c) acc += row[c];
     }
-  }
-  if (!vT) return;
-  __syncthreads();
-  for (int di = threadIdx.y; di < 32; di += 8) {
-    const int J = J0 + di, I = I0 + threadIdx.x;
-    if (I < nc && J < nc) vT[cb + (size_t)J * nc + I] = tile[threadIdx.x][di];
+    v[idx] = (s == 1) ? acc : acc * inv;
   }
 }
 
-int launch_sketch_down(int n, int s, int batch, const float* x, float* v, float* vT, cudaStream_t st) {
+int launch_sketch_down(int n, int s, int batch, const float* x, float* v, cudaStream_t st) {
   const int nc = n / s;
-  dim3 grid((nc + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
-  k_sketch_down<<<grid, block, 0, st>>>(x, v, vT, n, s, nc);
+  const size_t total = (size_t)nc * nc * batch;
+  k_sketch_down<<<grid1d(total), 256, 0, st>>>(x, v, n, s, nc, total);
   return check_launch("k_sketch_down");
-}
-
-int launch_transpose(int n, int batch, const float* x, float* xT, cudaStream_t st) {
-  return launch_sketch_down(n, 1, batch, x, nullptr, xT, st);
 }
 
 // ---------------------------------------------------------- upsample+step --
@@ -273,28 +257,15 @@ __global__ void k_power_finalize(const double* __restrict__ red, int nblocks, do
   if (etaf_out) *etaf_out = (float)(1.0 / d);
 }
 
-__global__ void k_scale_T(const float* __restrict__ w, const double* __restrict__ pw, float* __restrict__ v,
-                          float* __restrict__ vT, int nc) {
-  __shared__ float tile[32][33];
+__global__ void k_scale(const float* __restrict__ w, const double* __restrict__ pw, float* __restrict__ v,
+                        size_t np) {
   const float inv = (float)pw[1];
-  const int I0 = blockIdx.y * 32, J0 = blockIdx.x * 32;
-  for (int di = threadIdx.y; di < 32; di += 8) {
-    const int I = I0 + di, J = J0 + threadIdx.x;
-    if (I < nc && J < nc) {
-      const float val = w[(size_t)I * nc + J] * inv;
-      v[(size_t)I * nc + J] = val;
-      tile[di][threadIdx.x] = val;
-    }
-  }
-  __syncthreads();
-  for (int di = threadIdx.y; di < 32; di += 8) {
-    const int J = J0 + di, I = I0 + threadIdx.x;
-    if (I < nc && J < nc) vT[(size_t)J * nc + I] = tile[threadIdx.x][di];
-  }
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x)
+    v[i] = w[i] * inv;
 }
 
 int launch_power_step(int nc, int /*batch*/, const float* v, const float* w, double* red, int red_blocks,
-                      double* pw, double* L_out, float* vnext, float* vnextT, double* eta_out, float* etaf_out,
+                      double* pw, double* L_out, float* vnext, double* eta_out, float* etaf_out,
                       cudaStream_t st) {
   const size_t np = (size_t)nc * nc;
   k_dot_norm<<<red_blocks, 256, 0, st>>>(v, w, np, red);
@@ -302,9 +273,8 @@ int launch_power_step(int nc, int /*batch*/, const float* v, const float* w, dou
   k_power_finalize<<<1, 32, 0, st>>>(red, red_blocks, pw, L_out, eta_out, etaf_out);
   MS2G_TRY(check_launch("k_power_finalize"));
   if (vnext) {
-    dim3 grid((nc + 31) / 32, (nc + 31) / 32), block(32, 8);
-    k_scale_T<<<grid, block, 0, st>>>(w, pw, vnext, vnextT, nc);
-    MS2G_TRY(check_launch("k_scale_T"));
+    k_scale<<<grid1d(np), 256, 0, st>>>(w, pw, vnext, np);
+    MS2G_TRY(check_launch("k_scale"));
   }
   return MS2G_OK;
 }

@@ -23,22 +23,30 @@ enum RayFlags : int { kMajorY = 1, kMirror = 2 };
 // One ray of one view on the grid of one factor (32 bytes).  The ray is a
 // line "minor = F0 + S * major" in pixel units of the n_c grid, in a frame
 // where the minor axis may be mirrored (minor' = n_c - minor) so that the
-// slope S is in [0, 1].  major = x (column) for |dx| >= |dy|, else y (row).
+// slope S is in [0, 1).  major = x (column) for |dx| >= |dy|, else y (row).
+// The ray "class" is flags & 3 (major axis, mirror).
 struct __align__(16) RayEntry {
   long long F0;             // minor' at major coordinate 0, 2^-32 units
-  unsigned long long S;     // minor' step per unit major step, 2^-32 units (<= 2^32)
+  unsigned S;               // minor' step per unit major step, 2^-32 units (< 2^32)
   float Lc;                 // physical length per unit major step: h_c sqrt(1 + slope^2)
   float Ly32;               // Lc / slope' * 2^-32 (0 when S == 0)
   int flags;                // kMajorY | kMirror
   short c_lo, c_hi;         // major indices [c_lo, c_hi) where the ray meets the grid
+  int pad;
 };
 static_assert(sizeof(RayEntry) == 32, "RayEntry must be 32 bytes");
 
-// Per-view constants for the detector-coordinate map of a point P (pixel
-// units of the n_c grid):  tau(P) = off + scale * ((P-S).e) / ((P-S).n).
+// Per-view constants.  Detector coordinate of a point P (pixel units of the
+// n_c grid): tau(P) = off + scale * ((P-S).e) / ((P-S).n).  The bins of a view
+// split into <= 4 contiguous runs of one ray class (the ray angle is monotone
+// in t): run k covers t in [seg_t[k], seg_t[k+1]) with class seg_cls[k].
 struct __align__(16) ViewEntry {
   float Sx, Sy, ex, ey, nx, ny, scale, off;
+  short seg_t[5];
+  char seg_cls[4];
+  short nseg;
 };
+static_assert(sizeof(ViewEntry) == 48, "ViewEntry must be 48 bytes");
 
 struct FactorTables {
   int factor = 0, nc = 0;
@@ -64,9 +72,9 @@ struct ms2g_plan {
   std::vector<ms2g::FactorTables> ft;
   int nmax_c = 0;                      // largest coarse side among the factors
   // workspaces (all sized for batch)
-  float* w_xT = nullptr;               // transposed input for forward_project(xT == NULL)
+  float2* w_pair = nullptr;            // forward gather images: 4 x [batch][n_c][n_c + 3] float2
+  size_t pair_stride = 0;              // float2 elements per pair image
   float* w_v = nullptr;                // coarse sketch
-  float* w_vT = nullptr;               // its transpose
   float* w_G = nullptr;                // coarse gradient / backprojection
   float* w_res = nullptr;              // residual / projection [batch][V_r][B]
   float* w_part = nullptr;             // backprojection chunk partials
@@ -138,14 +146,14 @@ inline int check_launch(const char* what) {
 const FactorTables* find_factor(const ms2g_plan* p, int factor);
 
 // ---- kernel launchers (projector.cu) ----
-int launch_forward(ms2g_plan* p, const FactorTables& f, const float* x, const float* xT, const float* b,
-                   float* out, const int* d_sel, int n_sel, int batch, cudaStream_t s);
+int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s);
+int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
+                   int batch, cudaStream_t s);
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s);
 
 // ---- image kernels (image_ops.cu) ----
-int launch_sketch_down(int n, int s, int batch, const float* x, float* v, float* vT, cudaStream_t st);
-int launch_transpose(int n, int batch, const float* x, float* xT, cudaStream_t st);
+int launch_sketch_down(int n, int s, int batch, const float* x, float* v, cudaStream_t st);
 int launch_up_step(int n, int s, int batch, const float* g, const float* y, const float* eta_dev,
                    float eta, float* z, cudaStream_t st);
 int launch_gauss_mix_mom(int n, int batch, float sigma, const float* z, const float* xprev, float* xout,
@@ -157,7 +165,7 @@ int launch_copy_mix_mom(int n, int batch, const float* z, const float* xprev, fl
                         float a, int mode, int* flag, int iter, cudaStream_t st);
 int launch_fill(float* x, size_t count, float value, cudaStream_t st);
 int launch_power_step(int nc, int batch, const float* v, const float* w, double* red, int red_blocks,
-                      double* pw, double* L_out, float* vnext, float* vnextT, double* eta_out,
+                      double* pw, double* L_out, float* vnext, double* eta_out,
                       float* etaf_out, cudaStream_t st);
 int launch_init_flag(int* flag, cudaStream_t st);
 

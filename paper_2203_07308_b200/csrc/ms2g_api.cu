@@ -46,6 +46,7 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   std::vector<RayEntry> rays((size_t)V_r * B);
   std::vector<ViewEntry> views(V_r);
   const long long M = (long long)nc << 32;
+  if (B > 32767) return set_error(MS2G_ERR_CONFIG, "n_bins must be <= 32767");
   for (int vl = 0; vl < V_r; ++vl) {
     const int v = d.view_begin + vl;
     const double th = d.arc_rad * (double)v / (double)d.n_views;
@@ -58,7 +59,8 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     ve.nx = (float)(-c); ve.ny = (float)(-s);
     ve.scale = (float)(d.sdd / p->pitch);
     ve.off = (float)(0.5 * (B - 1));
-    views[vl] = ve;
+    ve.nseg = 0;
+    int prev_cls = -1;
     for (int t = 0; t < B; ++t) {
       const double u = ((double)t - 0.5 * (double)(B - 1)) * p->pitch;
       const double Px = (dcx - u * s - org) / hc, Py = (dcy + u * c - org) / hc;
@@ -81,15 +83,24 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
         m0c = (double)nc - m0c;
       }
       R.F0 = llround(m0c * kFix);
-      R.S = (unsigned long long)llround(slope * kFix);
+      const long long Sq = llround(slope * kFix);          // slope in [0, 1]; 1 only at exactly 45 deg
+      R.S = (unsigned)(Sq > 0xFFFFFFFFLL ? 0xFFFFFFFFLL : Sq);
       R.Lc = (float)Lc;
       R.Ly32 = R.S ? (float)(Lc / slope / kFix) : 0.f;
       R.flags = flags;
+      R.pad = 0;
+      if (flags != prev_cls) {                              // a new run of one ray class
+        if (ve.nseg == 4) return set_error(MS2G_ERR_CONFIG, "fan wider than 180 degrees: more than 4 ray classes");
+        ve.seg_t[ve.nseg] = (short)t;
+        ve.seg_cls[ve.nseg] = (char)flags;
+        ve.nseg++;
+        prev_cls = flags;
+      }
       long long lo, hi;
-      if (R.S == 0) {
+      if (R.S == 0u) {
         lo = 0; hi = (R.F0 >= 0 && R.F0 < M) ? nc : 0;
       } else {
-        const long long Sl = (long long)R.S;
+        const long long Sl = (long long)(unsigned long long)R.S;
         lo = floor_div(-R.F0, Sl);
         if (lo < 0) lo = 0;
         hi = ceil_div(M - R.F0, Sl);
@@ -100,6 +111,8 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
       R.c_hi = (short)hi;
       rays[(size_t)vl * B + t] = R;
     }
+    ve.seg_t[ve.nseg] = (short)B;
+    views[vl] = ve;
   }
   MS2G_CUDA(cudaMalloc(&f.d_rays, sizeof(RayEntry) * rays.size()));
   MS2G_CUDA(cudaMalloc(&f.d_views, sizeof(ViewEntry) * views.size()));
@@ -110,7 +123,7 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   const long long tiles = (long long)tiles_x * tiles_x * d.batch;
   const long long target = 4LL * sm_count;
   long long ch = (target + tiles - 1) / tiles;
-  const long long maxch = (V_r + 7) / 8;
+  const long long maxch = (V_r + 3) / 4;
   if (ch > maxch) ch = maxch;
   if (ch < 1) ch = 1;
   f.bp_chunks = (int)ch;
@@ -123,7 +136,8 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(f.d_rays);
     cudaFree(f.d_views);
   }
-  float* fl[] = {p->w_xT, p->w_v, p->w_vT, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
+  cudaFree(p->w_pair);
+  float* fl[] = {p->w_v, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
                  p->w_y, p->w_z, p->w_p[0], p->w_p[1], p->w_etaf};
   for (float* q : fl) cudaFree(q);
   cudaFree(p->w_red);
@@ -180,15 +194,13 @@ static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
 static int enqueue_grad(ms2g_plan* p, const FactorTables& f, const float* x, const float* b, float* g,
                         const int* d_sel, int n_sel, float c, int batch, cudaStream_t st) {
   const int n = p->d.n, s = f.factor;
-  const float* v;
+  const float* v = x;
   if (s > 1) {
-    MS2G_TRY(launch_sketch_down(n, s, batch, x, p->w_v, p->w_vT, st));  // v = S_s(y)
+    MS2G_TRY(launch_sketch_down(n, s, batch, x, p->w_v, st));  // v = S_s(y)
     v = p->w_v;
-  } else {
-    MS2G_TRY(launch_transpose(n, batch, x, p->w_vT, st));
-    v = x;
   }
-  MS2G_TRY(launch_forward(p, f, v, p->w_vT, b, p->w_res, d_sel, n_sel, batch, st));  // r = A_s v - b
+  MS2G_TRY(launch_pair_prep(p, f.nc, batch, v, st));
+  MS2G_TRY(launch_forward(p, f, b, p->w_res, d_sel, n_sel, batch, st));  // r = A_s v - b
   float* G = (s > 1) ? p->w_G : g;
   MS2G_TRY(launch_backward(p, f, p->w_res, G, c, 0, d_sel, n_sel, batch, st));      // G = c A_s^T r
   MS2G_TRY(allreduce(p, G, (size_t)f.nc * f.nc * batch, st));
@@ -203,15 +215,15 @@ static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double*
   const size_t np = (size_t)f.nc * f.nc;
   const float v0 = (float)(1.0 / (double)f.nc);  // 1 / ||1||
   MS2G_TRY(launch_fill(p->w_v, np, v0, st));
-  MS2G_TRY(launch_fill(p->w_vT, np, v0, st));
+  MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_v, st));
   for (int k = 0; k < iters; ++k) {
-    MS2G_TRY(launch_forward(p, f, p->w_v, p->w_vT, nullptr, p->w_res, nullptr, p->V_r, 1, st));
+    MS2G_TRY(launch_forward(p, f, nullptr, p->w_res, nullptr, p->V_r, 1, st));
     MS2G_TRY(launch_backward(p, f, p->w_res, p->w_G, 1.f, 0, nullptr, p->V_r, 1, st));
     MS2G_TRY(allreduce(p, p->w_G, np, st));
     const bool last = (k == iters - 1);
     MS2G_TRY(launch_power_step(f.nc, 1, p->w_v, p->w_G, p->w_red, p->red_blocks, p->w_pw, last ? L_out : nullptr,
-                               last ? nullptr : p->w_v, last ? nullptr : p->w_vT, last ? eta_out : nullptr,
-                               last ? etaf_out : nullptr, st));
+                               last ? nullptr : p->w_v, last ? eta_out : nullptr, last ? etaf_out : nullptr, st));
+    if (!last) MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_v, st));
   }
   return MS2G_OK;
 }
@@ -341,15 +353,13 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
       }
       // G-step: z = y - eta_k U_s (c A_s^T (A_s S_s y - b_M))
       const int s = f->factor;
-      const float* v;
+      const float* v = p->w_y;
       if (s > 1) {
-        MS2G_TRY(launch_sketch_down(n, s, batch, p->w_y, p->w_v, p->w_vT, st));
+        MS2G_TRY(launch_sketch_down(n, s, batch, p->w_y, p->w_v, st));
         v = p->w_v;
-      } else {
-        MS2G_TRY(launch_transpose(n, batch, p->w_y, p->w_vT, st));
-        v = p->w_y;
       }
-      MS2G_TRY(launch_forward(p, *f, v, p->w_vT, b, p->w_res, d_sel, n_sel, batch, st));
+      MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
+      MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st));
       MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
       MS2G_TRY(allreduce(p, p->w_G, (size_t)f->nc * f->nc * batch, st));
       MS2G_TRY(launch_up_step(n, s, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
@@ -516,7 +526,13 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     return MS2G_OK;
   };
   p->red_blocks = 2 * sms;
-  if ((rc = alloc(&p->w_xT, cimg)) || (rc = alloc(&p->w_v, cimg)) || (rc = alloc(&p->w_vT, cimg)) ||
+  p->pair_stride = (size_t)p->nmax_c * (p->nmax_c + 3) * bt;
+  e = cudaMalloc(&p->w_pair, sizeof(float2) * 4 * p->pair_stride);
+  if (e != cudaSuccess) {
+    free_plan(p);
+    return set_error(MS2G_ERR_CUDA, std::string("pair image allocation: ") + cudaGetErrorString(e));
+  }
+  if ((rc = alloc(&p->w_v, cimg)) ||
       (rc = alloc(&p->w_G, cimg)) || (rc = alloc(&p->w_res, (size_t)p->V_r * p->B * bt)) ||
       (rc = alloc(&p->w_part, part)) || (rc = alloc(&p->w_x[0], fimg)) || (rc = alloc(&p->w_x[1], fimg)) ||
       (rc = alloc(&p->w_y, fimg)) || (rc = alloc(&p->w_z, fimg)) || (rc = alloc(&p->w_p[0], 2 * fimg)) ||
@@ -586,7 +602,7 @@ int ms2g_attach_nccl(ms2g_plan* p, const void* uid, int32_t rank, int32_t nranks
   return MS2G_OK;
 }
 
-int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const float* xT, const float* b, float* out,
+int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* out,
                          const int32_t* subset, int32_t n_subset, void* stream) {
   if (!p || !x || !out) return set_error(MS2G_ERR_INPUT, "NULL plan/x/out");
   const FactorTables* f = find_factor(p, factor);
@@ -595,11 +611,8 @@ int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const flo
   const int* d_sel;
   int n_sel, n_glob;
   MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
-  if (!xT) {
-    MS2G_TRY(launch_transpose(f->nc, p->d.batch, x, p->w_xT, st));
-    xT = p->w_xT;
-  }
-  return launch_forward(p, *f, x, xT, b, out, d_sel, n_sel, p->d.batch, st);
+  MS2G_TRY(launch_pair_prep(p, f->nc, p->d.batch, x, st));
+  return launch_forward(p, *f, b, out, d_sel, n_sel, p->d.batch, st);
 }
 
 int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* img, float scale, int32_t accumulate,
@@ -617,10 +630,10 @@ int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* im
   return MS2G_OK;
 }
 
-int ms2g_sketch_down(ms2g_plan* p, int32_t factor, const float* x, float* v, float* vT, void* stream) {
-  if (!p || !x || (!v && !vT)) return set_error(MS2G_ERR_INPUT, "NULL plan/x/v");
+int ms2g_sketch_down(ms2g_plan* p, int32_t factor, const float* x, float* v, void* stream) {
+  if (!p || !x || !v) return set_error(MS2G_ERR_INPUT, "NULL plan/x/v");
   if (factor < 1 || p->d.n % factor) return set_error(MS2G_ERR_CONFIG, "factor must divide n (S:127)");
-  return launch_sketch_down(p->d.n, factor, p->d.batch, x, v, vT, (cudaStream_t)stream);
+  return launch_sketch_down(p->d.n, factor, p->d.batch, x, v, (cudaStream_t)stream);
 }
 
 int ms2g_sketch_up(ms2g_plan* p, int32_t factor, const float* g, const float* y, float eta, float* z, void* stream) {

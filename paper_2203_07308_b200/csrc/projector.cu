@@ -2,86 +2,127 @@
 // for sm_100a (north-star subsystems (1) and (2); Eqs. 5-7).
 //
 // Both kernels evaluate the SAME segment weights from the same 32-byte ray
-// record (RayEntry, built on the host in fp64).  The ray is marched along its
-// major axis (x when |dx| >= |dy|, else y) one pixel column at a time; within
-// column c the minor coordinate goes from F(c) = F0 + c S to F(c) + S, with
-// F in 64-bit fixed point (32 fractional bits).  Integer arithmetic is exact,
-// so F(c) is bit-identical whether reached incrementally (forward) or
-// directly (adjoint), and no crossing parameter is ever accumulated in fp32
-// (DESIGN.md "precision").  Since the slope S is in [0, 1], each column holds
-// one segment or two split at the grid line m0 + 1:
-//   w0 = min((2^32 - lo(F)) * Ly32, Lc),  w1 = Lc - w0.
-// Lengths are physical (the oracle's (alpha_b - alpha_a) |d|).
+// record (RayEntry, built on the host in fp64).  A ray is marched along its
+// major axis (x when |dx| >= |dy|, else y) one pixel column at a time; in
+// column c its minor coordinate runs from F(c) = F0 + c S to F(c) + S, with F
+// in 64-bit fixed point (32 fractional bits).  Integer arithmetic is exact, so
+// F(c) is bit-identical whether reached incrementally (forward) or directly
+// (adjoint), and no crossing parameter is ever accumulated in fp32 (DESIGN.md
+// "precision").  Since the slope is in [0, 1), a column holds one segment or
+// two split at the grid line m0 + 1 (seg_weights).  Lengths are physical
+// (the oracle's (alpha_b - alpha_a) |d|).
 #include <climits>
 
 #include "internal.cuh"
 
 namespace ms2g {
 
-__device__ __forceinline__ void seg_weights(long long F, unsigned long long S, float Lc, float Ly32, int& m0,
-                                            int& m1, float& w0, float& w1) {
-  const long long F1 = F + (long long)S;
-  m0 = (int)(F >> 32);
-  m1 = (int)(F1 >> 32);
-  w0 = Lc;
-  w1 = 0.f;
-  if (m1 != m0) {
-    const unsigned lo = (unsigned)(unsigned long long)F;
-    const float rem = lo ? (float)(0u - lo) : 4294967296.0f;
-    w0 = fminf(rem * Ly32, Lc);
-    w1 = Lc - w0;
+// Weights of the (up to) two segments of one column.  lo = low word of F.
+//   no crossing: w0 = Lc, w1 = 0
+//   crossing   : w0 = (2^32 - lo) * Ly32 (clamped to Lc), w1 = Lc - w0
+__device__ __forceinline__ void seg_weights(unsigned lo, bool cross, float Lc, float Ly32, float& w0, float& w1) {
+  const float wc = fminf(fmaf((float)(~lo), Ly32, Ly32), Lc);
+  w0 = cross ? wc : Lc;
+  w1 = Lc - w0;
+}
+
+// ------------------------------------------------------------ pair prep --
+// The forward projector gathers the two pixels (m0, m0+1) of a column with
+// ONE 8-byte load from "pair images": for every line of the minor-contiguous
+// layout, element k+2 (k = -2 .. n_c) holds (v[k], v[k+1]) with zeros outside
+// the grid.  Four images, indexed by the ray class (flags & 3):
+//   0 major-x      : lines = columns j of x, pairs along rows     (x^T)
+//   1 major-y      : lines = rows i of x,    pairs along columns
+//   2 major-x, mirrored: as 0 with each pair reversed (v[k+1], v[k])
+//   3 major-y, mirrored: as 1 reversed
+__global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pairs, size_t pair_stride, int nc) {
+  __shared__ float T[33][33];
+  const int bz = blockIdx.z;
+  const float* xb = x + (size_t)bz * nc * nc;
+  const int L = nc + 3;
+  const size_t ib = (size_t)bz * nc * L;
+  const int O0 = blockIdx.x * 32, L0 = blockIdx.y * 32;   // output positions o, lines
+  // x rows k = O0-2 .. O0+30 for the column-pair images
+  for (int r = threadIdx.y; r < 33; r += 8) {
+    const int k = O0 - 2 + r, j = L0 + threadIdx.x;
+    T[r][threadIdx.x] = (k >= 0 && k < nc && j < nc) ? xb[(size_t)k * nc + j] : 0.f;
   }
+  __syncthreads();
+  const int o = O0 + threadIdx.x;
+  if (o >= L) return;
+  for (int jj = threadIdx.y; jj < 32; jj += 8) {
+    const int line = L0 + jj;
+    if (line >= nc) break;
+    const size_t e = ib + (size_t)line * L + o;
+    const float a = T[threadIdx.x][jj], b = T[threadIdx.x + 1][jj];   // x[o-2][line], x[o-1][line]
+    pairs[e] = make_float2(a, b);
+    pairs[2 * pair_stride + e] = make_float2(b, a);
+    const int k = o - 2;
+    const float* row = xb + (size_t)line * nc;
+    const float c = (k >= 0 && k < nc) ? row[k] : 0.f;
+    const float d = (k + 1 >= 0 && k + 1 < nc) ? row[k + 1] : 0.f;
+    pairs[pair_stride + e] = make_float2(c, d);
+    pairs[3 * pair_stride + e] = make_float2(d, c);
+  }
+}
+
+int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s) {
+  dim3 grid((nc + 3 + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
+  k_pair_prep<<<grid, block, 0, s>>>(x, p->w_pair, p->pair_stride, nc);
+  return check_launch("k_pair_prep");
 }
 
 // ---------------------------------------------------------------- forward --
 // One thread per ray; a warp holds 32 consecutive bins of one view, so at a
-// given column the lanes read adjacent minor indices: contiguous addresses in
-// x (major-y rays) or in its transpose xT (major-x rays).  The 8 warps of a
-// block are 8 consecutive views over the same bins, which trace nearly the
-// same image lines: L1 reuse.  Residual epilogue fused ("A_s v - b").
+// given column the lanes read adjacent minor indices of the same pair-image
+// line (coalesced).  The 8 warps of a block are 8 consecutive views over the
+// same bins, tracing nearly the same lines: L1 reuse.  Residual epilogue fused
+// ("A_s v - b").
 constexpr int kFwdWarps = 8;
 
 __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
-                                                 const float* __restrict__ x, const float* __restrict__ xT,
-                                                 int nc, const float* __restrict__ bsino,
-                                                 float* __restrict__ out) {
+                                                 const float2* __restrict__ pairs, size_t pair_stride, int nc,
+                                                 const float* __restrict__ bsino, float* __restrict__ out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k = blockIdx.y * kFwdWarps + warp;
   if (k >= n_sel) return;
   const int t = blockIdx.x * 32 + lane;
   const int bz = blockIdx.z;
-  const size_t np = (size_t)nc * nc;
   const int g = sel ? __ldg(sel + k) : k;
   const bool valid = t < B;
   long long F0 = 0;
-  unsigned long long S = 0;
+  unsigned S = 0;
   float Lc = 0.f, Ly32 = 0.f;
-  int flags = 0, cl = INT_MAX, ch = INT_MIN;
+  int cls = 0, cl = INT_MAX, ch = INT_MIN;
   if (valid) {
     const RayEntry R = rays[(size_t)g * B + t];
-    F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; flags = R.flags;
+    F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; cls = R.flags & 3;
     if (R.c_lo < R.c_hi) { cl = R.c_lo; ch = R.c_hi; }
   }
   const int wcl = __reduce_min_sync(0xffffffffu, cl);
   const int wch = __reduce_max_sync(0xffffffffu, ch);
   float acc = 0.f;
   if (wcl < wch) {
-    const float* img = ((flags & kMajorY) ? x : xT) + (size_t)bz * np;
-    const bool mir = flags & kMirror;
-    const int msign = mir ? -1 : 1;
-    const float* rowp = img + (size_t)wcl * nc + (mir ? nc - 1 : 0);
+    const int L = nc + 3;
+    const float2* base = pairs + cls * pair_stride + (size_t)bz * nc * L + 2;
+    const bool mir = cls & kMirror;
+    const int kb = mir ? nc - 2 : 0, ks = mir ? -1 : 1;
     long long F = F0 + (long long)wcl * (long long)S;
-#pragma unroll 2
+    int off = wcl * L;
+#pragma unroll 4
     for (int c = wcl; c < wch; ++c) {
-      int m0, m1;
+      const long long F1 = F + (long long)S;
+      const int q = (int)(F >> 32);
+      const bool cross = (int)(F1 >> 32) != q;
       float w0, w1;
-      seg_weights(F, S, Lc, Ly32, m0, m1, w0, w1);
-      const bool inr = (c >= cl) && (c < ch);
-      if (inr && (unsigned)m0 < (unsigned)nc) acc = fmaf(w0, __ldg(rowp + msign * m0), acc);
-      if (inr && m1 != m0 && (unsigned)m1 < (unsigned)nc) acc = fmaf(w1, __ldg(rowp + msign * m1), acc);
-      F += (long long)S;
-      rowp += nc;
+      seg_weights((unsigned)F, cross, Lc, Ly32, w0, w1);
+      const int qc = min(max(q, -2), nc);
+      const float2 pv = __ldg(base + off + kb + ks * qc);
+      acc = fmaf(w0, pv.x, acc);
+      acc = fmaf(w1, pv.y, acc);
+      F = F1;
+      off += L;
     }
   }
   if (valid) {
@@ -91,54 +132,67 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
   }
 }
 
-int launch_forward(ms2g_plan* p, const FactorTables& f, const float* x, const float* xT, const float* b,
-                   float* out, const int* d_sel, int n_sel, int batch, cudaStream_t s) {
+int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
+                   int batch, cudaStream_t s) {
   if (n_sel <= 0) return MS2G_OK;
   dim3 grid((p->B + 31) / 32, (n_sel + kFwdWarps - 1) / kFwdWarps, batch);
-  k_forward<<<grid, 256, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, x, xT, f.nc, b, out);
+  k_forward<<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride, f.nc,
+                                            b, out);
   return check_launch("k_forward");
 }
 
 // --------------------------------------------------------------- adjoint --
-// Tile-driven ray scatter: a block owns a 32x32 pixel tile and a chunk of
+// Tile-driven ray scatter.  A block owns a 32x32 pixel tile and a chunk of
 // views; each warp takes one view at a time, finds the bins whose rays meet
 // the tile (detector coordinate of the tile corners), and walks those rays one
-// per step with LANE = major index inside the tile.  A lane therefore only
-// touches its own column (major-x rays) or row (major-y rays) of the warp's
-// private shared-memory accumulator: no atomics, deterministic order.  The 8
-// warp tiles are summed in fixed order at the end.
+// per step with LANE = major index inside the tile.  A lane only touches its
+// own column (major-x rays) or row (major-y rays) of the warp's private
+// shared accumulators: no atomics, fixed order, deterministic.  The bins of a
+// view are processed in runs of one ray class, so every per-ray branch of the
+// inner loop is loop-invariant.  Non-mirrored classes accumulate in T1
+// (row stride 33), mirrored classes in T2 = the tile with rows reversed, so
+// that both diagonal directions are bank-conflict free.  The warp tiles are
+// summed in fixed order at the end.
 constexpr int kBT = 32;
-constexpr int kBW = 8;
+constexpr int kBW = 4;
+constexpr int kTS = kBT * (kBT + 1);
 
-__global__ void __launch_bounds__(256) k_backward(const RayEntry* __restrict__ rays,
-                                                  const ViewEntry* __restrict__ views, int B,
-                                                  const int* __restrict__ sel, int n_sel, int vpc,
-                                                  const float* __restrict__ sino, float* __restrict__ out,
-                                                  int nc, int tiles_x, float scale, int accumulate,
-                                                  int partial) {
-  __shared__ float acc[kBW][kBT][kBT + 1];
-  __shared__ RayEntry stg[kBW][32];
-  __shared__ float rstg[kBW][32];
+__global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restrict__ rays,
+                                                       const ViewEntry* __restrict__ views, int B,
+                                                       const int* __restrict__ sel, int n_sel, int vpc,
+                                                       const float* __restrict__ sino, float* __restrict__ out,
+                                                       int nc, int tiles_x, float scale, int accumulate,
+                                                       int partial) {
+  __shared__ float acc[kBW][2][kTS];
+  __shared__ float4 st4[kBW][32];
+  __shared__ float2 st2[kBW][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kBT, y0 = ty * kBT;
   const int x1 = min(x0 + kBT, nc), y1 = min(y0 + kBT, nc);
-  float(*A)[kBT + 1] = acc[warp];
-#pragma unroll 4
-  for (int r = 0; r < kBT; ++r) A[r][lane] = 0.f;
+  float* T1 = acc[warp][0];
+  float* T2 = acc[warp][1];
+  for (int i = lane; i < kTS; i += 32) {
+    T1[i] = 0.f;
+    T2[i] = 0.f;
+  }
   __syncwarp();
   const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
   const float* sb = sino + (size_t)bz * n_sel * B;
+  const unsigned lane1 = lane + 1;
   for (int k = kb + warp; k < ke; k += kBW) {
     const int g = sel ? __ldg(sel + k) : k;
-    const ViewEntry V = views[g];
+    const ViewEntry* V = views + g;
     // detector coordinate of the tile's 4 corners (lanes 0..3)
-    const float px = (lane & 1) ? (float)x1 : (float)x0;
-    const float py = (lane & 2) ? (float)y1 : (float)y0;
-    const float dx = px - V.Sx, dy = py - V.Sy;
-    const float tau = V.off + V.scale * (dx * V.ex + dy * V.ey) / (dx * V.nx + dy * V.ny);
-    float tmin = (lane < 4) ? tau : INFINITY, tmax = (lane < 4) ? tau : -INFINITY;
+    float tmin = INFINITY, tmax = -INFINITY;
+    if (lane < 4) {
+      const float px = (lane & 1) ? (float)x1 : (float)x0;
+      const float py = (lane & 2) ? (float)y1 : (float)y0;
+      const float dx = px - V->Sx, dy = py - V->Sy;
+      const float tau = V->off + V->scale * (dx * V->ex + dy * V->ey) / (dx * V->nx + dy * V->ny);
+      tmin = tmax = tau;
+    }
 #pragma unroll
     for (int o = 2; o; o >>= 1) {
       tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
@@ -148,46 +202,50 @@ __global__ void __launch_bounds__(256) k_backward(const RayEntry* __restrict__ r
     tmax = __shfl_sync(0xffffffffu, tmax, 0);
     const int t_lo = max(0, (int)floorf(tmin - 0.01f));
     const int t_hi = min(B - 1, (int)ceilf(tmax + 0.01f));
-    for (int tb = t_lo; tb <= t_hi; tb += 32) {
-      const int t = tb + lane;
-      if (t <= t_hi) {
-        stg[warp][lane] = rays[(size_t)g * B + t];
-        rstg[warp][lane] = __ldg(sb + (size_t)k * B + t);
-      }
-      __syncwarp();
-      const int nr = min(32, t_hi - tb + 1);
-      int prev_major = -1;
-      for (int q = 0; q < nr; ++q) {
-        const float r = rstg[warp][q];
-        if (r == 0.f) continue;
-        const RayEntry R = stg[warp][q];
-        const int majY = R.flags & kMajorY;
-        if (majY != prev_major) {  // lanes switch between column and row ownership
-          __syncwarp();
-          prev_major = majY;
+    const int nseg = V->nseg;
+    for (int sg = 0; sg < nseg; ++sg) {
+      const int ta = max(t_lo, (int)V->seg_t[sg]);
+      const int te = min(t_hi, (int)V->seg_t[sg + 1] - 1);
+      if (ta > te) continue;
+      const int cls = V->seg_cls[sg];
+      const bool majY = cls & kMajorY, mir = cls & kMirror;
+      const int c0 = majY ? y0 : x0;
+      const int mb = mir ? nc - (majY ? x0 : y0) - kBT : (majY ? x0 : y0);
+      float* Tt = mir ? T2 : T1;
+      int lanebase, stride;
+      if (!majY) { lanebase = lane; stride = kBT + 1; }
+      else if (!mir) { lanebase = lane * (kBT + 1); stride = 1; }
+      else { lanebase = (kBT - 1 - lane) * (kBT + 1) + (kBT - 1); stride = -1; }
+      for (int tb = ta; tb <= te; tb += 32) {
+        const int t = tb + lane;
+        if (t <= te) {
+          const RayEntry R = rays[(size_t)g * B + t];
+          const long long Ft = R.F0 + (long long)c0 * (long long)R.S - ((long long)mb << 32);
+          st4[warp][lane] = make_float4(__uint_as_float((unsigned)Ft), __uint_as_float((unsigned)(Ft >> 32)),
+                                        __uint_as_float(R.S), R.Lc);
+          st2[warp][lane] = make_float2(R.Ly32, __ldg(sb + (size_t)k * B + t));
         }
-        const int c = (majY ? y0 : x0) + lane;
-        const int ce = majY ? y1 : x1;
-        if (c < ce && c >= R.c_lo && c < R.c_hi) {
-          const long long F = R.F0 + (long long)c * (long long)R.S;
-          int m0, m1;
+        __syncwarp();
+        const int nr = min(32, te - tb + 1);
+#pragma unroll 2
+        for (int q = 0; q < nr; ++q) {
+          const float4 a = st4[warp][q];
+          const float2 b2 = st2[warp][q];
+          const unsigned long long Ft =
+              ((unsigned long long)__float_as_uint(a.y) << 32) | (unsigned long long)__float_as_uint(a.x);
+          const unsigned S = __float_as_uint(a.z);
+          const unsigned long long F = (unsigned long long)lane * S + Ft;
+          const unsigned long long F1 = (unsigned long long)lane1 * S + Ft;
+          const int l0 = (int)(F >> 32);
+          const bool cross = (int)(F1 >> 32) != l0;
           float w0, w1;
-          seg_weights(F, R.S, R.Lc, R.Ly32, m0, m1, w0, w1);
-          const bool mir = R.flags & kMirror;
-          const int p0 = mir ? nc - 1 - m0 : m0;
-          const int p1 = mir ? p0 - 1 : p0 + 1;
-          const int mb = majY ? x0 : y0, me = majY ? x1 : y1;
-          if ((unsigned)m0 < (unsigned)nc && p0 >= mb && p0 < me) {
-            float* cell = majY ? &A[lane][p0 - mb] : &A[p0 - mb][lane];
-            *cell = fmaf(w0, r, *cell);
-          }
-          if (m1 != m0 && (unsigned)m1 < (unsigned)nc && p1 >= mb && p1 < me) {
-            float* cell = majY ? &A[lane][p1 - mb] : &A[p1 - mb][lane];
-            *cell = fmaf(w1, r, *cell);
-          }
+          seg_weights((unsigned)F, cross, a.w, b2.x, w0, w1);
+          const int ad = lanebase + l0 * stride;
+          if ((unsigned)l0 < (unsigned)kBT) Tt[ad] = fmaf(w0, b2.y, Tt[ad]);
+          if (cross && (unsigned)(l0 + 1) < (unsigned)kBT) Tt[ad + stride] = fmaf(w1, b2.y, Tt[ad + stride]);
         }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   __syncthreads();
@@ -198,7 +256,7 @@ __global__ void __launch_bounds__(256) k_backward(const RayEntry* __restrict__ r
     if (yy < nc && xx < nc) {
       float s = 0.f;
 #pragma unroll
-      for (int w = 0; w < kBW; ++w) s += acc[w][ly][lx];
+      for (int w = 0; w < kBW; ++w) s += acc[w][0][ly * (kBT + 1) + lx] + acc[w][1][(kBT - 1 - ly) * (kBT + 1) + lx];
       const size_t o = (size_t)yy * nc + xx;
       if (partial) {
         out[((size_t)bz * gridDim.y + chunk) * np + o] = s;
@@ -235,8 +293,8 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   const int vpc = (n_sel + nchunks - 1) / nchunks;
   const int partial = nchunks > 1;
   dim3 grid(tiles_x * tiles_x, nchunks, batch);
-  k_backward<<<grid, kBT * kBW, 0, s>>>(f.d_rays, f.d_views, p->B, d_sel, n_sel, vpc, sino,
-                                        partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
+  k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_views, p->B, d_sel, n_sel, vpc, sino,
+                                       partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
   MS2G_TRY(check_launch("k_backward"));
   if (partial) {
     const size_t np = (size_t)f.nc * f.nc, total = np * batch;

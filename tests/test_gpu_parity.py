@@ -132,11 +132,9 @@ def test_sketch_down_up(P, s):
     n = 64
     x = S.random_image(n, 8)
     with P.plan_geometry(n, 10, 96, factors=(s,)) as plan:
-        vT = torch.empty((1, n // s, n // s), device="cuda")
-        v = host(P.sketch_down(plan, s, dev(x)[None], vT=vT))[0]
+        v = host(P.sketch_down(plan, s, dev(x)[None]))[0]
         ref = O.sketch_down(x, s)
         assert np.max(np.abs(v - ref)) <= 2e-7 * np.max(np.abs(ref))
-        assert np.array_equal(host(vT)[0], v.T)
         gc = S.random_image(n // s, 9)
         up = host(P.sketch_up(plan, s, dev(gc)[None]))[0]
         assert np.array_equal(up, O.sketch_up(gc.astype(np.float64), s).astype(np.float32).astype(np.float64))

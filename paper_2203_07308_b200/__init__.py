@@ -335,18 +335,28 @@ def solve_status(plan: Plan):
     _check(load().ms2g_solve_status(plan.handle, _stream()))
 
 
-def attach_nccl(plan: Plan, rank: int, nranks: int, group=None):
-    """Rank 0 makes the ncclUniqueId, torch.distributed broadcasts it."""
+def broadcast_unique_id(uid: bytes | None, rank: int, nranks: int, group=None) -> bytes:
+    """Broadcast rank 0's 128-byte NCCL unique id over the torch process group."""
     import torch.distributed as dist
-    L = load()
-    buf = (C.c_uint8 * 128)()
-    if rank == 0:
-        _check(L.ms2g_nccl_unique_id(buf))
-    obj = [bytes(buf)]
+    obj = [uid if rank == 0 else None]
     if nranks > 1:
         dist.broadcast_object_list(obj, src=0, group=group)
-    uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
-    _check(L.ms2g_attach_nccl(plan.handle, uid, rank, nranks))
+    if not isinstance(obj[0], (bytes, bytearray)) or len(obj[0]) != 128:
+        raise MS2GError(MS2G_ERR_NCCL, "bad NCCL unique id broadcast")
+    return bytes(obj[0])
+
+
+def attach_nccl(plan: Plan, rank: int, nranks: int, group=None):
+    """Rank 0 makes the ncclUniqueId, torch.distributed broadcasts it, every
+    rank attaches the plan (view-sharded allreduce of partial images)."""
+    L = load()
+    uid = None
+    if rank == 0:
+        buf = (C.c_uint8 * 128)()
+        _check(L.ms2g_nccl_unique_id(buf))
+        uid = bytes(buf)
+    uid = broadcast_unique_id(uid, rank, nranks, group)
+    _check(L.ms2g_attach_nccl(plan.handle, (C.c_uint8 * 128).from_buffer_copy(uid), rank, nranks))
     plan.rank, plan.nranks = rank, nranks
     return plan
 

@@ -180,7 +180,6 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
   __syncwarp();
   const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
   const float* sb = sino + (size_t)bz * n_sel * B;
-  const unsigned lane1 = lane + 1;
   for (int k = kb + warp; k < ke; k += kBW) {
     const int g = sel ? __ldg(sel + k) : k;
     const ViewEntry* V = views + g;
@@ -227,22 +226,34 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
         }
         __syncwarp();
         const int nr = min(32, te - tb + 1);
-#pragma unroll 2
+        // software pipeline: ray q+1's record is read from shared memory
+        // before ray q's accumulator update (no alias between st4/st2 and T)
+        float4 a = st4[warp][0];
+        float2 b2 = st2[warp][0];
         for (int q = 0; q < nr; ++q) {
-          const float4 a = st4[warp][q];
-          const float2 b2 = st2[warp][q];
+          const int qn = min(q + 1, 31);
+          const float4 an = st4[warp][qn];
+          const float2 bn = st2[warp][qn];
+          const unsigned S = __float_as_uint(a.z);
           const unsigned long long Ft =
               ((unsigned long long)__float_as_uint(a.y) << 32) | (unsigned long long)__float_as_uint(a.x);
-          const unsigned S = __float_as_uint(a.z);
           const unsigned long long F = (unsigned long long)lane * S + Ft;
-          const unsigned long long F1 = (unsigned long long)lane1 * S + Ft;
-          const int l0 = (int)(F >> 32);
-          const bool cross = (int)(F1 >> 32) != l0;
+          const unsigned long long F1 = F + S;
+          const unsigned lo = (unsigned)F, hi = (unsigned)(F >> 32), hi1 = (unsigned)(F1 >> 32);
+          const int l0 = (int)hi;
+          const bool cross = hi1 != hi;
           float w0, w1;
-          seg_weights((unsigned)F, cross, a.w, b2.x, w0, w1);
+          seg_weights(lo, cross, a.w, b2.x, w0, w1);
           const int ad = lanebase + l0 * stride;
-          if ((unsigned)l0 < (unsigned)kBT) Tt[ad] = fmaf(w0, b2.y, Tt[ad]);
-          if (cross && (unsigned)(l0 + 1) < (unsigned)kBT) Tt[ad + stride] = fmaf(w1, b2.y, Tt[ad + stride]);
+          const bool v0 = (unsigned)l0 < (unsigned)kBT;
+          const bool v1 = cross && (unsigned)(l0 + 1) < (unsigned)kBT;
+          float c0v = 0.f, c1v = 0.f;
+          if (v0) c0v = Tt[ad];
+          if (v1) c1v = Tt[ad + stride];
+          if (v0) Tt[ad] = fmaf(w0, b2.y, c0v);
+          if (v1) Tt[ad + stride] = fmaf(w1, b2.y, c1v);
+          a = an;
+          b2 = bn;
         }
         __syncwarp();
       }

@@ -17,6 +17,14 @@
 
 namespace ms2g {
 
+// Hide a value from the optimizer so that 32-bit compares of the high word of
+// a 64-bit fixed-point coordinate stay 32-bit.
+__device__ __forceinline__ int opaque_i32(int v) {
+  int r;
+  asm("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 // Weights of the (up to) two segments of one column.  lo = low word of F.
 //   no crossing: w0 = Lc, w1 = 0
 //   crossing   : w0 = (2^32 - lo) * Ly32 (clamped to Lc), w1 = Lc - w0
@@ -109,20 +117,20 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
     const bool mir = cls & kMirror;
     const int kb = mir ? nc - 2 : 0, ks = mir ? -1 : 1;
     long long F = F0 + (long long)wcl * (long long)S;
-    int off = wcl * L;
+    int offk = wcl * L + kb;                 // element index of pair k = 0 on line c, plus kb
 #pragma unroll 4
     for (int c = wcl; c < wch; ++c) {
       const long long F1 = F + (long long)S;
-      const int q = (int)(F >> 32);
-      const bool cross = (int)(F1 >> 32) != q;
+      const int q = opaque_i32((int)(F >> 32));
+      const bool cross = opaque_i32((int)(F1 >> 32)) != q;
       float w0, w1;
       seg_weights((unsigned)F, cross, Lc, Ly32, w0, w1);
-      const int qc = min(max(q, -2), nc);
-      const float2 pv = __ldg(base + off + kb + ks * qc);
+      const int e = opaque_i32(offk + ks * min(max(q, -2), nc));
+      const float2 pv = __ldg(base + e);
       acc = fmaf(w0, pv.x, acc);
       acc = fmaf(w1, pv.y, acc);
       F = F1;
-      off += L;
+      offk += L;
     }
   }
   if (valid) {
@@ -164,8 +172,8 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
                                                        int nc, int tiles_x, float scale, int accumulate,
                                                        int partial) {
   __shared__ float acc[kBW][2][kTS];
-  __shared__ float4 st4[kBW][32];
-  __shared__ float2 st2[kBW][32];
+  __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
+  __shared__ float2 st2[kBW][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -228,30 +236,32 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
         const int nr = min(32, te - tb + 1);
         // software pipeline: ray q+1's record is read from shared memory
         // before ray q's accumulator update (no alias between st4/st2 and T)
-        float4 a = st4[warp][0];
-        float2 b2 = st2[warp][0];
+        const float4* p4 = st4[warp];
+        const float2* p2 = st2[warp];
+        float4 a = p4[0];
+        float2 b2 = p2[0];
         for (int q = 0; q < nr; ++q) {
-          const int qn = min(q + 1, 31);
-          const float4 an = st4[warp][qn];
-          const float2 bn = st2[warp][qn];
+          const float4 an = p4[q + 1];
+          const float2 bn = p2[q + 1];
           const unsigned S = __float_as_uint(a.z);
           const unsigned long long Ft =
               ((unsigned long long)__float_as_uint(a.y) << 32) | (unsigned long long)__float_as_uint(a.x);
           const unsigned long long F = (unsigned long long)lane * S + Ft;
           const unsigned long long F1 = F + S;
-          const unsigned lo = (unsigned)F, hi = (unsigned)(F >> 32), hi1 = (unsigned)(F1 >> 32);
-          const int l0 = (int)hi;
-          const bool cross = hi1 != hi;
+          const unsigned lo = (unsigned)F;
+          const int l0 = opaque_i32((int)(F >> 32));
+          const bool cross = opaque_i32((int)(F1 >> 32)) != l0;
           float w0, w1;
           seg_weights(lo, cross, a.w, b2.x, w0, w1);
-          const int ad = lanebase + l0 * stride;
+          float* c0p = Tt + lanebase + l0 * stride;
+          float* c1p = c0p + stride;
           const bool v0 = (unsigned)l0 < (unsigned)kBT;
           const bool v1 = cross && (unsigned)(l0 + 1) < (unsigned)kBT;
-          float c0v = 0.f, c1v = 0.f;
-          if (v0) c0v = Tt[ad];
-          if (v1) c1v = Tt[ad + stride];
-          if (v0) Tt[ad] = fmaf(w0, b2.y, c0v);
-          if (v1) Tt[ad + stride] = fmaf(w1, b2.y, c1v);
+          float c0v, c1v;
+          if (v0) c0v = *c0p;
+          if (v1) c1v = *c1p;
+          if (v0) *c0p = fmaf(w0, b2.y, c0v);
+          if (v1) *c1p = fmaf(w1, b2.y, c1v);
           a = an;
           b2 = bn;
         }

@@ -205,6 +205,13 @@ def run_ms2g(args, rank, nranks, local_rank):
     def step():
         P.pnp_ms2g_solve_async(plan, pr.stages, b, x0, xo, **kw)
 
+    if args.profile_once:
+        step()
+        step()
+        P.solve_status(plan)
+        plan.destroy()
+        return
+
     for _ in range(args.warmup):
         step()
     P.solve_status(plan)
@@ -336,6 +343,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ms2g", choices=["ms2g", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle sample")
+    ap.add_argument("--profile-once", action="store_true",
+                    help="run one warm-up solve and one solve, print nothing (for ncu launch lists)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

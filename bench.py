@@ -306,7 +306,7 @@ def run_ms2g(args, rank, nranks, local_rank):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(f"k_{dom}")
+            traffic = json.load(f).get(f"k_{dom}", {}).get(str(s_dom))
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,

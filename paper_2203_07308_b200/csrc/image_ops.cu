@@ -244,12 +244,26 @@ __global__ void k_dot_norm(const float* __restrict__ v, const float* __restrict_
 
 __global__ void k_power_finalize(const double* __restrict__ red, int nblocks, double* __restrict__ pw,
                                  double* L_out, double* eta_out, float* etaf_out) {
-  if (threadIdx.x != 0) return;
+  // fixed-order tree over the block partials (deterministic)
+  __shared__ double sd[256], sn[256];
   double d = 0.0, q = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
     d += red[2 * b];
     q += red[2 * b + 1];
   }
+  sd[threadIdx.x] = d;
+  sn[threadIdx.x] = q;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sd[threadIdx.x] += sd[threadIdx.x + o];
+      sn[threadIdx.x] += sn[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  d = sd[0];
+  q = sn[0];
   pw[0] = d;
   pw[1] = q > 0.0 ? 1.0 / sqrt(q) : 0.0;
   if (L_out) *L_out = d;
@@ -270,7 +284,7 @@ int launch_power_step(int nc, int /*batch*/, const float* v, const float* w, dou
   const size_t np = (size_t)nc * nc;
   k_dot_norm<<<red_blocks, 256, 0, st>>>(v, w, np, red);
   MS2G_TRY(check_launch("k_dot_norm"));
-  k_power_finalize<<<1, 32, 0, st>>>(red, red_blocks, pw, L_out, eta_out, etaf_out);
+  k_power_finalize<<<1, 256, 0, st>>>(red, red_blocks, pw, L_out, eta_out, etaf_out);
   MS2G_TRY(check_launch("k_power_finalize"));
   if (vnext) {
     k_scale<<<grid1d(np), 256, 0, st>>>(w, pw, vnext, np);

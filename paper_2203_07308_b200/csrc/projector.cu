@@ -157,13 +157,14 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 // own column (major-x rays) or row (major-y rays) of the warp's private
 // shared accumulators: no atomics, fixed order, deterministic.  The bins of a
 // view are processed in runs of one ray class, so every per-ray branch of the
-// inner loop is loop-invariant.  Non-mirrored classes accumulate in T1
-// (row stride 33), mirrored classes in T2 = the tile with rows reversed, so
-// that both diagonal directions are bank-conflict free.  The warp tiles are
-// summed in fixed order at the end.
+// inner loop is loop-invariant.  Major-x rays accumulate in TX[row][col],
+// major-y rays in TY[col][row] (transposed): in both the lane index is the
+// fastest-varying coordinate, so every access of a step hits 32 distinct
+// banks whatever the slope or mirroring.  The warp tiles are summed in fixed
+// order at the end.
 constexpr int kBT = 32;
 constexpr int kBW = 4;
-constexpr int kTS = kBT * (kBT + 1);
+constexpr int kTS = kBT * kBT;
 
 __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restrict__ rays,
                                                        const ViewEntry* __restrict__ views, int B,
@@ -179,11 +180,11 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kBT, y0 = ty * kBT;
   const int x1 = min(x0 + kBT, nc), y1 = min(y0 + kBT, nc);
-  float* T1 = acc[warp][0];
-  float* T2 = acc[warp][1];
+  float* TX = acc[warp][0];
+  float* TY = acc[warp][1];
   for (int i = lane; i < kTS; i += 32) {
-    T1[i] = 0.f;
-    T2[i] = 0.f;
+    TX[i] = 0.f;
+    TY[i] = 0.f;
   }
   __syncwarp();
   const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
@@ -218,11 +219,10 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
       const bool majY = cls & kMajorY, mir = cls & kMirror;
       const int c0 = majY ? y0 : x0;
       const int mb = mir ? nc - (majY ? x0 : y0) - kBT : (majY ? x0 : y0);
-      float* Tt = mir ? T2 : T1;
-      int lanebase, stride;
-      if (!majY) { lanebase = lane; stride = kBT + 1; }
-      else if (!mir) { lanebase = lane * (kBT + 1); stride = 1; }
-      else { lanebase = (kBT - 1 - lane) * (kBT + 1) + (kBT - 1); stride = -1; }
+      // cell (local minor l, lane) -> T[phys_minor * 32 + lane], phys_minor = mir ? 31 - l : l
+      float* Tt = majY ? TY : TX;
+      const int lanebase = lane + (mir ? (kBT - 1) * kBT : 0);
+      const int stride = mir ? -kBT : kBT;
       for (int tb = ta; tb <= te; tb += 32) {
         const int t = tb + lane;
         if (t <= te) {
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
     if (yy < nc && xx < nc) {
       float s = 0.f;
 #pragma unroll
-      for (int w = 0; w < kBW; ++w) s += acc[w][0][ly * (kBT + 1) + lx] + acc[w][1][(kBT - 1 - ly) * (kBT + 1) + lx];
+      for (int w = 0; w < kBW; ++w) s += acc[w][0][ly * kBT + lx] + acc[w][1][lx * kBT + ly];
       const size_t o = (size_t)yy * nc + xx;
       if (partial) {
         out[((size_t)bz * gridDim.y + chunk) * np + o] = s;

@@ -53,6 +53,7 @@ struct FactorTables {
   RayEntry* d_rays = nullptr;     // [V_r][B]
   ViewEntry* d_views = nullptr;   // [V_r]
   int bp_chunks = 1;              // view chunks of the backprojector
+  int4* d_bpr = nullptr;          // per (32x32 tile, view): bin runs meeting the tile
 };
 
 struct SolveGraph {
@@ -149,6 +150,7 @@ const FactorTables* find_factor(const ms2g_plan* p, int factor);
 int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s);
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s);
+int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s);
 

@@ -118,6 +118,22 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   MS2G_CUDA(cudaMalloc(&f.d_views, sizeof(ViewEntry) * views.size()));
   MS2G_CUDA(cudaMemcpy(f.d_rays, rays.data(), sizeof(RayEntry) * rays.size(), cudaMemcpyHostToDevice));
   MS2G_CUDA(cudaMemcpy(f.d_views, views.data(), sizeof(ViewEntry) * views.size(), cudaMemcpyHostToDevice));
+  {  // adjoint tile/view bin ranges (geometry only, once per plan)
+    const int tx = (nc + 31) / 32;
+    int* d_err = nullptr;
+    MS2G_CUDA(cudaMalloc(&f.d_bpr, sizeof(int4) * (size_t)tx * tx * V_r));
+    MS2G_CUDA(cudaMalloc(&d_err, sizeof(int)));
+    MS2G_CUDA(cudaMemset(d_err, 0, sizeof(int)));
+    int rc = launch_bp_ranges(f, V_r, B, f.d_bpr, d_err, 0);
+    int herr = 0;
+    if (rc == MS2G_OK) {
+      cudaError_t e = cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) rc = set_error(MS2G_ERR_CUDA, std::string("bp ranges: ") + cudaGetErrorString(e));
+    }
+    cudaFree(d_err);
+    if (rc != MS2G_OK) return rc;
+    if (herr) return set_error(MS2G_ERR_CONFIG, "a tile's shadow spans more than 2 ray classes (fan too wide)");
+  }
   // backprojector view chunks: enough blocks for ~4 waves of 148 SMs
   const int tiles_x = (nc + 31) / 32;
   const long long tiles = (long long)tiles_x * tiles_x * d.batch;
@@ -135,6 +151,7 @@ static void free_plan(ms2g_plan* p) {
   for (auto& f : p->ft) {
     cudaFree(f.d_rays);
     cudaFree(f.d_views);
+    cudaFree(f.d_bpr);
   }
   cudaFree(p->w_pair);
   float* fl[] = {p->w_v, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],

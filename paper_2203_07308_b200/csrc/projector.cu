@@ -151,23 +151,64 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 
 // --------------------------------------------------------------- adjoint --
 // Tile-driven ray scatter.  A block owns a 32x32 pixel tile and a chunk of
-// views; each warp takes one view at a time, finds the bins whose rays meet
-// the tile (detector coordinate of the tile corners), and walks those rays one
-// per step with LANE = major index inside the tile.  A lane only touches its
-// own column (major-x rays) or row (major-y rays) of the warp's private
-// shared accumulators: no atomics, fixed order, deterministic.  The bins of a
-// view are processed in runs of one ray class, so every per-ray branch of the
-// inner loop is loop-invariant.  Major-x rays accumulate in TX[row][col],
-// major-y rays in TY[col][row] (transposed): in both the lane index is the
-// fastest-varying coordinate, so every access of a step hits 32 distinct
-// banks whatever the slope or mirroring.  The warp tiles are summed in fixed
-// order at the end.
+// views; each warp takes one view at a time and walks the rays that meet the
+// tile, one per step, with LANE = major index inside the tile.  A lane only
+// touches its own column (major-x rays) or row (major-y rays) of the warp's
+// private shared accumulators: no atomics, fixed order, deterministic.
+// Major-x rays accumulate in TX[row][col], major-y rays in TY[col][row]: the
+// lane is the fastest-varying coordinate, so every access of a step hits 32
+// distinct banks whatever the slope or mirroring.  The bins that meet each
+// (tile, view) are precomputed per plan (k_bp_ranges), split into <= 2 runs of
+// one ray class (major axis, mirror), so the addressing constants are
+// loop-invariant.  The ray records of the next 32-ray round are fetched from
+// global memory while the current round is processed (software pipeline).
+// The warp tiles are summed in fixed order at the end.
 constexpr int kBT = 32;
 constexpr int kBW = 4;
 constexpr int kTS = kBT * kBT;
 
+// Per (tile, view): bins [ta_r, te_r] of run r (r < n), class cls_r.
+__global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B, int nc, int tiles_x,
+                            int4* __restrict__ out, int* __restrict__ err) {
+  const size_t n = (size_t)tiles_x * tiles_x * V_r;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i % V_r);
+    const int tile = (int)(i / V_r);
+    const int x0 = (tile % tiles_x) * kBT, y0 = (tile / tiles_x) * kBT;
+    const int x1 = min(x0 + kBT, nc), y1 = min(y0 + kBT, nc);
+    const ViewEntry V = views[g];
+    float tmin = INFINITY, tmax = -INFINITY;
+    for (int c = 0; c < 4; ++c) {
+      const float px = (c & 1) ? (float)x1 : (float)x0, py = (c & 2) ? (float)y1 : (float)y0;
+      const float dx = px - V.Sx, dy = py - V.Sy;
+      const float tau = V.off + V.scale * (dx * V.ex + dy * V.ey) / (dx * V.nx + dy * V.ny);
+      tmin = fminf(tmin, tau);
+      tmax = fmaxf(tmax, tau);
+    }
+    const int t_lo = max(0, (int)floorf(tmin - 0.01f));
+    const int t_hi = min(B - 1, (int)ceilf(tmax + 0.01f));
+    int nr = 0, ta[2] = {0, 0}, te[2] = {-1, -1}, cl[2] = {0, 0};
+    for (int sg = 0; sg < V.nseg; ++sg) {
+      const int a = max(t_lo, (int)V.seg_t[sg]), e = min(t_hi, (int)V.seg_t[sg + 1] - 1);
+      if (a > e) continue;
+      if (nr == 2) { atomicExch(err, 1); break; }
+      ta[nr] = a; te[nr] = e; cl[nr] = V.seg_cls[sg]; ++nr;
+    }
+    out[i] = make_int4((ta[0] & 0xffff) | (te[0] << 16), (ta[1] & 0xffff) | (te[1] << 16),
+                       cl[0] | (cl[1] << 8) | (nr << 16), 0);
+  }
+}
+
+int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s) {
+  const int tiles_x = (f.nc + kBT - 1) / kBT;
+  const size_t n = (size_t)tiles_x * tiles_x * V_r;
+  const int blocks = (int)((n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192);
+  k_bp_ranges<<<blocks, 256, 0, s>>>(f.d_views, V_r, B, f.nc, tiles_x, out, err);
+  return check_launch("k_bp_ranges");
+}
+
 __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restrict__ rays,
-                                                       const ViewEntry* __restrict__ views, int B,
+                                                       const int4* __restrict__ ranges, int V_r, int B,
                                                        const int* __restrict__ sel, int n_sel, int vpc,
                                                        const float* __restrict__ sino, float* __restrict__ out,
                                                        int nc, int tiles_x, float scale, int accumulate,
@@ -179,7 +220,6 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
   const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kBT, y0 = ty * kBT;
-  const int x1 = min(x0 + kBT, nc), y1 = min(y0 + kBT, nc);
   float* TX = acc[warp][0];
   float* TY = acc[warp][1];
   for (int i = lane; i < kTS; i += 32) {
@@ -189,85 +229,128 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
   __syncwarp();
   const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
   const float* sb = sino + (size_t)bz * n_sel * B;
-  for (int k = kb + warp; k < ke; k += kBW) {
-    const int g = sel ? __ldg(sel + k) : k;
-    const ViewEntry* V = views + g;
-    // detector coordinate of the tile's 4 corners (lanes 0..3)
-    float tmin = INFINITY, tmax = -INFINITY;
-    if (lane < 4) {
-      const float px = (lane & 1) ? (float)x1 : (float)x0;
-      const float py = (lane & 2) ? (float)y1 : (float)y0;
-      const float dx = px - V->Sx, dy = py - V->Sy;
-      const float tau = V->off + V->scale * (dx * V->ex + dy * V->ey) / (dx * V->nx + dy * V->ny);
-      tmin = tmax = tau;
-    }
-#pragma unroll
-    for (int o = 2; o; o >>= 1) {
-      tmin = fminf(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
-      tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-    }
-    tmin = __shfl_sync(0xffffffffu, tmin, 0);
-    tmax = __shfl_sync(0xffffffffu, tmax, 0);
-    const int t_lo = max(0, (int)floorf(tmin - 0.01f));
-    const int t_hi = min(B - 1, (int)ceilf(tmax + 0.01f));
-    const int nseg = V->nseg;
-    for (int sg = 0; sg < nseg; ++sg) {
-      const int ta = max(t_lo, (int)V->seg_t[sg]);
-      const int te = min(t_hi, (int)V->seg_t[sg + 1] - 1);
-      if (ta > te) continue;
-      const int cls = V->seg_cls[sg];
-      const bool majY = cls & kMajorY, mir = cls & kMirror;
-      const int c0 = majY ? y0 : x0;
-      const int mb = mir ? nc - (majY ? x0 : y0) - kBT : (majY ? x0 : y0);
-      // cell (local minor l, lane) -> T[phys_minor * 32 + lane], phys_minor = mir ? 31 - l : l
-      float* Tt = majY ? TY : TX;
-      const int lanebase = lane + (mir ? (kBT - 1) * kBT : 0);
-      const int stride = mir ? -kBT : kBT;
-      for (int tb = ta; tb <= te; tb += 32) {
-        const int t = tb + lane;
-        if (t <= te) {
-          const RayEntry R = rays[(size_t)g * B + t];
-          const long long Ft = R.F0 + (long long)c0 * (long long)R.S - ((long long)mb << 32);
-          st4[warp][lane] = make_float4(__uint_as_float((unsigned)Ft), __uint_as_float((unsigned)(Ft >> 32)),
-                                        __uint_as_float(R.S), R.Lc);
-          st2[warp][lane] = make_float2(R.Ly32, __ldg(sb + (size_t)k * B + t));
+  const int4* trange = ranges + (size_t)tile * V_r;
+
+  // ---- round iterator: (view k, run, [tb, te]) of this warp ----
+  int vbase = kb + warp - 32 * kBW;     // first view of the current 32-view batch
+  int g_lane = 0;                       // rank-local view held by this lane for the batch
+  int4 rr_lane = make_int4(0, 0, 0, 0); // its range record
+  int j = 31;                           // index of the current view within the batch
+  int k = -1, g = 0, nr = 0, run = 0, tb = 0, te = -1, cls = 0;
+  int ra0 = 0, re0 = -1, ra1 = 0, re1 = -1, cls0 = 0, cls1 = 0;
+  auto next_round = [&]() -> bool {
+    tb += 32;
+    while (tb > te) {
+      ++run;
+      if (run >= nr) {
+        ++j;
+        if (j == 32) {                    // load the next batch of 32 views (lane j <-> view)
+          vbase += 32 * kBW;
+          if (vbase >= ke) return false;
+          const int kk = vbase + lane * kBW;
+          g_lane = (kk < ke) ? (sel ? __ldg(sel + kk) : kk) : 0;
+          rr_lane = (kk < ke) ? __ldg(trange + g_lane) : make_int4(0, 0, 0, 0);
+          j = 0;
         }
-        __syncwarp();
-        const int nr = min(32, te - tb + 1);
-        // software pipeline: ray q+1's record is read from shared memory
-        // before ray q's accumulator update (no alias between st4/st2 and T)
-        const float4* p4 = st4[warp];
-        const float2* p2 = st2[warp];
-        float4 a = p4[0];
-        float2 b2 = p2[0];
-        for (int q = 0; q < nr; ++q) {
-          const float4 an = p4[q + 1];
-          const float2 bn = p2[q + 1];
-          const unsigned S = __float_as_uint(a.z);
-          const unsigned long long Ft =
-              ((unsigned long long)__float_as_uint(a.y) << 32) | (unsigned long long)__float_as_uint(a.x);
-          const unsigned long long F = (unsigned long long)lane * S + Ft;
-          const unsigned long long F1 = F + S;
-          const unsigned lo = (unsigned)F;
-          const int l0 = opaque_i32((int)(F >> 32));
-          const bool cross = opaque_i32((int)(F1 >> 32)) != l0;
-          float w0, w1;
-          seg_weights(lo, cross, a.w, b2.x, w0, w1);
-          float* c0p = Tt + lanebase + l0 * stride;
-          float* c1p = c0p + stride;
-          const bool v0 = (unsigned)l0 < (unsigned)kBT;
-          const bool v1 = cross && (unsigned)(l0 + 1) < (unsigned)kBT;
-          float c0v, c1v;
-          if (v0) c0v = *c0p;
-          if (v1) c1v = *c1p;
-          if (v0) *c0p = fmaf(w0, b2.y, c0v);
-          if (v1) *c1p = fmaf(w1, b2.y, c1v);
-          a = an;
-          b2 = bn;
-        }
-        __syncwarp();
+        k = vbase + j * kBW;
+        if (k >= ke) return false;
+        g = __shfl_sync(0xffffffffu, g_lane, j);
+        const int rx = __shfl_sync(0xffffffffu, rr_lane.x, j);
+        const int ry = __shfl_sync(0xffffffffu, rr_lane.y, j);
+        const int rz = __shfl_sync(0xffffffffu, rr_lane.z, j);
+        ra0 = rx & 0xffff; re0 = (short)(rx >> 16); ra1 = ry & 0xffff; re1 = (short)(ry >> 16);
+        cls0 = rz & 0xff; cls1 = (rz >> 8) & 0xff; nr = (rz >> 16) & 0xff;
+        run = -1;
+        continue;
+      }
+      tb = run ? ra1 : ra0;
+      te = run ? re1 : re0;
+      cls = run ? cls1 : cls0;
+    }
+    return true;
+  };
+  auto frame = [&](int c, int& c0, int& mb) {
+    const bool majY = c & kMajorY, mir = c & kMirror;
+    c0 = majY ? y0 : x0;
+    mb = mir ? nc - (majY ? x0 : y0) - kBT : (majY ? x0 : y0);
+  };
+
+  run = 0; nr = 0; te = -1; tb = 0;
+  bool have = next_round();
+  // prefetch the first round
+  RayEntry Rn;
+  float rn = 0.f;
+  int tn = tb + lane;
+  if (have && tn <= te) {
+    Rn = rays[(size_t)g * B + tn];
+    rn = __ldg(sb + (size_t)k * B + tn);
+  }
+  while (have) {
+    // commit the prefetched round to shared memory (tile-relative coordinate)
+    const int ccls = cls, cte = te, ctb = tb;
+    {
+      int c0, mb;
+      frame(ccls, c0, mb);
+      if (tn <= cte) {
+        const long long Ft = Rn.F0 + (long long)c0 * (long long)Rn.S - ((long long)mb << 32);
+        st4[warp][lane] = make_float4(__uint_as_float((unsigned)Ft), __uint_as_float((unsigned)(Ft >> 32)),
+                                      __uint_as_float(Rn.S), Rn.Lc);
+        st2[warp][lane] = make_float2(Rn.Ly32, rn);
       }
     }
+    __syncwarp();
+    // fetch the next round while this one is processed
+    have = next_round();
+    tn = tb + lane;
+    if (have && tn <= te) {
+      Rn = rays[(size_t)g * B + tn];
+      rn = __ldg(sb + (size_t)k * B + tn);
+    }
+    const bool majY = ccls & kMajorY, mir = ccls & kMirror;
+    // cell (local minor l, lane) -> T[phys_minor * 32 + lane], phys_minor = mir ? 31 - l : l
+    // (byte addresses in the shared window)
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(majY ? TY : TX) +
+                           4u * (unsigned)(lane + (mir ? (kBT - 1) * kBT : 0));
+    const int sstride = mir ? -4 * kBT : 4 * kBT;
+    const int nrays = min(32, cte - ctb + 1);
+    const float4* p4 = st4[warp];
+    const float2* p2 = st2[warp];
+    float4 a = p4[0];
+    float2 b2 = p2[0];
+    for (int q = 0; q < nrays; ++q) {
+      const float4 an = p4[q + 1];
+      const float2 bn = p2[q + 1];
+      unsigned lo, hi, hi1;
+      asm("{\n\t.reg .u64 ft, f, f1, s64;\n\t"
+          "mov.b64 ft, {%3, %4};\n\t"
+          "cvt.u64.u32 s64, %6;\n\t"
+          "mad.wide.u32 f, %5, %6, ft;\n\t"
+          "add.u64 f1, f, s64;\n\t"
+          "mov.b64 {%0, %1}, f;\n\t"
+          "{\n\t.reg .u32 t;\n\tmov.b64 {t, %2}, f1;\n\t}\n\t}"
+          : "=r"(lo), "=r"(hi), "=r"(hi1)
+          : "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)), "r"((unsigned)lane), "r"(__float_as_uint(a.z)));
+      const bool cross = hi1 != hi;
+      float w0, w1;
+      seg_weights(lo, cross, a.w, b2.x, w0, w1);
+      const unsigned ad0 = sbase + hi * (unsigned)sstride;
+      const unsigned ad1 = ad0 + (unsigned)sstride;
+      const unsigned v0 = hi < (unsigned)kBT;
+      const unsigned v1 = cross && (hi + 1u) < (unsigned)kBT;
+      asm volatile("{\n\t.reg .pred p0, p1;\n\t.reg .f32 c0, c1;\n\t"
+                   "setp.ne.u32 p0, %5, 0;\n\t"
+                   "setp.ne.u32 p1, %6, 0;\n\t"
+                   "@p0 ld.shared.f32 c0, [%0];\n\t"
+                   "@p1 ld.shared.f32 c1, [%1];\n\t"
+                   "@p0 fma.rn.f32 c0, %2, %4, c0;\n\t"
+                   "@p1 fma.rn.f32 c1, %3, %4, c1;\n\t"
+                   "@p0 st.shared.f32 [%0], c0;\n\t"
+                   "@p1 st.shared.f32 [%1], c1;\n\t}"
+                   :: "r"(ad0), "r"(ad1), "f"(w0), "f"(w1), "f"(b2.y), "r"(v0), "r"(v1) : "memory");
+      a = an;
+      b2 = bn;
+    }
+    __syncwarp();
   }
   __syncthreads();
   const size_t np = (size_t)nc * nc;
@@ -314,7 +397,7 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   const int vpc = (n_sel + nchunks - 1) / nchunks;
   const int partial = nchunks > 1;
   dim3 grid(tiles_x * tiles_x, nchunks, batch);
-  k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_views, p->B, d_sel, n_sel, vpc, sino,
+  k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino,
                                        partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
   MS2G_TRY(check_launch("k_backward"));
   if (partial) {

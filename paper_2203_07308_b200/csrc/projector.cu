@@ -116,20 +116,25 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
     const float2* base = pairs + cls * pair_stride + (size_t)bz * nc * L + 2;
     const bool mir = cls & kMirror;
     const int kb = mir ? nc - 2 : 0, ks = mir ? -1 : 1;
-    long long F = F0 + (long long)wcl * (long long)S;
+    const long long Fs = F0 + (long long)wcl * (long long)S;
+    unsigned flo = (unsigned)Fs, fhi = (unsigned)(Fs >> 32);
     int offk = wcl * L + kb;                 // element index of pair k = 0 on line c, plus kb
 #pragma unroll 4
     for (int c = wcl; c < wch; ++c) {
-      const long long F1 = F + (long long)S;
-      const int q = opaque_i32((int)(F >> 32));
-      const bool cross = opaque_i32((int)(F1 >> 32)) != q;
+      unsigned lo1, hi1;
+      asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(flo), "r"(fhi), "r"(S));
+      const int q = (int)fhi;
+      const bool cross = hi1 != fhi;
       float w0, w1;
-      seg_weights((unsigned)F, cross, Lc, Ly32, w0, w1);
-      const int e = opaque_i32(offk + ks * min(max(q, -2), nc));
-      const float2 pv = __ldg(base + e);
-      acc = fmaf(w0, pv.x, acc);
-      acc = fmaf(w1, pv.y, acc);
-      F = F1;
+      seg_weights(flo, cross, Lc, Ly32, w0, w1);
+      const int e = offk + ks * min(max(q, -2), nc);
+      float px, py;
+      asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
+          : "=f"(px), "=f"(py) : "r"(e), "l"(base));
+      acc = fmaf(w0, px, acc);
+      acc = fmaf(w1, py, acc);
+      flo = lo1;
+      fhi = hi1;
       offk += L;
     }
   }

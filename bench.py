@@ -182,6 +182,52 @@ def time_calls(fn, reps, warm=3):
     return e0.elapsed_time(e1) / reps / 1000.0
 
 
+def detail_512(P, dev):
+    """512^2 numbers of the metric (C3/C5 geometry, 720 x 768): sketched-
+    gradient evals/s at s = 4, 2, 1 on all views and on one 1/8 subset, the
+    C3 Option-2 solve (64 iterations, 3 stages with power iterations) and the
+    C5 batch-8 solve (Poisson data, TV) in iterations/s per image."""
+    import torch
+    out = {}
+    pr3, pr5 = S.PRESETS[3], S.PRESETS[5]
+    nnz = nnz_counts()["C3"]
+    with P.plan_geometry(pr3.n, pr3.n_views, pr3.n_bins, factors=(4, 2, 1)) as plan:
+        x = torch.from_numpy(S.phantom(pr3.n, pr3.n_ellipses, S.config_seed(3, 9))).to(dev)[None].contiguous()
+        xt = S.phantom(pr3.n, pr3.n_ellipses, S.config_seed(3), texture=pr3.texture)
+        p = P.forward_project(plan, 1, torch.from_numpy(xt).to(dev)[None])[0].cpu().numpy()
+        b = torch.from_numpy(S.gaussian_data(p, pr3.noise[1], S.config_seed(3))).to(dev)[None].contiguous()
+        g = torch.empty_like(x)
+        sub = list(range(0, pr3.n_views, 8))
+        for s_ in (4, 2, 1):
+            t_all = time_calls(lambda: P.sketched_grad(plan, s_, x, b, g=g), 10)
+            t_sub = time_calls(lambda: P.sketched_grad(plan, s_, x, b, g=g, subset=sub), 10)
+            out[f"C3_512_grad_s{s_}"] = {"evals_per_s": 1.0 / t_all, "subset_evals_per_s": 1.0 / t_sub,
+                                         "segments_per_s": 2 * nnz[str(s_)] / t_all,
+                                         "subset_segments_per_s": 2 * nnz[f"{s_}_subset0"] / t_sub}
+        x0 = torch.zeros_like(x); xo = torch.empty_like(x)
+        kw = dict(option=2, n_subsets=8, seed=S.config_seed(3), den=pr3.den, alpha=pr3.alpha)
+        ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr3.stages, b, x0, xo, **kw), 3, warm=2)
+        P.solve_status(plan)
+        out["C3_512_solve"] = {"iters_per_s": pr3.n_steps / ts, "ms_per_solve": ts * 1e3,
+                               "schedule": "Option 2, 8 subsets, epochs [3,3,2] at s=4,2,1"}
+    nb = pr5.batch
+    with P.plan_geometry(pr5.n, pr5.n_views, pr5.n_bins, factors=(2, 1), batch=nb) as plan:
+        bs = []
+        with P.plan_geometry(pr5.n, pr5.n_views, pr5.n_bins, factors=(1,)) as one:
+            for im in range(nb):
+                xt = S.phantom(pr5.n, pr5.n_ellipses, S.config_seed(5, im))
+                p = P.forward_project(one, 1, torch.from_numpy(xt).to(dev)[None])[0].cpu().numpy()
+                bs.append(S.poisson_data(p, pr5.noise[1], S.config_seed(5, im)))
+        b = torch.from_numpy(np.stack(bs)).to(dev).contiguous()
+        x0 = torch.zeros((nb, pr5.n, pr5.n), device=dev); xo = torch.empty_like(x0)
+        kw = dict(den=pr5.den, alpha=pr5.alpha)
+        ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr5.stages, b, x0, xo, **kw), 3, warm=2)
+        P.solve_status(plan)
+        out["C5_512_batch8_solve"] = {"image_iters_per_s": nb * pr5.n_steps / ts, "ms_per_solve": ts * 1e3,
+                                      "images_per_solve": nb}
+    return out
+
+
 def run_ms2g(args, rank, nranks, local_rank):
     import torch
     import torch.distributed as dist
@@ -316,6 +362,9 @@ def run_ms2g(args, rank, nranks, local_rank):
                 "compulsory_frac": compulsory / tk / 1e9 / hbm,
                 "share_ms_per_solve": share}
 
+    if nranks == 1 and not args.no_detail:
+        detail.update(detail_512(P, dev))
+
     cpu = None
     if rank == 0 and nranks == 1 and not args.no_cpu:
         import oracle as O
@@ -343,6 +392,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ms2g", choices=["ms2g", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle sample")
+    ap.add_argument("--no-detail", action="store_true", help="skip the 512^2 detail numbers")
     ap.add_argument("--profile-once", action="store_true",
                     help="run one warm-up solve and one solve, print nothing (for ncu launch lists)")
     args = ap.parse_args()

@@ -337,3 +337,32 @@ def test_launch_count_increases(P):
     with P.plan_geometry(64, 10, 96, factors=(1,)) as plan:
         P.forward_project(plan, 1, torch.ones((1, 64, 64), device="cuda"))
     assert P.launch_count() > before
+
+
+def test_emulated_sharding_with_subsets(P):
+    """Option-2 subsets across view shards: each rank's compacted output covers
+    shard ∩ subset in ascending order, and the partial adjoints sum to the
+    full-plan adjoint; sketched_grad partials (scaled by V/|M| with the
+    global |M|) sum to the single-plan gradient."""
+    n, V, B = 96, 90, 144
+    sub = O.subset_views(V, 8, 3)
+    x = S.phantom(n, 8, 5)
+    b = S.random_sinogram((V, B), 6, zero_mean=False)
+    with P.plan_geometry(n, V, B, factors=(2, 1)) as full:
+        f_ref = host(P.forward_project(full, 2, dev(x[::2, ::2])[None], b=dev(b)[None], subset=sub))[0]
+        r = S.random_sinogram((len(sub), B), 7)
+        b_ref = host(P.back_project(full, 1, dev(r)[None], scale=8.0, subset=sub))[0]
+        g_ref = host(P.sketched_grad(full, 2, dev(x)[None], dev(b)[None], subset=sub))[0]
+    fwd, acc, gacc = [], np.zeros_like(b_ref), np.zeros_like(g_ref)
+    pos = 0
+    for rk in range(3):
+        vb, ve = P.view_shard(V, rk, 3)
+        mine = [v for v in sub if vb <= v < ve]
+        with P.plan_geometry(n, V, B, factors=(2, 1), view_begin=vb, view_end=ve) as sh:
+            fwd.append(host(P.forward_project(sh, 2, dev(x[::2, ::2])[None], b=dev(b[vb:ve])[None], subset=sub))[0])
+            acc += host(P.back_project(sh, 1, dev(r[pos:pos + len(mine)])[None], scale=8.0, subset=sub))[0]
+            gacc += host(P.sketched_grad(sh, 2, dev(x)[None], dev(b[vb:ve])[None], subset=sub))[0]
+        pos += len(mine)
+    assert np.array_equal(np.concatenate(fwd, 0), f_ref)
+    assert rel(acc, b_ref) <= 1e-6
+    assert rel(gacc, g_ref) <= 1e-6

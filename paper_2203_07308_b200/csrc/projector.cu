@@ -88,6 +88,9 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
 // ("A_s v - b").
 constexpr int kFwdWarps = 8;
 
+// NB images of a batch share one traversal: the weights of a column are
+// computed once and applied to NB pair images (C5: 8 reconstructions per GPU).
+template <int NB>
 __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
   const int k = blockIdx.y * kFwdWarps + warp;
   if (k >= n_sel) return;
   const int t = blockIdx.x * 32 + lane;
-  const int bz = blockIdx.z;
+  const int bz0 = blockIdx.z * NB;
   const int g = sel ? __ldg(sel + k) : k;
   const bool valid = t < B;
   long long F0 = 0;
@@ -110,10 +113,13 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
   }
   const int wcl = __reduce_min_sync(0xffffffffu, cl);
   const int wch = __reduce_max_sync(0xffffffffu, ch);
-  float acc = 0.f;
+  float acc[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) acc[i] = 0.f;
   if (wcl < wch) {
     const int L = nc + 3;
-    const float2* base = pairs + cls * pair_stride + (size_t)bz * nc * L + 2;
+    const size_t istride = (size_t)nc * L;          // pair-image stride between batch images
+    const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride + 2;
     const bool mir = cls & kMirror;
     const int kb = mir ? nc - 2 : 0, ks = mir ? -1 : 1;
     const long long Fs = F0 + (long long)wcl * (long long)S;
@@ -128,29 +134,45 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
       float w0, w1;
       seg_weights(flo, cross, Lc, Ly32, w0, w1);
       const int e = offk + ks * min(max(q, -2), nc);
-      float px, py;
-      asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
-          : "=f"(px), "=f"(py) : "r"(e), "l"(base));
-      acc = fmaf(w0, px, acc);
-      acc = fmaf(w1, py, acc);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        float px, py;
+        asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
+            : "=f"(px), "=f"(py) : "r"(e), "l"(base + i * istride));
+        acc[i] = fmaf(w0, px, acc[i]);
+        acc[i] = fmaf(w1, py, acc[i]);
+      }
       flo = lo1;
       fhi = hi1;
       offk += L;
     }
   }
   if (valid) {
-    float r = acc;
-    if (bsino) r -= __ldg(bsino + ((size_t)bz * V_r + g) * B + t);
-    out[((size_t)bz * n_sel + k) * B + t] = r;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      float r = acc[i];
+      if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
+      out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
+    }
   }
+}
+
+template <int NB>
+static void fwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const int* d_sel, int n_sel,
+                       const float* b, float* out) {
+  k_forward<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
+                                                f.nc, b, out);
 }
 
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s) {
   if (n_sel <= 0) return MS2G_OK;
-  dim3 grid((p->B + 31) / 32, (n_sel + kFwdWarps - 1) / kFwdWarps, batch);
-  k_forward<<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride, f.nc,
-                                            b, out);
+  const int nb = (batch % 8 == 0) ? 8 : (batch % 4 == 0) ? 4 : (batch % 2 == 0) ? 2 : 1;
+  dim3 grid((p->B + 31) / 32, (n_sel + kFwdWarps - 1) / kFwdWarps, batch / nb);
+  if (nb == 8) fwd_launch<8>(grid, s, p, f, d_sel, n_sel, b, out);
+  else if (nb == 4) fwd_launch<4>(grid, s, p, f, d_sel, n_sel, b, out);
+  else if (nb == 2) fwd_launch<2>(grid, s, p, f, d_sel, n_sel, b, out);
+  else fwd_launch<1>(grid, s, p, f, d_sel, n_sel, b, out);
   return check_launch("k_forward");
 }
 

@@ -366,3 +366,23 @@ def test_emulated_sharding_with_subsets(P):
     assert np.array_equal(np.concatenate(fwd, 0), f_ref)
     assert rel(acc, b_ref) <= 1e-6
     assert rel(gacc, g_ref) <= 1e-6
+
+
+@pytest.mark.parametrize("nb", [8, 4, 2, 6])
+def test_batched_forward_shares_traversal(P, nb):
+    """A batch-nb plan (one traversal applied to nb images) gives, per image,
+    exactly the single-image forward projection and the oracle's."""
+    n, V, B = 64, 45, 96
+    g = O.Geometry(n, V, B)
+    xs = np.stack([S.phantom(n, 6, 40 + i) for i in range(nb)]).astype(np.float32)
+    bs = np.stack([S.random_sinogram((V, B), 50 + i) for i in range(nb)]).astype(np.float32)
+    with P.plan_geometry(n, V, B, factors=(2, 1), batch=nb) as plan, \
+            P.plan_geometry(n, V, B, factors=(2, 1), batch=1) as one:
+        for s in (2, 1):
+            xin = xs if s == 1 else xs[:, ::2, ::2].copy()
+            got = host(P.forward_project(plan, s, dev(xin), b=dev(bs)))
+            for i in range(nb):
+                single = host(P.forward_project(one, s, dev(xin[i])[None], b=dev(bs[i])[None]))[0]
+                assert np.array_equal(got[i], single)
+            i = nb - 1
+            assert rel(got[i], O.forward(g, s, xin[i], b=bs[i])) <= TOL_OP

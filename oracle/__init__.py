@@ -73,6 +73,12 @@ def lib():
         _lib.orc_sketch_down.argtypes = [i, i, p, p]
         _lib.orc_sketch_up.argtypes = [i, i, p, p]
         _lib.orc_sketched_grad.argtypes = [G, i, p, p, p, p, i, i]
+        _lib.orc_sketched_grad_kind.argtypes = [G, i, i, p, p, p, p, i, i]
+        _lib.orc_keys.argtypes = [d]
+        _lib.orc_keys.restype = d
+        _lib.orc_bicubic_down.argtypes = [i, i, p, p]
+        _lib.orc_bicubic_up.argtypes = [i, i, p, p]
+        _lib.orc_set_resampler.argtypes = [i]
         _lib.orc_power_iteration.argtypes = [G, i, i, i]
         _lib.orc_power_iteration.restype = d
         _lib.orc_gauss3_weights.argtypes = [d, p]
@@ -208,13 +214,35 @@ def sketch_up(gc, s: int):
     return out
 
 
-def sketched_grad(g: Geometry, factor: int, x, b, views=None, nthreads: int | None = None):
-    """O6/O7: g = (V/|M|) U_s A_s^T (A_s S_s x - b_M)  (Eqs. 6-7)."""
+def sketched_grad(g: Geometry, factor: int, x, b, views=None, nthreads: int | None = None, resampler: int = 0):
+    """O6/O7: g = (V/|M|) U A_s^T (A_s S x - b_M)  (Eqs. 6-7).
+    resampler 0: average pool + replication (O4/O5); 1: bicubic (NEXT-1)."""
     x = _f64(x); b = _f64(b)
     vv, n_sel = _views(views, g.n_views)
     out = np.zeros((g.n, g.n))
-    lib().orc_sketched_grad(C.byref(g.c()), factor, _ptr(x), _ptr(b), _ptr(out),
-                            _ptr(vv) if vv is not None else None, n_sel, nthreads or default_threads())
+    lib().orc_sketched_grad_kind(C.byref(g.c()), factor, resampler, _ptr(x), _ptr(b), _ptr(out),
+                                 _ptr(vv) if vv is not None else None, n_sel, nthreads or default_threads())
+    return out
+
+
+def keys(x: float) -> float:
+    """Keys cubic convolution kernel, a = -0.5 (NEXT-1)."""
+    return lib().orc_keys(float(x))
+
+
+def bicubic_down(x, s: int):
+    """NEXT-1 S: bicubic antialiased downscale by s (P:156 imresize)."""
+    x = _f64(x); n = x.shape[-1]
+    v = np.zeros((n // s, n // s))
+    lib().orc_bicubic_down(n, s, _ptr(x), _ptr(v))
+    return v
+
+
+def bicubic_up(gc, s: int):
+    """NEXT-1 U: bicubic upscale by s (P:156 imresize)."""
+    gc = _f64(gc); nc = gc.shape[-1]
+    out = np.zeros((nc * s, nc * s))
+    lib().orc_bicubic_up(nc * s, s, _ptr(gc), _ptr(out))
     return out
 
 
@@ -292,7 +320,7 @@ class DivergedError(RuntimeError):
 
 def pnp_ms2g(g: Geometry, stages, b, x0=None, option: int = 1, n_subsets: int = 1, seed: int = 0,
              den: tuple = ("identity",), alpha: float = 1.0, power_iters: int = 20,
-             nthreads: int | None = None):
+             nthreads: int | None = None, resampler: int = 0):
     """O11 Algorithm 1.  den = ("identity",) | ("gauss", sigma) |
     ("tv", lambda, iters[, tau]).  Returns (x, trace, etas)."""
     n = g.n
@@ -311,9 +339,11 @@ def pnp_ms2g(g: Geometry, stages, b, x0=None, option: int = 1, n_subsets: int = 
     trace = (SchedEntry * max(total, 1))()
     etas = np.zeros(len(stages))
     bad = C.c_int(0)
+    lib().orc_set_resampler(resampler)
     rc = lib().orc_pnp_ms2g(C.byref(g.c()), st, len(stages), option, n_subsets, seed, kind, sigma, lam, tau,
                             diters, alpha, power_iters, _ptr(b), _ptr(x0), _ptr(out), trace, _ptr(etas),
                             nthreads or default_threads(), C.byref(bad))
+    lib().orc_set_resampler(0)
     if rc == 3:
         raise DivergedError(f"non-finite iterate at iteration {bad.value}")
     if rc != 0:

@@ -328,22 +328,84 @@ void orc_sketch_up(int n, int s, const double* gc, double* out) {
     for (int j = 0; j < n; ++j) out[(size_t)i * n + j] = gc[(size_t)(i / s) * nc + (j / s)];
 }
 
+/* --------------------------------------------------------- NEXT-1 bicubic --
+ * The paper's own S and U: "MATLAB imresize function with bicubic
+ * interpolation" ("bi-cubic interpolation suffice").  Reading
+ * (SPEC S:126): Keys cubic convolution, a = -0.5; sample
+ * centres aligned (u = (i + 0.5)/scale - 0.5); on downscale the kernel is
+ * widened by the factor (antialiasing) and each output's weights are
+ * renormalised to sum 1; replicate (clamp) boundary; separable, rows then
+ * columns.  scale = 1/s for down, s for up.                                */
+double orc_keys(double x) {
+  const double a = -0.5;
+  double t = fabs(x);
+  if (t <= 1.0) return (a + 2.0) * t * t * t - (a + 3.0) * t * t + 1.0;
+  if (t < 2.0) return a * t * t * t - 5.0 * a * t * t + 8.0 * a * t - 4.0 * a;
+  return 0.0;
+}
+
+/* 1-D resample of n_in samples to n_out samples (step `in` apart in memory) */
+static void resample_1d(const double* in, int n_in, int in_stride, double* out, int n_out, int out_stride,
+                        double scale) {
+  double kscale = scale < 1.0 ? scale : 1.0;      /* antialias on downscale */
+  double support = 2.0 / kscale;
+  for (int i = 0; i < n_out; ++i) {
+    double u = (i + 0.5) / scale - 0.5;
+    int j0 = (int)floor(u - support), j1 = (int)ceil(u + support);
+    double acc = 0.0, wsum = 0.0;
+    for (int j = j0; j <= j1; ++j) {
+      double w = kscale * orc_keys(kscale * (u - j));
+      if (w == 0.0) continue;
+      int jc = j < 0 ? 0 : (j > n_in - 1 ? n_in - 1 : j);
+      acc += w * in[(size_t)jc * in_stride];
+      wsum += w;
+    }
+    out[(size_t)i * out_stride] = acc / wsum;
+  }
+}
+
+/* 2-D: rows (along j) then columns (along i) */
+static void resample_2d(const double* x, int n_in, double* out, int n_out, double scale) {
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)n_in * n_out);
+  for (int i = 0; i < n_in; ++i) resample_1d(x + (size_t)i * n_in, n_in, 1, tmp + (size_t)i * n_out, n_out, 1, scale);
+  for (int j = 0; j < n_out; ++j) resample_1d(tmp + j, n_in, n_out, out + j, n_out, n_out, scale);
+  free(tmp);
+}
+
+void orc_bicubic_down(int n, int s, const double* x, double* v) {
+  if (s == 1) { memcpy(v, x, sizeof(double) * (size_t)n * n); return; }
+  resample_2d(x, n, v, n / s, 1.0 / s);
+}
+
+void orc_bicubic_up(int n, int s, const double* gc, double* out) {
+  if (s == 1) { memcpy(out, gc, sizeof(double) * (size_t)n * n); return; }
+  resample_2d(gc, n / s, out, n, (double)s);
+}
+
 /* ------------------------------------------------------------ O6 / O7 --
  * g = c * U_s A_s^T (A_s S_s x - b_M),  c = V/|M|  (Eq. 6,
  * P:95-97 Eq. 7, S:284/S:302 for the V/|M| reading Z7).  views == NULL
  * means all views (Option 1, c = 1).  g is full resolution N^2.          */
-void orc_sketched_grad(const orc_geom* g, int factor, const double* x, const double* b, double* grad,
-                       const int* views, int n_sel, int nthreads) {
+/* kind 0: average pool / replication (O4/O5); kind 1: bicubic (NEXT-1) */
+void orc_sketched_grad_kind(const orc_geom* g, int factor, int kind, const double* x, const double* b,
+                            double* grad, const int* views, int n_sel, int nthreads) {
   int n = g->n, nc = n / factor, V = g->n_views, B = g->n_bins;
   if (!views) n_sel = V;
   double* v = (double*)malloc(sizeof(double) * nc * nc);
   double* r = (double*)malloc(sizeof(double) * (size_t)n_sel * B);
   double* G = (double*)malloc(sizeof(double) * nc * nc);
-  orc_sketch_down(n, factor, x, v);                       /* v = S_s(y) */
+  if (kind == 1) orc_bicubic_down(n, factor, x, v);        /* v = S(y) */
+  else orc_sketch_down(n, factor, x, v);
   orc_forward(g, factor, v, b, r, views, n_sel, nthreads); /* r = A_s v - b */
   orc_backward(g, factor, r, G, (double)V / n_sel, views, n_sel, nthreads); /* G = c A_s^T r */
-  orc_sketch_up(n, factor, G, grad);                      /* U_s G */
+  if (kind == 1) orc_bicubic_up(n, factor, G, grad);       /* U G */
+  else orc_sketch_up(n, factor, G, grad);
   free(v); free(r); free(G);
+}
+
+void orc_sketched_grad(const orc_geom* g, int factor, const double* x, const double* b, double* grad,
+                       const int* views, int n_sel, int nthreads) {
+  orc_sketched_grad_kind(g, factor, 0, x, b, grad, views, n_sel, nthreads);
 }
 
 /* ------------------------------------------------------------------ O8 --
@@ -535,6 +597,9 @@ int orc_subset_views(int n_views, int n_subsets, int k, int* out) {
  *     x = (1-alpha) z + alpha D(z); y = x + a_i (x - x_prev); x_prev = x
  * den_kind: 0 identity, 1 gauss3 (sigma), 2 TV-Chambolle (lambda, tau, iters).
  * Returns 0, or 3 with *bad_i set when an iterate is non-finite.  */
+static int g_resampler = 0;
+void orc_set_resampler(int kind) { g_resampler = kind; }
+
 int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int option, int n_subsets,
                  uint64_t seed, int den_kind, double sigma, double lambda, double tau, int den_iters,
                  double alpha, int power_iters, const double* b, const double* x0, double* x_out,
@@ -565,10 +630,10 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
       orc_sched_entry e = sch[step];
       int i = e.i;
       if (e.subset < 0) {
-        orc_sketched_grad(g, e.factor, y, b, gr, NULL, V, nthreads);
+        orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, NULL, V, nthreads);
       } else {
         int m = orc_subset_views(V, n_subsets, e.subset, views);
-        orc_sketched_grad(g, e.factor, y, b, gr, views, m, nthreads);
+        orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, views, m, nthreads);
       }
       for (size_t p = 0; p < np; ++p) z[p] = y[p] - eta * gr[p];
       if (den_kind == 1) orc_gauss3(n, sigma, z, dz);

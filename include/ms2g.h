@@ -93,20 +93,27 @@ int ms2g_back_project(ms2g_plan* plan, int32_t factor, const float* sino, float*
                       int32_t accumulate, const int32_t* subset, int32_t n_subset, int32_t allreduce,
                       void* stream);
 
-/* Image-space sketch S_s (north-star D; reading Z2): s x s average pool,
- * x [batch][n][n] -> v [batch][n/s][n/s]. */
-int ms2g_sketch_down(ms2g_plan* plan, int32_t factor, const float* x, float* v, void* stream);
+/* Resampler kinds for S and U:
+ *   0  s x s average pool / nearest replication (BASELINE configs; reading Z2)
+ *   1  bicubic, the paper's own choice "MATLAB imresize ... bicubic" (P:156,
+ *      P:92): Keys a = -0.5, centre-aligned, antialiased downscale, clamped
+ *      boundary (NEXT-1; needs the factor in the plan). */
+enum { MS2G_RESAMPLE_MEAN = 0, MS2G_RESAMPLE_BICUBIC = 1 };
 
-/* Upsample + step ("z = y - eta U G"; reading Z2: U_s = nearest
- * replication = s^2 S_s^T):  z = y - eta * U_s g.  y == NULL gives z = U_s g. */
-int ms2g_sketch_up(ms2g_plan* plan, int32_t factor, const float* g, const float* y, float eta,
+/* Image-space sketch S (north-star D): x [batch][n][n] -> v [batch][n/s][n/s]. */
+int ms2g_sketch_down(ms2g_plan* plan, int32_t factor, int32_t kind, const float* x, float* v, void* stream);
+
+/* Upsample + step ("z = y - eta U G"):  z = y - eta * U g.  y == NULL
+ * gives z = U g.  kind 0: U = nearest replication = s^2 S^T (reading Z2). */
+int ms2g_sketch_up(ms2g_plan* plan, int32_t factor, int32_t kind, const float* g, const float* y, float eta,
                    float* z, void* stream);
 
 /* Sketched data-fidelity gradient (Eq. 6, Eq. 7):
- *   g = (V/|M|) U_s A_s^T (A_s S_s x - b_M)      (full resolution n x n)
+ *   g = (V/|M|) U A_s^T (A_s S x - b_M)      (full resolution n x n)
  * factor 1 gives A^T(Ax - b).  subset NULL = all views (|M| = V).
- * With NCCL attached the partial A_s^T is allreduced before U_s. */
-int ms2g_sketched_grad(ms2g_plan* plan, int32_t factor, const float* x, const float* bsino, float* g,
+ * kind selects S/U (see MS2G_RESAMPLE_*).  With NCCL attached the partial
+ * A_s^T is allreduced before U. */
+int ms2g_sketched_grad(ms2g_plan* plan, int32_t factor, int32_t kind, const float* x, const float* bsino, float* g,
                        const int32_t* subset, int32_t n_subset, void* stream);
 
 /* Lipschitz constant of the factor-s fidelity ("eta = O(1/L)"; reading
@@ -144,6 +151,7 @@ typedef struct {
   float alpha;           /* RED-PRO mix weight, 0 < alpha <= 1      */
   int32_t power_iters;   /* per-stage power iterations (20 in the configs) */
   int32_t check_every;   /* unused by the graph path: every step is checked on device */
+  int32_t resampler;     /* MS2G_RESAMPLE_MEAN (configs) | MS2G_RESAMPLE_BICUBIC (paper) */
 } ms2g_solve_desc;
 /* One global iteration: i (1-based, continuous over stages), stage,
  * factor, subset (-1 = all views), eta = 1/L_stage, a_i = (i-1)/(i+3). */

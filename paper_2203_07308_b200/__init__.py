@@ -54,7 +54,7 @@ class Stage(C.Structure):
 class SolveDesc(C.Structure):
     _fields_ = [("stages", C.POINTER(Stage)), ("n_stages", C.c_int32), ("option", C.c_int32),
                 ("n_subsets", C.c_int32), ("seed", C.c_uint64), ("den", Denoiser), ("alpha", C.c_float),
-                ("power_iters", C.c_int32), ("check_every", C.c_int32)]
+                ("power_iters", C.c_int32), ("check_every", C.c_int32), ("resampler", C.c_int32)]
 
 
 class SchedEntry(C.Structure):
@@ -88,9 +88,9 @@ def load():
     L.ms2g_attach_nccl.argtypes = [p, p, i, i]
     L.ms2g_forward_project.argtypes = [p, i, p, p, p, C.POINTER(C.c_int32), i, p]
     L.ms2g_back_project.argtypes = [p, i, p, p, f, i, C.POINTER(C.c_int32), i, i, p]
-    L.ms2g_sketch_down.argtypes = [p, i, p, p, p]
-    L.ms2g_sketch_up.argtypes = [p, i, p, p, f, p, p]
-    L.ms2g_sketched_grad.argtypes = [p, i, p, p, p, C.POINTER(C.c_int32), i, p]
+    L.ms2g_sketch_down.argtypes = [p, i, i, p, p, p]
+    L.ms2g_sketch_up.argtypes = [p, i, i, p, p, f, p, p]
+    L.ms2g_sketched_grad.argtypes = [p, i, i, p, p, p, C.POINTER(C.c_int32), i, p]
     L.ms2g_power_iteration.argtypes = [p, i, i, C.POINTER(d), p]
     L.ms2g_denoise.argtypes = [p, C.POINTER(Denoiser), p, p, p]
     L.ms2g_schedule.argtypes = [p, C.POINTER(SolveDesc), C.POINTER(SchedEntry), i, C.POINTER(C.c_int32)]
@@ -219,31 +219,38 @@ def back_project(plan: Plan, factor: int, sino, img=None, scale=1.0, accumulate=
     return img
 
 
-def sketch_down(plan: Plan, factor: int, x, v=None):
-    """S_s: s x s average pool."""
+RESAMPLERS = {"mean": 0, "bicubic": 1}
+
+
+def _kind(resampler) -> int:
+    return RESAMPLERS[resampler] if isinstance(resampler, str) else int(resampler)
+
+
+def sketch_down(plan: Plan, factor: int, x, v=None, resampler="mean"):
+    """S: s x s average pool ("mean", configs) or bicubic ("bicubic")."""
     nc = plan.nc(factor)
     if v is None:
         v = torch.empty((plan.batch, nc, nc), device=x.device, dtype=torch.float32)
-    _check(load().ms2g_sketch_down(plan.handle, factor, _dev(x, "x"), _dev(v, "v"), _stream()))
+    _check(load().ms2g_sketch_down(plan.handle, factor, _kind(resampler), _dev(x, "x"), _dev(v, "v"), _stream()))
     return v
 
 
-def sketch_up(plan: Plan, factor: int, g, y=None, eta=0.0, z=None):
-    """z = y - eta U_s g  (z = U_s g when y is None)."""
+def sketch_up(plan: Plan, factor: int, g, y=None, eta=0.0, z=None, resampler="mean"):
+    """z = y - eta U g  (z = U g when y is None); U replication or bicubic."""
     if z is None:
         z = torch.empty((plan.batch, plan.n, plan.n), device=g.device, dtype=torch.float32)
-    _check(load().ms2g_sketch_up(plan.handle, factor, _dev(g, "g"), _dev(y, "y"), float(eta), _dev(z, "z"),
-                                 _stream()))
+    _check(load().ms2g_sketch_up(plan.handle, factor, _kind(resampler), _dev(g, "g"), _dev(y, "y"), float(eta),
+                                 _dev(z, "z"), _stream()))
     return z
 
 
-def sketched_grad(plan: Plan, factor: int, x, b, g=None, subset=None):
-    """g = (V/|M|) U_s A_s^T (A_s S_s x - b_M)."""
+def sketched_grad(plan: Plan, factor: int, x, b, g=None, subset=None, resampler="mean"):
+    """g = (V/|M|) U A_s^T (A_s S x - b_M)."""
     sel, m = _subset(subset)
     if g is None:
         g = torch.empty((plan.batch, plan.n, plan.n), device=x.device, dtype=torch.float32)
-    _check(load().ms2g_sketched_grad(plan.handle, factor, _dev(x, "x"), _dev(b, "b"), _dev(g, "g"), sel, m,
-                                     _stream()))
+    _check(load().ms2g_sketched_grad(plan.handle, factor, _kind(resampler), _dev(x, "x"), _dev(b, "b"), _dev(g, "g"),
+                                     sel, m, _stream()))
     return g
 
 
@@ -274,9 +281,9 @@ def denoise(plan: Plan, den, z, out=None):
     return out
 
 
-def _solve_desc(stages, option, n_subsets, seed, den, alpha, power_iters):
+def _solve_desc(stages, option, n_subsets, seed, den, alpha, power_iters, resampler="mean"):
     st = (Stage * len(stages))(*[Stage(*s) for s in stages])
-    desc = SolveDesc(st, len(stages), option, n_subsets, seed, _den(den), alpha, power_iters, 1)
+    desc = SolveDesc(st, len(stages), option, n_subsets, seed, _den(den), alpha, power_iters, 1, _kind(resampler))
     return desc, st
 
 
@@ -292,7 +299,7 @@ def schedule(plan: Plan | None, stages, option=1, n_subsets=1, seed=0):
 
 
 def pnp_ms2g_solve(plan: Plan, stages, b, x0=None, option=1, n_subsets=1, seed=0, den=("gauss", 0.8),
-                   alpha=0.5, power_iters=20, x_out=None, trace=False):
+                   alpha=0.5, power_iters=20, x_out=None, trace=False, resampler="mean"):
     """Algorithm 1 as one CUDA graph.  b: [batch][V_r][B].
 
     Device tensors in -> device tensor out.  Host (CPU) tensors are copied to
@@ -308,7 +315,7 @@ def pnp_ms2g_solve(plan: Plan, stages, b, x0=None, option=1, n_subsets=1, seed=0
     if x0_d is None:
         x0_d = torch.zeros((plan.batch, plan.n, plan.n), device=b_d.device, dtype=torch.float32)
     out_d = x_out if (x_out is not None and x_out.is_cuda) else torch.empty_like(x0_d)
-    desc, keep = _solve_desc(stages, option, n_subsets, seed, den, alpha, power_iters)
+    desc, keep = _solve_desc(stages, option, n_subsets, seed, den, alpha, power_iters, resampler)
     n_steps = len(schedule(plan, stages, option, n_subsets, seed))
     tr = (SchedEntry * max(1, n_steps))() if trace else None
     _check(load().ms2g_pnp_ms2g_solve(plan.handle, C.byref(desc), _dev(b_d, "b"), _dev(x0_d, "x0"),
@@ -324,9 +331,9 @@ def pnp_ms2g_solve(plan: Plan, stages, b, x0=None, option=1, n_subsets=1, seed=0
 
 
 def pnp_ms2g_solve_async(plan: Plan, stages, b, x0, x_out, option=1, n_subsets=1, seed=0, den=("gauss", 0.8),
-                         alpha=0.5, power_iters=20):
+                         alpha=0.5, power_iters=20, resampler="mean"):
     """Launch the cached solve graph on the current stream and return."""
-    desc, keep = _solve_desc(stages, option, n_subsets, seed, den, alpha, power_iters)
+    desc, keep = _solve_desc(stages, option, n_subsets, seed, den, alpha, power_iters, resampler)
     _check(load().ms2g_pnp_ms2g_solve_async(plan.handle, C.byref(desc), _dev(b, "b"), _dev(x0, "x0"),
                                             _dev(x_out, "x_out"), _stream()))
 

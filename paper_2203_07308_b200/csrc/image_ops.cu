@@ -5,6 +5,8 @@
 // These are HBM/L2-streaming kernels; one thread per
 // output pixel, coalesced along rows, 32x32 shared tiles for transposes.
 #include <climits>
+#include <cmath>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -65,6 +67,116 @@ int launch_up_step(int n, int s, int batch, const float* g, const float* y, cons
   const size_t total = (size_t)n * n * batch;
   k_up_step<<<grid1d(total), 256, 0, st>>>(g, y, eta_dev, eta, z, n, s, n / s, total);
   return check_launch("k_up_step");
+}
+
+// ------------------------------------------------------ bicubic (NEXT-1) --
+// The paper's S and U: MATLAB imresize, bicubic.  Keys cubic
+// convolution a = -0.5, centre-aligned samples u = (i + 0.5)/scale - 0.5,
+// kernel widened by the factor on downscale (antialiasing) with per-output
+// renormalisation, clamped boundary; separable (rows then columns).  The
+// per-output taps are tabulated on the host in fp64 once per plan.
+static double keys_cubic(double x) {
+  const double a = -0.5;
+  const double t = std::fabs(x);
+  if (t <= 1.0) return (a + 2.0) * t * t * t - (a + 3.0) * t * t + 1.0;
+  if (t < 2.0) return a * t * t * t - 5.0 * a * t * t + 8.0 * a * t - 4.0 * a;
+  return 0.0;
+}
+
+static void bicubic_table(int n_in, int n_out, double scale, int& taps, std::vector<int>& idx,
+                          std::vector<float>& w) {
+  const double ks = scale < 1.0 ? scale : 1.0;
+  const double support = 2.0 / ks;
+  taps = (int)std::ceil(2.0 * support) + 2;
+  idx.assign((size_t)n_out * taps, 0);
+  w.assign((size_t)n_out * taps, 0.f);
+  for (int o = 0; o < n_out; ++o) {
+    const double u = (o + 0.5) / scale - 0.5;
+    const int j0 = (int)std::floor(u - support);
+    std::vector<double> ww(taps, 0.0);
+    double sum = 0.0;
+    for (int k = 0; k < taps; ++k) {
+      const int j = j0 + k;
+      ww[k] = ks * keys_cubic(ks * (u - j));
+      sum += ww[k];
+      idx[(size_t)o * taps + k] = j < 0 ? 0 : (j > n_in - 1 ? n_in - 1 : j);
+    }
+    for (int k = 0; k < taps; ++k) w[(size_t)o * taps + k] = (float)(ww[k] / sum);
+  }
+}
+
+int build_bicubic_tables(FactorTables& f, int n) {
+  if (f.factor == 1) return MS2G_OK;
+  std::vector<int> idx;
+  std::vector<float> w;
+  bicubic_table(n, f.nc, 1.0 / f.factor, f.taps_down, idx, w);
+  MS2G_CUDA(cudaMalloc(&f.d_idx_down, sizeof(int) * idx.size()));
+  MS2G_CUDA(cudaMalloc(&f.d_w_down, sizeof(float) * w.size()));
+  MS2G_CUDA(cudaMemcpy(f.d_idx_down, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice));
+  MS2G_CUDA(cudaMemcpy(f.d_w_down, w.data(), sizeof(float) * w.size(), cudaMemcpyHostToDevice));
+  bicubic_table(f.nc, n, (double)f.factor, f.taps_up, idx, w);
+  MS2G_CUDA(cudaMalloc(&f.d_idx_up, sizeof(int) * idx.size()));
+  MS2G_CUDA(cudaMalloc(&f.d_w_up, sizeof(float) * w.size()));
+  MS2G_CUDA(cudaMemcpy(f.d_idx_up, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice));
+  MS2G_CUDA(cudaMemcpy(f.d_w_up, w.data(), sizeof(float) * w.size(), cudaMemcpyHostToDevice));
+  return MS2G_OK;
+}
+
+// rows pass: out[b][r][o] = sum_t w[o][t] in[b][r][idx[o][t]]   (rows x n_in -> rows x n_out)
+__global__ void k_rs_rows(const float* __restrict__ in, float* __restrict__ out, int rows, int n_in, int n_out,
+                          int taps, const int* __restrict__ idx, const float* __restrict__ w, size_t total) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e % n_out);
+    const size_t br = e / n_out;           // b * rows + r
+    const float* row = in + br * n_in;
+    float acc = 0.f;
+    for (int t = 0; t < taps; ++t) acc = fmaf(__ldg(w + o * taps + t), row[__ldg(idx + o * taps + t)], acc);
+    out[e] = acc;
+  }
+}
+
+// columns pass: val = sum_t w[o][t] in[b][idx[o][t]][c]; z = y - eta val (y != NULL) or val
+__global__ void k_rs_cols(const float* __restrict__ in, float* __restrict__ out, int cols, int n_in, int n_out,
+                          int taps, const int* __restrict__ idx, const float* __restrict__ w,
+                          const float* __restrict__ y, const float* __restrict__ eta_dev, float eta, size_t total) {
+  const float e_ = eta_dev ? *eta_dev : eta;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % cols);
+    const size_t bo = e / cols;
+    const int o = (int)(bo % n_out);
+    const size_t b = bo / n_out;
+    const float* base = in + b * (size_t)n_in * cols + c;
+    float acc = 0.f;
+    for (int t = 0; t < taps; ++t)
+      acc = fmaf(__ldg(w + o * taps + t), base[(size_t)__ldg(idx + o * taps + t) * cols], acc);
+    out[e] = y ? y[e] - e_ * acc : acc;
+  }
+}
+
+int launch_resample_down(ms2g_plan* p, const FactorTables& f, int kind, int batch, const float* x, float* v,
+                         cudaStream_t st) {
+  const int n = p->d.n;
+  if (kind == 0 || f.factor == 1) return launch_sketch_down(n, f.factor, batch, x, v, st);
+  const size_t t1 = (size_t)batch * n * f.nc;
+  k_rs_rows<<<grid1d(t1), 256, 0, st>>>(x, p->w_rs, n, n, f.nc, f.taps_down, f.d_idx_down, f.d_w_down, t1);
+  MS2G_TRY(check_launch("k_rs_rows"));
+  const size_t t2 = (size_t)batch * f.nc * f.nc;
+  k_rs_cols<<<grid1d(t2), 256, 0, st>>>(p->w_rs, v, f.nc, n, f.nc, f.taps_down, f.d_idx_down, f.d_w_down,
+                                        nullptr, nullptr, 0.f, t2);
+  return check_launch("k_rs_cols");
+}
+
+int launch_resample_up_step(ms2g_plan* p, const FactorTables& f, int kind, int batch, const float* g,
+                            const float* y, const float* eta_dev, float eta, float* z, cudaStream_t st) {
+  const int n = p->d.n;
+  if (kind == 0 || f.factor == 1) return launch_up_step(n, f.factor, batch, g, y, eta_dev, eta, z, st);
+  const size_t t1 = (size_t)batch * f.nc * n;
+  k_rs_rows<<<grid1d(t1), 256, 0, st>>>(g, p->w_rs, f.nc, f.nc, n, f.taps_up, f.d_idx_up, f.d_w_up, t1);
+  MS2G_TRY(check_launch("k_rs_rows"));
+  const size_t t2 = (size_t)batch * n * n;
+  k_rs_cols<<<grid1d(t2), 256, 0, st>>>(p->w_rs, z, n, f.nc, n, f.taps_up, f.d_idx_up, f.d_w_up, y, eta_dev, eta,
+                                        t2);
+  return check_launch("k_rs_cols");
 }
 
 // --------------------------------------------------- mix + momentum core --

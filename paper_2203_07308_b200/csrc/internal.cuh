@@ -54,6 +54,12 @@ struct FactorTables {
   ViewEntry* d_views = nullptr;   // [V_r]
   int bp_chunks = 1;              // view chunks of the backprojector
   int4* d_bpr = nullptr;          // per (32x32 tile, view): bin runs meeting the tile
+  // bicubic resampling tables (NEXT-1), [n_out][taps] clamped input index / weight
+  int taps_down = 0, taps_up = 0;
+  int* d_idx_down = nullptr;
+  float* d_w_down = nullptr;
+  int* d_idx_up = nullptr;
+  float* d_w_up = nullptr;
 };
 
 struct SolveGraph {
@@ -76,6 +82,7 @@ struct ms2g_plan {
   float2* w_pair = nullptr;            // forward gather images: 4 x [batch][n_c][n_c + 3] float2
   size_t pair_stride = 0;              // float2 elements per pair image
   float* w_v = nullptr;                // coarse sketch
+  float* w_rs = nullptr;               // separable-resampling intermediate [batch][n][n]
   float* w_G = nullptr;                // coarse gradient / backprojection
   float* w_res = nullptr;              // residual / projection [batch][V_r][B]
   float* w_part = nullptr;             // backprojection chunk partials
@@ -158,6 +165,12 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
 int launch_sketch_down(int n, int s, int batch, const float* x, float* v, cudaStream_t st);
 int launch_up_step(int n, int s, int batch, const float* g, const float* y, const float* eta_dev,
                    float eta, float* z, cudaStream_t st);
+// kind 0: average pool / replication; kind 1: bicubic (tables in f)
+int launch_resample_down(ms2g_plan* p, const FactorTables& f, int kind, int batch, const float* x, float* v,
+                         cudaStream_t st);
+int launch_resample_up_step(ms2g_plan* p, const FactorTables& f, int kind, int batch, const float* g,
+                            const float* y, const float* eta_dev, float eta, float* z, cudaStream_t st);
+int build_bicubic_tables(FactorTables& f, int n);
 int launch_gauss_mix_mom(int n, int batch, float sigma, const float* z, const float* xprev, float* xout,
                          float* yout, float alpha, float a, int mode, int* flag, int iter, cudaStream_t st);
 int launch_tv(int n, int batch, float lambda, float tau, int iters, const float* f, float* p0, float* p1,

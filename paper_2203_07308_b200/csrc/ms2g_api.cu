@@ -118,6 +118,7 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   MS2G_CUDA(cudaMalloc(&f.d_views, sizeof(ViewEntry) * views.size()));
   MS2G_CUDA(cudaMemcpy(f.d_rays, rays.data(), sizeof(RayEntry) * rays.size(), cudaMemcpyHostToDevice));
   MS2G_CUDA(cudaMemcpy(f.d_views, views.data(), sizeof(ViewEntry) * views.size(), cudaMemcpyHostToDevice));
+  MS2G_TRY(build_bicubic_tables(f, d.n));
   {  // adjoint tile/view bin ranges (geometry only, once per plan)
     const int tx = (nc + 31) / 32;
     int* d_err = nullptr;
@@ -152,9 +153,13 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(f.d_rays);
     cudaFree(f.d_views);
     cudaFree(f.d_bpr);
+    cudaFree(f.d_idx_down);
+    cudaFree(f.d_w_down);
+    cudaFree(f.d_idx_up);
+    cudaFree(f.d_w_up);
   }
   cudaFree(p->w_pair);
-  float* fl[] = {p->w_v, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
+  float* fl[] = {p->w_v, p->w_rs, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
                  p->w_y, p->w_z, p->w_p[0], p->w_p[1], p->w_etaf};
   for (float* q : fl) cudaFree(q);
   cudaFree(p->w_red);
@@ -208,12 +213,12 @@ static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
 }
 
 // g = c U_s A_s^T (A_s S_s x - b), into a full-resolution image.
-static int enqueue_grad(ms2g_plan* p, const FactorTables& f, const float* x, const float* b, float* g,
+static int enqueue_grad(ms2g_plan* p, const FactorTables& f, int kind, const float* x, const float* b, float* g,
                         const int* d_sel, int n_sel, float c, int batch, cudaStream_t st) {
-  const int n = p->d.n, s = f.factor;
+  const int s = f.factor;
   const float* v = x;
   if (s > 1) {
-    MS2G_TRY(launch_sketch_down(n, s, batch, x, p->w_v, st));  // v = S_s(y)
+    MS2G_TRY(launch_resample_down(p, f, kind, batch, x, p->w_v, st));  // v = S(y)
     v = p->w_v;
   }
   MS2G_TRY(launch_pair_prep(p, f.nc, batch, v, st));
@@ -221,7 +226,7 @@ static int enqueue_grad(ms2g_plan* p, const FactorTables& f, const float* x, con
   float* G = (s > 1) ? p->w_G : g;
   MS2G_TRY(launch_backward(p, f, p->w_res, G, c, 0, d_sel, n_sel, batch, st));      // G = c A_s^T r
   MS2G_TRY(allreduce(p, G, (size_t)f.nc * f.nc * batch, st));
-  if (s > 1) MS2G_TRY(launch_up_step(n, s, batch, G, nullptr, nullptr, -1.f, g, st));  // U_s G
+  if (s > 1) MS2G_TRY(launch_resample_up_step(p, f, kind, batch, G, nullptr, nullptr, 0.f, g, st));  // U G
   return MS2G_OK;
 }
 
@@ -372,14 +377,14 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
       const int s = f->factor;
       const float* v = p->w_y;
       if (s > 1) {
-        MS2G_TRY(launch_sketch_down(n, s, batch, p->w_y, p->w_v, st));
+        MS2G_TRY(launch_resample_down(p, *f, sd->resampler, batch, p->w_y, p->w_v, st));
         v = p->w_v;
       }
       MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
       MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st));
       MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
       MS2G_TRY(allreduce(p, p->w_G, (size_t)f->nc * f->nc * batch, st));
-      MS2G_TRY(launch_up_step(n, s, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
+      MS2G_TRY(launch_resample_up_step(p, *f, sd->resampler, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
       // x = (1-alpha) z + alpha D(z);  y = x + a_i (x - x_prev)
       MS2G_TRY(denoise_mix(p, sd->den, p->w_z, p->w_x[cur], p->w_x[cur ^ 1], p->w_y, sd->alpha, (float)e.a, 1,
                            e.i, batch, st));
@@ -395,7 +400,7 @@ static std::string solve_key(const ms2g_solve_desc* sd, const float* b, const fl
   std::ostringstream os;
   os << sd->n_stages << ':' << sd->option << ':' << sd->n_subsets << ':' << sd->seed << ':' << sd->den.kind << ':'
      << sd->den.sigma << ':' << sd->den.lambda << ':' << sd->den.tau << ':' << sd->den.inner_iters << ':'
-     << sd->alpha << ':' << sd->power_iters << ':' << (const void*)b << ':' << (const void*)x0 << ':'
+     << sd->alpha << ':' << sd->power_iters << ':' << sd->resampler << ':' << (const void*)b << ':' << (const void*)x0 << ':'
      << (const void*)x_out;
   for (int k = 0; k < sd->n_stages; ++k)
     os << '|' << sd->stages[k].factor << ',' << sd->stages[k].n_iters << ',' << sd->stages[k].n_epochs;
@@ -407,6 +412,7 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
   if (!b || !x0 || !x_out) return set_error(MS2G_ERR_INPUT, "NULL b/x0/x_out");
   if (!(sd->alpha > 0.f && sd->alpha <= 1.f)) return set_error(MS2G_ERR_CONFIG, "alpha must be in (0, 1] (S:197)");
   if (sd->power_iters < 1) return set_error(MS2G_ERR_CONFIG, "power_iters must be >= 1");
+  if (sd->resampler != 0 && sd->resampler != 1) return set_error(MS2G_ERR_CONFIG, "resampler must be 0 or 1");
   MS2G_TRY(check_denoiser(sd->den));
   std::vector<ms2g_sched_entry> sch;
   MS2G_TRY(make_schedule(p, sd, sch));
@@ -549,7 +555,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     free_plan(p);
     return set_error(MS2G_ERR_CUDA, std::string("pair image allocation: ") + cudaGetErrorString(e));
   }
-  if ((rc = alloc(&p->w_v, cimg)) ||
+  if ((rc = alloc(&p->w_v, cimg)) || (rc = alloc(&p->w_rs, fimg)) ||
       (rc = alloc(&p->w_G, cimg)) || (rc = alloc(&p->w_res, (size_t)p->V_r * p->B * bt)) ||
       (rc = alloc(&p->w_part, part)) || (rc = alloc(&p->w_x[0], fimg)) || (rc = alloc(&p->w_x[1], fimg)) ||
       (rc = alloc(&p->w_y, fimg)) || (rc = alloc(&p->w_z, fimg)) || (rc = alloc(&p->w_p[0], 2 * fimg)) ||
@@ -647,20 +653,30 @@ int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* im
   return MS2G_OK;
 }
 
-int ms2g_sketch_down(ms2g_plan* p, int32_t factor, const float* x, float* v, void* stream) {
+int ms2g_sketch_down(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, float* v, void* stream) {
   if (!p || !x || !v) return set_error(MS2G_ERR_INPUT, "NULL plan/x/v");
   if (factor < 1 || p->d.n % factor) return set_error(MS2G_ERR_CONFIG, "factor must divide n (S:127)");
-  return launch_sketch_down(p->d.n, factor, p->d.batch, x, v, (cudaStream_t)stream);
+  if (kind != 0 && kind != 1) return set_error(MS2G_ERR_CONFIG, "kind must be 0 (mean) or 1 (bicubic)");
+  if (kind == 0) return launch_sketch_down(p->d.n, factor, p->d.batch, x, v, (cudaStream_t)stream);
+  const FactorTables* f = find_factor(p, factor);
+  if (!f) return set_error(MS2G_ERR_CONFIG, "bicubic resampling needs the factor in the plan");
+  return launch_resample_down(p, *f, kind, p->d.batch, x, v, (cudaStream_t)stream);
 }
 
-int ms2g_sketch_up(ms2g_plan* p, int32_t factor, const float* g, const float* y, float eta, float* z, void* stream) {
+int ms2g_sketch_up(ms2g_plan* p, int32_t factor, int32_t kind, const float* g, const float* y, float eta, float* z,
+                   void* stream) {
   if (!p || !g || !z) return set_error(MS2G_ERR_INPUT, "NULL plan/g/z");
   if (factor < 1 || p->d.n % factor) return set_error(MS2G_ERR_CONFIG, "factor must divide n");
-  return launch_up_step(p->d.n, factor, p->d.batch, g, y, nullptr, y ? eta : 0.f, z, (cudaStream_t)stream);
+  if (kind != 0 && kind != 1) return set_error(MS2G_ERR_CONFIG, "kind must be 0 (replicate) or 1 (bicubic)");
+  if (kind == 0) return launch_up_step(p->d.n, factor, p->d.batch, g, y, nullptr, y ? eta : 0.f, z, (cudaStream_t)stream);
+  const FactorTables* f = find_factor(p, factor);
+  if (!f) return set_error(MS2G_ERR_CONFIG, "bicubic resampling needs the factor in the plan");
+  return launch_resample_up_step(p, *f, kind, p->d.batch, g, y, nullptr, y ? eta : 0.f, z, (cudaStream_t)stream);
 }
 
-int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* g,
+int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, const float* b, float* g,
                        const int32_t* subset, int32_t n_subset, void* stream) {
+  if (kind != 0 && kind != 1) return set_error(MS2G_ERR_CONFIG, "kind must be 0 or 1");
   if (!p || !x || !b || !g) return set_error(MS2G_ERR_INPUT, "NULL plan/x/b/g");
   const FactorTables* f = find_factor(p, factor);
   if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
@@ -670,7 +686,7 @@ int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, const float* x, const float
   int n_sel, n_glob;
   MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
   const float c = (float)((double)p->d.n_views / (double)n_glob);
-  return enqueue_grad(p, *f, x, b, g, d_sel, n_sel, c, p->d.batch, st);
+  return enqueue_grad(p, *f, kind, x, b, g, d_sel, n_sel, c, p->d.batch, st);
 }
 
 int ms2g_power_iteration(ms2g_plan* p, int32_t factor, int32_t iters, double* L, void* stream) {

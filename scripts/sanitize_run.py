@@ -22,6 +22,7 @@ for (n, V, B, fac, batch) in [(64, 30, 96, (2, 1), 1), (40, 12, 62, (2, 1), 2)]:
             P.sketched_grad(plan, s, x, b)
             P.sketched_grad(plan, s, x, b, subset=list(range(1, V, 4)))
             P.sketch_up(plan, s, P.back_project(plan, s, r), y=x, eta=0.1)
+            P.sketched_grad(plan, s, x, b, resampler="bicubic")
             P.power_iteration(plan, s, 3)
         for den in (("gauss", 0.8), ("tv", 0.02, 3), ("identity",)):
             P.denoise(plan, den, x)

@@ -386,3 +386,34 @@ def test_batched_forward_shares_traversal(P, nb):
                 assert np.array_equal(got[i], single)
             i = nb - 1
             assert rel(got[i], O.forward(g, s, xin[i], b=bs[i])) <= TOL_OP
+
+
+@pytest.mark.parametrize("s", [2, 4])
+def test_bicubic_resampling_parity(P, s):
+    """NEXT-1 bicubic S/U (P:156 imresize) against the oracle."""
+    n = 96
+    x = S.random_image(n, 60 + s)
+    with P.plan_geometry(n, 10, 150, factors=(s,)) as plan:
+        v = host(P.sketch_down(plan, s, dev(x)[None], resampler="bicubic"))[0]
+        assert rel(v, O.bicubic_down(x, s)) <= 1e-6
+        gc = S.random_image(n // s, 70 + s) - 0.5
+        up = host(P.sketch_up(plan, s, dev(gc)[None], resampler="bicubic"))[0]
+        assert rel(up, O.bicubic_up(gc, s)) <= 1e-6
+        y = S.random_image(n, 80)
+        z = host(P.sketch_up(plan, s, dev(gc)[None], y=dev(y)[None], eta=0.25, resampler="bicubic"))[0]
+        assert rel(z, y - np.float32(0.25) * O.bicubic_up(gc, s)) <= 1e-6
+
+
+def test_bicubic_sketched_grad_and_solve(P):
+    """Sketched gradient and a 3-stage solve with the paper's bicubic S/U."""
+    pr = S.PRESETS[2]
+    g, xt, b = _make_data(pr, 2)
+    x = S.phantom(pr.n, pr.n_ellipses, S.config_seed(2, 9))
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(4, 2, 1)) as plan:
+        for s in (4, 2):
+            got = host(P.sketched_grad(plan, s, dev(x)[None], dev(b)[None], resampler="bicubic"))[0]
+            assert rel(got, O.sketched_grad(g, s, x, b, resampler=1)) <= TOL_OP
+        stages = [(4, 6, 0), (2, 6, 0), (1, 4, 0)]
+        xo = host(P.pnp_ms2g_solve(plan, stages, dev(b)[None], den=pr.den, alpha=pr.alpha, resampler="bicubic"))[0]
+    xr, _, _ = O.pnp_ms2g(g, stages, b, den=pr.den, alpha=pr.alpha, resampler=1)
+    assert rel(xo, xr) <= TOL_SOLVE

@@ -188,7 +188,9 @@ def plan_geometry(n, n_views, n_bins, factors=(1,), fov=2.0, arc=2 * math.pi, so
     h = C.c_void_p()
     torch.cuda.current_device()
     _check(L.ms2g_plan_geometry(C.byref(desc), fs, len(factors), C.byref(h)))
-    return Plan(h, n, n_views, n_bins, factors, view_begin, view_end, batch, torch.device("cuda"))
+    plan = Plan(h, n, n_views, n_bins, factors, view_begin, view_end, batch, torch.device("cuda"))
+    plan.arc, plan.fov = arc, fov
+    return plan
 
 
 def _n_sel(plan: Plan, subset) -> int:

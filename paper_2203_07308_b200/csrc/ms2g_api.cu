@@ -207,7 +207,7 @@ static int resolve_subset(ms2g_plan* p, const int32_t* subset, int n_subset, cud
 }
 
 static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
-  if (!p->comm || p->nranks <= 1) return MS2G_OK;
+  if (!p->comm) return MS2G_OK;   // attached communicators are always used (1 rank: NCCL identity)
   MS2G_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, p->comm, st));
   return MS2G_OK;
 }

@@ -417,3 +417,24 @@ def test_bicubic_sketched_grad_and_solve(P):
         xo = host(P.pnp_ms2g_solve(plan, stages, dev(b)[None], den=pr.den, alpha=pr.alpha, resampler="bicubic"))[0]
     xr, _, _ = O.pnp_ms2g(g, stages, b, den=pr.den, alpha=pr.alpha, resampler=1)
     assert rel(xo, xr) <= TOL_SOLVE
+
+
+def test_nccl_attached_single_rank(P):
+    """The NCCL path (ncclCommInitRank + in-graph ncclAllReduce of the partial
+    adjoint) with a 1-rank communicator: results equal the unattached plan."""
+    n, V, B = 64, 45, 96
+    x = S.phantom(n, 6, 3)
+    b = S.random_sinogram((V, B), 4, zero_mean=False)
+    stages = [(2, 3, 0), (1, 2, 0)]
+    with P.plan_geometry(n, V, B, factors=(2, 1)) as a, P.plan_geometry(n, V, B, factors=(2, 1)) as c:
+        P.attach_nccl(c, 0, 1)
+        ga = host(P.sketched_grad(a, 2, dev(x)[None], dev(b)[None]))
+        gc = host(P.sketched_grad(c, 2, dev(x)[None], dev(b)[None]))
+        assert np.array_equal(ga, gc)
+        ra = host(P.back_project(a, 1, dev(b)[None]))
+        rc = host(P.back_project(c, 1, dev(b)[None], allreduce=True))
+        assert np.array_equal(ra, rc)
+        xa = host(P.pnp_ms2g_solve(a, stages, dev(b)[None], den=("gauss", 0.8), alpha=0.5))
+        xc = host(P.pnp_ms2g_solve(c, stages, dev(b)[None], den=("gauss", 0.8), alpha=0.5))
+        assert np.array_equal(xa, xc)
+        assert abs(P.power_iteration(a, 2, 5) - P.power_iteration(c, 2, 5)) == 0.0

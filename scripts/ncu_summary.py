@@ -62,7 +62,8 @@ def full(rep, out, traffic_json=None):
             def tob(w):
                 v = float(r[hdr.index(w)]); u = units[hdr.index(w)]
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-            traffic.setdefault(name.split("::")[-1], []).append(tob("dram__bytes_read.sum") + tob("dram__bytes_write.sum"))
+            key = name.split("::")[-1].replace("void ", "").split("<")[0].strip()
+            traffic.setdefault(key, []).append(tob("dram__bytes_read.sum") + tob("dram__bytes_write.sum"))
         except Exception:
             pass
     open(out, "w").write("\n".join(lines) + "\n")

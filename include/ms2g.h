@@ -137,14 +137,18 @@ int ms2g_denoise(ms2g_plan* plan, const ms2g_denoiser* den, const float* z, floa
 /* Algorithm 1.  Option 1: n_iters steps per stage on all views.
  * Option 2: n_epochs per stage, each epoch visits the n_subsets interleaved
  * view subsets {v : v mod n_subsets == k} in a Fisher-Yates order drawn from
- * one SplitMix64 stream seeded with `seed` (reading Z8/Z9; O13). */
+ * one SplitMix64 stream seeded with `seed` (reading Z8/Z9; O13).
+ * Option 3 (NEXT-4, "variance-reduced estimator ... SVRG"): the Option 2
+ * schedule with the SVRG estimator: at each epoch start xs = y and
+ * mu = A_s^T (A_s S xs - b) on all views; a step uses
+ * G = (V/|M|) A_M^T A_M S (y - xs) + mu. */
 typedef struct {
   int32_t factor, n_iters, n_epochs;
 } ms2g_stage;
 typedef struct {
   const ms2g_stage* stages;
   int32_t n_stages;
-  int32_t option;        /* 1 | 2                                         */
+  int32_t option;        /* 1 | 2 | 3 (SVRG)                              */
   int32_t n_subsets;     /* Option 2 only                                 */
   uint64_t seed;
   ms2g_denoiser den;

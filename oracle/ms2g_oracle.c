@@ -556,7 +556,7 @@ int orc_schedule(const orc_stage* st, int n_stages, int option, int n_subsets, u
           out[i - 1] = e;
         }
       }
-    } else if (option == 2) {
+    } else if (option == 2 || option == 3) {   /* 3 = SVRG on the same subset schedule */
       if (n_subsets < 1) { free(perm); return -1; }
       for (int ep = 0; ep < st[k].n_epochs; ++ep) {
         for (int q = 0; q < n_subsets; ++q) perm[q] = q;
@@ -617,6 +617,15 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
   double* z = (double*)malloc(sizeof(double) * np);
   double* dz = (double*)malloc(sizeof(double) * np);
   int* views = (int*)malloc(sizeof(int) * V);
+  /* Option 3 (NEXT-4, "stochastic variance-reduced gradient estimator",
+   * SVRG): at the start of every epoch the snapshot xs = y and its full
+   * sketched gradient mu = g_s(xs) are taken; a step on subset M uses
+   *   G = (V/|M|) U A_{s,M}^T A_{s,M} S (y - xs) + mu
+   * (= the SVRG estimator g_M(y) - g_M(xs) + g(xs) of the quadratic). */
+  double* xs = (option == 3) ? (double*)malloc(sizeof(double) * np) : NULL;
+  double* mu = (option == 3) ? (double*)malloc(sizeof(double) * np) : NULL;
+  double* dd = (option == 3) ? (double*)malloc(sizeof(double) * np) : NULL;
+  double* zero = (option == 3) ? (double*)calloc((size_t)V * g->n_bins, sizeof(double)) : NULL;
   memcpy(x, x0, sizeof(double) * np);
   memcpy(xp, x0, sizeof(double) * np);
   memcpy(y, x0, sizeof(double) * np);
@@ -631,6 +640,15 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
       int i = e.i;
       if (e.subset < 0) {
         orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, NULL, V, nthreads);
+      } else if (option == 3) {
+        if (j % n_subsets == 0) {                    /* epoch start: snapshot */
+          memcpy(xs, y, sizeof(double) * np);
+          orc_sketched_grad_kind(g, e.factor, g_resampler, xs, b, mu, NULL, V, nthreads);
+        }
+        for (size_t p = 0; p < np; ++p) dd[p] = y[p] - xs[p];
+        int m = orc_subset_views(V, n_subsets, e.subset, views);
+        orc_sketched_grad_kind(g, e.factor, g_resampler, dd, zero, gr, views, m, nthreads);
+        for (size_t p = 0; p < np; ++p) gr[p] += mu[p];
       } else {
         int m = orc_subset_views(V, n_subsets, e.subset, views);
         orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, views, m, nthreads);
@@ -655,5 +673,6 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
   }
   memcpy(x_out, x, sizeof(double) * np);
   free(sch); free(x); free(xp); free(y); free(gr); free(z); free(dz); free(views);
+  free(xs); free(mu); free(dd); free(zero);
   return rc;
 }

@@ -294,6 +294,18 @@ __global__ void k_tv_final(const float* __restrict__ f, const float* __restrict_
   }
 }
 
+// out = a x + b y  (SVRG difference / correction, NEXT-4)
+__global__ void k_axpby(float* __restrict__ out, const float* __restrict__ x, const float* __restrict__ y, float a,
+                        float b, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + b * y[i];
+}
+
+int launch_axpby(float* out, const float* x, const float* y, float a, float b, size_t count, cudaStream_t st) {
+  k_axpby<<<grid1d(count), 256, 0, st>>>(out, x, y, a, b, count);
+  return check_launch("k_axpby");
+}
+
 __global__ void k_fill(float* __restrict__ x, size_t count, float value) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
     x[i] = value;

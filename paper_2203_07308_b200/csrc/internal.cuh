@@ -90,6 +90,8 @@ struct ms2g_plan {
   float* w_x[2] = {nullptr, nullptr};  // iterate double buffer (full res)
   float* w_y = nullptr;                // extrapolated point
   float* w_z = nullptr;                // pre-denoiser point
+  float* w_snap = nullptr;             // SVRG snapshot (full res)
+  float* w_mu = nullptr;               // SVRG snapshot gradient (coarse)
   float* w_p[2] = {nullptr, nullptr};  // TV dual double buffer [batch][2][n][n]
   double* w_red = nullptr;             // reduction partials
   int red_blocks = 0;
@@ -179,6 +181,7 @@ int launch_tv(int n, int batch, float lambda, float tau, int iters, const float*
 int launch_copy_mix_mom(int n, int batch, const float* z, const float* xprev, float* xout, float* yout,
                         float a, int mode, int* flag, int iter, cudaStream_t st);
 int launch_fill(float* x, size_t count, float value, cudaStream_t st);
+int launch_axpby(float* out, const float* x, const float* y, float a, float b, size_t count, cudaStream_t st);
 int launch_power_step(int nc, int batch, const float* v, const float* w, double* red, int red_blocks,
                       double* pw, double* L_out, float* vnext, double* eta_out,
                       float* etaf_out, cudaStream_t st);

@@ -159,7 +159,7 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(f.d_w_up);
   }
   cudaFree(p->w_pair);
-  float* fl[] = {p->w_v, p->w_rs, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
+  float* fl[] = {p->w_v, p->w_rs, p->w_snap, p->w_mu, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
                  p->w_y, p->w_z, p->w_p[0], p->w_p[1], p->w_etaf};
   for (float* q : fl) cudaFree(q);
   cudaFree(p->w_red);
@@ -289,12 +289,12 @@ static int make_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, std::vec
   out.clear();
   if (!sd || !sd->stages || sd->n_stages < 1 || sd->n_stages > 63)
     return set_error(MS2G_ERR_CONFIG, "solve needs 1..63 stages");
-  if (sd->option != 1 && sd->option != 2) return set_error(MS2G_ERR_CONFIG, "option must be 1 or 2");
-  if (sd->option == 2 && (sd->n_subsets < 1 || (p && sd->n_subsets > p->d.n_views)))
+  if (sd->option < 1 || sd->option > 3) return set_error(MS2G_ERR_CONFIG, "option must be 1, 2 or 3");
+  if (sd->option >= 2 && (sd->n_subsets < 1 || (p && sd->n_subsets > p->d.n_views)))
     return set_error(MS2G_ERR_CONFIG, "n_subsets must be in [1, n_views]");
   uint64_t state = sd->seed;
   int i = 0;
-  std::vector<int> perm(sd->option == 2 ? sd->n_subsets : 1);
+  std::vector<int> perm(sd->option >= 2 ? sd->n_subsets : 1);
   for (int k = 0; k < sd->n_stages; ++k) {
     const ms2g_stage& st = sd->stages[k];
     if (st.factor < 1 || (p && p->d.n % st.factor != 0))
@@ -363,6 +363,7 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
     const ms2g_stage& stg = sd->stages[k];
     const FactorTables* f = find_factor(p, stg.factor);
     MS2G_TRY(enqueue_power(p, *f, sd->power_iters, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
+    int step_in_stage = 0;
     while (step < sch.size() && sch[step].stage == k) {
       const ms2g_sched_entry& e = sch[step];
       const int* d_sel = nullptr;
@@ -373,23 +374,53 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
         n_sel = p->subset_len[e.subset];
         c = (float)((double)p->d.n_views / (double)p->subset_global_len[e.subset]);
       }
-      // G-step: z = y - eta_k U_s (c A_s^T (A_s S_s y - b_M))
+      // G-step: z = y - eta_k U (c A_s^T (A_s S y - b_M))       (Options 1, 2)
+      //         z = y - eta_k U (c A_M^T A_M S (y - xs) + mu)  (Option 3, SVRG)
       const int s = f->factor;
-      const float* v = p->w_y;
-      if (s > 1) {
-        MS2G_TRY(launch_resample_down(p, *f, sd->resampler, batch, p->w_y, p->w_v, st));
-        v = p->w_v;
+      const size_t ncimg = (size_t)f->nc * f->nc * batch;
+      const int kind = sd->resampler;
+      if (sd->option == 3) {
+        if (step_in_stage % sd->n_subsets == 0) {   // epoch start: snapshot xs = y, mu = g_s(xs) (all views)
+          MS2G_CUDA(cudaMemcpyAsync(p->w_snap, p->w_y, sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
+          const float* vs = p->w_y;
+          if (s > 1) {
+            MS2G_TRY(launch_resample_down(p, *f, kind, batch, p->w_y, p->w_v, st));
+            vs = p->w_v;
+          }
+          MS2G_TRY(launch_pair_prep(p, f->nc, batch, vs, st));
+          MS2G_TRY(launch_forward(p, *f, b, p->w_res, nullptr, p->V_r, batch, st));
+          MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_mu, 1.f, 0, nullptr, p->V_r, batch, st));
+          MS2G_TRY(allreduce(p, p->w_mu, ncimg, st));
+        }
+        MS2G_TRY(launch_axpby(p->w_z, p->w_y, p->w_snap, 1.f, -1.f, img, st));   // d = y - xs
+        const float* vd = p->w_z;
+        if (s > 1) {
+          MS2G_TRY(launch_resample_down(p, *f, kind, batch, p->w_z, p->w_v, st));
+          vd = p->w_v;
+        }
+        MS2G_TRY(launch_pair_prep(p, f->nc, batch, vd, st));
+        MS2G_TRY(launch_forward(p, *f, nullptr, p->w_res, d_sel, n_sel, batch, st));
+        MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
+        MS2G_TRY(allreduce(p, p->w_G, ncimg, st));
+        MS2G_TRY(launch_axpby(p->w_G, p->w_G, p->w_mu, 1.f, 1.f, ncimg, st));  // + mu
+      } else {
+        const float* v = p->w_y;
+        if (s > 1) {
+          MS2G_TRY(launch_resample_down(p, *f, kind, batch, p->w_y, p->w_v, st));
+          v = p->w_v;
+        }
+        MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
+        MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st));
+        MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
+        MS2G_TRY(allreduce(p, p->w_G, ncimg, st));
       }
-      MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
-      MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st));
-      MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
-      MS2G_TRY(allreduce(p, p->w_G, (size_t)f->nc * f->nc * batch, st));
-      MS2G_TRY(launch_resample_up_step(p, *f, sd->resampler, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
+      MS2G_TRY(launch_resample_up_step(p, *f, kind, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
       // x = (1-alpha) z + alpha D(z);  y = x + a_i (x - x_prev)
       MS2G_TRY(denoise_mix(p, sd->den, p->w_z, p->w_x[cur], p->w_x[cur ^ 1], p->w_y, sd->alpha, (float)e.a, 1,
                            e.i, batch, st));
       cur ^= 1;
       ++step;
+      ++step_in_stage;
     }
   }
   MS2G_CUDA(cudaMemcpyAsync(x_out, p->w_x[cur], sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
@@ -421,7 +452,7 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
       return set_error(MS2G_ERR_CONFIG, "stage factor was not planned (ms2g_plan_geometry factors)");
   if (!find_factor(p, 1) && p->nmax_c < p->d.n)
     return set_error(MS2G_ERR_CONFIG, "the solve needs full-resolution workspaces: plan factor 1 as well");
-  if (sd->option == 2) MS2G_TRY(prepare_subsets(p, sd->n_subsets));
+  if (sd->option >= 2) MS2G_TRY(prepare_subsets(p, sd->n_subsets));
   const std::string key = solve_key(sd, b, x0, x_out);
   if (key != p->sg.key || !p->sg.exec) {
     if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
@@ -555,7 +586,8 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     free_plan(p);
     return set_error(MS2G_ERR_CUDA, std::string("pair image allocation: ") + cudaGetErrorString(e));
   }
-  if ((rc = alloc(&p->w_v, cimg)) || (rc = alloc(&p->w_rs, fimg)) ||
+  if ((rc = alloc(&p->w_v, cimg)) || (rc = alloc(&p->w_rs, fimg)) || (rc = alloc(&p->w_snap, fimg)) ||
+      (rc = alloc(&p->w_mu, cimg)) ||
       (rc = alloc(&p->w_G, cimg)) || (rc = alloc(&p->w_res, (size_t)p->V_r * p->B * bt)) ||
       (rc = alloc(&p->w_part, part)) || (rc = alloc(&p->w_x[0], fimg)) || (rc = alloc(&p->w_x[1], fimg)) ||
       (rc = alloc(&p->w_y, fimg)) || (rc = alloc(&p->w_z, fimg)) || (rc = alloc(&p->w_p[0], 2 * fimg)) ||

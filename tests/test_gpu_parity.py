@@ -438,3 +438,20 @@ def test_nccl_attached_single_rank(P):
         xc = host(P.pnp_ms2g_solve(c, stages, dev(b)[None], den=("gauss", 0.8), alpha=0.5))
         assert np.array_equal(xa, xc)
         assert abs(P.power_iteration(a, 2, 5) - P.power_iteration(c, 2, 5)) == 0.0
+
+
+def test_svrg_option3_solve(P):
+    """NEXT-4 SVRG estimator (Option 3) on the C3-shaped subset schedule:
+    GPU solve vs the oracle, bit-exact schedule."""
+    n, V, B = 128, 160, 192
+    g = O.Geometry(n, V, B)
+    xt = S.phantom(n, 12, S.config_seed(3))
+    b = S.gaussian_data(O.forward(g, 1, xt), 0.01, S.config_seed(3))
+    stages = [(4, 0, 1), (2, 0, 1), (1, 0, 1)]
+    with P.plan_geometry(n, V, B, factors=(4, 2, 1)) as plan:
+        xo, tr = P.pnp_ms2g_solve(plan, stages, dev(b)[None], option=3, n_subsets=8, seed=7, den=("tv", 0.01, 10),
+                                  alpha=1.0, trace=True)
+        xo = host(xo)[0]
+    xr, trr, _ = O.pnp_ms2g(g, stages, b, option=3, n_subsets=8, seed=7, den=("tv", 0.01, 10), alpha=1.0)
+    assert [e[:4] for e in tr] == [e[:4] for e in trr]
+    assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)

@@ -61,7 +61,7 @@ def test_schedule_random_descriptions(P):
     for _ in range(50):
         ns = int(rng.integers(1, 5))
         stages = [(int(rng.integers(1, 5)), int(rng.integers(0, 7)), int(rng.integers(0, 4))) for _ in range(ns)]
-        opt = int(rng.integers(1, 3)); nsub = int(rng.integers(1, 12)); seed = int(rng.integers(0, 2**63))
+        opt = int(rng.integers(1, 4)); nsub = int(rng.integers(1, 12)); seed = int(rng.integers(0, 2**63))
         assert P.schedule(None, stages, opt, nsub, seed) == O.schedule(stages, opt, nsub, seed)
 
 

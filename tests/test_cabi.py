@@ -67,7 +67,7 @@ def test_schedule_random_descriptions(P):
 
 def test_schedule_config_errors(P):
     with pytest.raises(P.MS2GError) as e:
-        P.schedule(None, [(2, 3, 0)], option=3)
+        P.schedule(None, [(2, 3, 0)], option=4)
     assert e.value.code == 2
     with pytest.raises(P.MS2GError):
         P.schedule(None, [(0, 3, 0)])

@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
                                                        int partial) {
   __shared__ float acc[kBW][2][kTS];
   __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
-  __shared__ float2 st2[kBW][33];
+  __shared__ float4 st2[kBW][33];   // {Ly32, r, ~S, -}
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
         const long long Ft = Rn.F0 + (long long)c0 * (long long)Rn.S - ((long long)mb << 32);
         st4[warp][lane] = make_float4(__uint_as_float((unsigned)Ft), __uint_as_float((unsigned)(Ft >> 32)),
                                       __uint_as_float(Rn.S), Rn.Lc);
-        st2[warp][lane] = make_float2(Rn.Ly32, rn);
+        st2[warp][lane] = make_float4(Rn.Ly32, rn, __uint_as_float(~Rn.S), 0.f);
       }
     }
     __syncwarp();
@@ -341,23 +341,19 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
     const int sstride = mir ? -4 * kBT : 4 * kBT;
     const int nrays = min(32, cte - ctb + 1);
     const float4* p4 = st4[warp];
-    const float2* p2 = st2[warp];
+    const float4* p2 = st2[warp];
     float4 a = p4[0];
-    float2 b2 = p2[0];
+    float4 b2 = p2[0];
     for (int q = 0; q < nrays; ++q) {
       const float4 an = p4[q + 1];
-      const float2 bn = p2[q + 1];
-      unsigned lo, hi, hi1;
-      asm("{\n\t.reg .u64 ft, f, f1, s64;\n\t"
-          "mov.b64 ft, {%3, %4};\n\t"
-          "cvt.u64.u32 s64, %6;\n\t"
-          "mad.wide.u32 f, %5, %6, ft;\n\t"
-          "add.u64 f1, f, s64;\n\t"
-          "mov.b64 {%0, %1}, f;\n\t"
-          "{\n\t.reg .u32 t;\n\tmov.b64 {t, %2}, f1;\n\t}\n\t}"
-          : "=r"(lo), "=r"(hi), "=r"(hi1)
-          : "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)), "r"((unsigned)lane), "r"(__float_as_uint(a.z)));
-      const bool cross = hi1 != hi;
+      const float4 bn = p2[q + 1];
+      // F = Ft + lane * S as (lo, hi); the column crosses a grid line iff
+      // lo + S carries, i.e. lo > ~S
+      unsigned lo, hi;
+      asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;"
+          : "=r"(lo), "=r"(hi)
+          : "r"((unsigned)lane), "r"(__float_as_uint(a.z)), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
+      const bool cross = lo > __float_as_uint(b2.z);
       float w0, w1;
       seg_weights(lo, cross, a.w, b2.x, w0, w1);
       const unsigned ad0 = sbase + hi * (unsigned)sstride;

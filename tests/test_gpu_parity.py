@@ -455,3 +455,20 @@ def test_svrg_option3_solve(P):
     xr, trr, _ = O.pnp_ms2g(g, stages, b, option=3, n_subsets=8, seed=7, den=("tv", 0.01, 10), alpha=1.0)
     assert [e[:4] for e in tr] == [e[:4] for e in trr]
     assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)
+
+
+@pytest.mark.parametrize("nb", [2, 4, 3])
+def test_batched_backward_shares_traversal(P, nb):
+    """Batch plans backproject each image like a single-image plan (pairs of
+    images share one traversal) and match the oracle."""
+    n, V, B = 96, 60, 144
+    g = O.Geometry(n, V, B)
+    rs = np.stack([S.random_sinogram((V, B), 90 + i) for i in range(nb)]).astype(np.float32)
+    with P.plan_geometry(n, V, B, factors=(2, 1), batch=nb) as plan, \
+            P.plan_geometry(n, V, B, factors=(2, 1), batch=1) as one:
+        for s in (2, 1):
+            got = host(P.back_project(plan, s, dev(rs)))
+            for i in range(nb):
+                single = host(P.back_project(one, s, dev(rs[i])[None]))[0]
+                assert rel(got[i], single) <= 1e-6
+            assert rel(got[nb - 1], O.backward(g, s, rs[nb - 1])) <= TOL_OP

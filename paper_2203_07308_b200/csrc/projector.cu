@@ -234,33 +234,32 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
   return check_launch("k_bp_ranges");
 }
 
-// NB images of a batch share one traversal (C5: weights computed once per
-// (ray, column) and applied to NB sinograms / accumulators); NW warps per block.
-template <int NB, int NW>
-__global__ void __launch_bounds__(32 * NW) k_backward(const RayEntry* __restrict__ rays,
+__global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restrict__ rays,
                                                        const int4* __restrict__ ranges, int V_r, int B,
                                                        const int* __restrict__ sel, int n_sel, int vpc,
                                                        const float* __restrict__ sino, float* __restrict__ out,
                                                        int nc, int tiles_x, float scale, int accumulate,
                                                        int partial) {
-  __shared__ float acc[NW][NB][2][kTS];
-  __shared__ float4 st4[NW][33];   // entry 32 is a pipeline pad
-  __shared__ float4 st2[NW][33];   // {Ly32, r_0, ~S, r_1}
+  __shared__ float acc[kBW][2][kTS];
+  __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
+  __shared__ float4 st2[kBW][33];   // {Ly32, r, ~S, -}
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kBT, y0 = ty * kBT;
-  float* TX = acc[warp][0][0];
-  float* TY = acc[warp][0][1];
-  for (int i = lane; i < NB * 2 * kTS; i += 32) TX[i] = 0.f;
+  float* TX = acc[warp][0];
+  float* TY = acc[warp][1];
+  for (int i = lane; i < kTS; i += 32) {
+    TX[i] = 0.f;
+    TY[i] = 0.f;
+  }
   __syncwarp();
   const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
-  const float* sb = sino + (size_t)bz * NB * n_sel * B;
-  const size_t sstep = (size_t)n_sel * B;   // sinogram stride between batch images
+  const float* sb = sino + (size_t)bz * n_sel * B;
   const int4* trange = ranges + (size_t)tile * V_r;
 
   // ---- round iterator: (view k, run, [tb, te]) of this warp ----
-  int vbase = kb + warp - 32 * NW;      // first view of the current 32-view batch
+  int vbase = kb + warp - 32 * kBW;     // first view of the current 32-view batch
   int g_lane = 0;                       // rank-local view held by this lane for the batch
   int4 rr_lane = make_int4(0, 0, 0, 0); // its range record
   int j = 31;                           // index of the current view within the batch
@@ -273,14 +272,14 @@ __global__ void __launch_bounds__(32 * NW) k_backward(const RayEntry* __restrict
       if (run >= nr) {
         ++j;
         if (j == 32) {                    // load the next batch of 32 views (lane j <-> view)
-          vbase += 32 * NW;
+          vbase += 32 * kBW;
           if (vbase >= ke) return false;
-          const int kk = vbase + lane * NW;
+          const int kk = vbase + lane * kBW;
           g_lane = (kk < ke) ? (sel ? __ldg(sel + kk) : kk) : 0;
           rr_lane = (kk < ke) ? __ldg(trange + g_lane) : make_int4(0, 0, 0, 0);
           j = 0;
         }
-        k = vbase + j * NW;
+        k = vbase + j * kBW;
         if (k >= ke) return false;
         g = __shfl_sync(0xffffffffu, g_lane, j);
         const int rx = __shfl_sync(0xffffffffu, rr_lane.x, j);
@@ -307,12 +306,11 @@ __global__ void __launch_bounds__(32 * NW) k_backward(const RayEntry* __restrict
   bool have = next_round();
   // prefetch the first round
   RayEntry Rn;
-  float rn = 0.f, rn1 = 0.f;
+  float rn = 0.f;
   int tn = tb + lane;
   if (have && tn <= te) {
     Rn = rays[(size_t)g * B + tn];
     rn = __ldg(sb + (size_t)k * B + tn);
-    if (NB == 2) rn1 = __ldg(sb + sstep + (size_t)k * B + tn);
   }
   while (have) {
     // commit the prefetched round to shared memory (tile-relative coordinate)
@@ -324,7 +322,7 @@ __global__ void __launch_bounds__(32 * NW) k_backward(const RayEntry* __restrict
         const long long Ft = Rn.F0 + (long long)c0 * (long long)Rn.S - ((long long)mb << 32);
         st4[warp][lane] = make_float4(__uint_as_float((unsigned)Ft), __uint_as_float((unsigned)(Ft >> 32)),
                                       __uint_as_float(Rn.S), Rn.Lc);
-        st2[warp][lane] = make_float4(Rn.Ly32, rn, __uint_as_float(~Rn.S), rn1);
+        st2[warp][lane] = make_float4(Rn.Ly32, rn, __uint_as_float(~Rn.S), 0.f);
       }
     }
     __syncwarp();
@@ -334,7 +332,6 @@ __global__ void __launch_bounds__(32 * NW) k_backward(const RayEntry* __restrict
     if (have && tn <= te) {
       Rn = rays[(size_t)g * B + tn];
       rn = __ldg(sb + (size_t)k * B + tn);
-      if (NB == 2) rn1 = __ldg(sb + sstep + (size_t)k * B + tn);
     }
     const bool majY = ccls & kMajorY, mir = ccls & kMirror;
     // cell (local minor l, lane) -> T[phys_minor * 32 + lane], phys_minor = mir ? 31 - l : l
@@ -373,19 +370,6 @@ __global__ void __launch_bounds__(32 * NW) k_backward(const RayEntry* __restrict
                    "@p0 st.shared.f32 [%0], c0;\n\t"
                    "@p1 st.shared.f32 [%1], c1;\n\t}"
                    :: "r"(ad0), "r"(ad1), "f"(w0), "f"(w1), "f"(b2.y), "r"(v0), "r"(v1) : "memory");
-      if (NB == 2) {
-        constexpr unsigned kImg = 2u * kTS * 4u;   // byte stride between the images' accumulators
-        asm volatile("{\n\t.reg .pred p0, p1;\n\t.reg .f32 c0, c1;\n\t"
-                     "setp.ne.u32 p0, %5, 0;\n\t"
-                     "setp.ne.u32 p1, %6, 0;\n\t"
-                     "@p0 ld.shared.f32 c0, [%0];\n\t"
-                     "@p1 ld.shared.f32 c1, [%1];\n\t"
-                     "@p0 fma.rn.f32 c0, %2, %4, c0;\n\t"
-                     "@p1 fma.rn.f32 c1, %3, %4, c1;\n\t"
-                     "@p0 st.shared.f32 [%0], c0;\n\t"
-                     "@p1 st.shared.f32 [%1], c1;\n\t}"
-                     :: "r"(ad0 + kImg), "r"(ad1 + kImg), "f"(w0), "f"(w1), "f"(b2.w), "r"(v0), "r"(v1) : "memory");
-      }
       a = an;
       b2 = bn;
     }
@@ -393,20 +377,18 @@ __global__ void __launch_bounds__(32 * NW) k_backward(const RayEntry* __restrict
   }
   __syncthreads();
   const size_t np = (size_t)nc * nc;
-  for (int idx = threadIdx.x; idx < NB * kBT * kBT; idx += blockDim.x) {
-    const int im = idx / (kBT * kBT);
-    const int ly = (idx / kBT) % kBT, lx = idx % kBT;
+  for (int idx = threadIdx.x; idx < kBT * kBT; idx += blockDim.x) {
+    const int ly = idx / kBT, lx = idx % kBT;
     const int yy = y0 + ly, xx = x0 + lx;
     if (yy < nc && xx < nc) {
       float s = 0.f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) s += acc[w][im][0][ly * kBT + lx] + acc[w][im][1][lx * kBT + ly];
+      for (int w = 0; w < kBW; ++w) s += acc[w][0][ly * kBT + lx] + acc[w][1][lx * kBT + ly];
       const size_t o = (size_t)yy * nc + xx;
-      const int b_img = bz * NB + im;
       if (partial) {
-        out[((size_t)b_img * gridDim.y + chunk) * np + o] = s;
+        out[((size_t)bz * gridDim.y + chunk) * np + o] = s;
       } else {
-        float* dst = out + (size_t)b_img * np + o;
+        float* dst = out + (size_t)bz * np + o;
         float v = scale * s;
         if (accumulate) v += *dst;
         *dst = v;
@@ -431,22 +413,15 @@ __global__ void k_chunk_reduce(const float* __restrict__ part, int nchunks, size
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s) {
   const int tiles_x = (f.nc + kBT - 1) / kBT;
-  const int nb = (batch % 2 == 0) ? 2 : 1;          // images sharing one traversal
-  const int nw = nb == 2 ? 2 : kBW;                  // warps per block (shared-memory budget)
   int nchunks = f.bp_chunks;
-  const int max_chunks = (n_sel + nw - 1) / nw;
+  const int max_chunks = (n_sel + kBW - 1) / kBW;
   if (nchunks > max_chunks) nchunks = max_chunks;
   if (nchunks < 1) nchunks = 1;
   const int vpc = (n_sel + nchunks - 1) / nchunks;
   const int partial = nchunks > 1;
-  dim3 grid(tiles_x * tiles_x, nchunks, batch / nb);
-  float* dst = partial ? p->w_part : img;
-  if (nb == 2)
-    k_backward<2, 2><<<grid, 64, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino, dst, f.nc,
-                                         tiles_x, scale, accumulate, partial);
-  else
-    k_backward<1, kBW><<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino, dst,
-                                                 f.nc, tiles_x, scale, accumulate, partial);
+  dim3 grid(tiles_x * tiles_x, nchunks, batch);
+  k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino,
+                                       partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
   MS2G_TRY(check_launch("k_backward"));
   if (partial) {
     const size_t np = (size_t)f.nc * f.nc, total = np * batch;

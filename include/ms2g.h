@@ -141,15 +141,19 @@ int ms2g_denoise(ms2g_plan* plan, const ms2g_denoiser* den, const float* z, floa
  * Option 3 (NEXT-4, "variance-reduced estimator ... SVRG"): the Option 2
  * schedule with the SVRG estimator: at each epoch start xs = y and
  * mu = A_s^T (A_s S xs - b) on all views; a step uses
- * G = (V/|M|) A_M^T A_M S (y - xs) + mu. */
+ * G = (V/|M|) A_M^T A_M S (y - xs) + mu.
+ * Option 4 (NEXT-4, "randomly sampled minibatch", "uniformly
+ * sampled"): n_iters steps per stage, each on m = n_subsets views drawn
+ * uniformly without replacement (partial Fisher-Yates on the SplitMix64
+ * stream), scaled by V/m; ms2g_schedule_views returns a step's views. */
 typedef struct {
   int32_t factor, n_iters, n_epochs;
 } ms2g_stage;
 typedef struct {
   const ms2g_stage* stages;
   int32_t n_stages;
-  int32_t option;        /* 1 | 2 | 3 (SVRG)                              */
-  int32_t n_subsets;     /* Option 2 only                                 */
+  int32_t option;        /* 1 | 2 | 3 (SVRG) | 4 (uniform minibatches)      */
+  int32_t n_subsets;     /* Options 2/3: subsets; Option 4: views per step */
   uint64_t seed;
   ms2g_denoiser den;
   float alpha;           /* RED-PRO mix weight, 0 < alpha <= 1      */
@@ -170,6 +174,12 @@ typedef struct {
  * checked); no device is touched. */
 int ms2g_schedule(const ms2g_plan* plan, const ms2g_solve_desc* desc, ms2g_sched_entry* out, int32_t cap,
                   int32_t* n_out);
+
+/* Host-only: the ascending GLOBAL view indices used by schedule step `step`
+ * (0-based): all views (Option 1), interleaved subset (Options 2/3) or the
+ * drawn minibatch (Option 4).  *n_out = their count; <= cap are written. */
+int ms2g_schedule_views(const ms2g_plan* plan, const ms2g_solve_desc* desc, int32_t step, int32_t* out,
+                        int32_t cap, int32_t* n_out);
 
 /* Whole PnP-MS2G solve, captured once as a CUDA graph per (plan, desc,
  * pointers) and replayed: per stage the power iteration, then per step

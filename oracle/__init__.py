@@ -92,6 +92,8 @@ def lib():
         _lib.orc_momentum.restype = d
         _lib.orc_schedule.argtypes = [C.POINTER(_Stage), i, i, i, C.c_uint64, C.POINTER(SchedEntry), i]
         _lib.orc_schedule.restype = i
+        _lib.orc_minibatch_views.argtypes = [i, i, C.c_uint64, i, p]
+        _lib.orc_minibatch_views.restype = i
         _lib.orc_subset_views.argtypes = [i, i, i, p]
         _lib.orc_subset_views.restype = i
         _lib.orc_pnp_ms2g.argtypes = [G, C.POINTER(_Stage), i, i, i, C.c_uint64, i, d, d, d, i, d, i,
@@ -306,6 +308,15 @@ def schedule(stages, option: int = 1, n_subsets: int = 1, seed: int = 0):
     buf = (SchedEntry * max(n, 1))()
     lib().orc_schedule(st, len(stages), option, n_subsets, seed, buf, n)
     return [buf[k].as_tuple() for k in range(n)]
+
+
+def minibatch_views(n_views: int, m: int, seed: int, n_steps: int):
+    """Option 4: per step m distinct views, uniform without replacement (partial
+    Fisher-Yates on one SplitMix64 stream), ascending.  Shape (n_steps, m)."""
+    out = np.zeros((max(n_steps, 1), m), dtype=np.int32)
+    if lib().orc_minibatch_views(n_views, m, seed, n_steps, _ptr(out)) != 0:
+        raise ValueError("bad minibatch size")
+    return out[:n_steps].copy()
 
 
 def subset_views(n_views: int, n_subsets: int, k: int):

@@ -548,11 +548,11 @@ int orc_schedule(const orc_stage* st, int n_stages, int option, int n_subsets, u
   int i = 0;
   int* perm = (int*)malloc(sizeof(int) * (n_subsets > 0 ? n_subsets : 1));
   for (int k = 0; k < n_stages; ++k) {
-    if (option == 1) {
+    if (option == 1 || option == 4) {
       for (int j = 0; j < st[k].n_iters; ++j) {
         ++i;
         if (i <= cap) {
-          orc_sched_entry e = {i, k, st[k].factor, -1, 0.0, orc_momentum(i)};
+          orc_sched_entry e = {i, k, st[k].factor, option == 4 ? i - 1 : -1, 0.0, orc_momentum(i)};
           out[i - 1] = e;
         }
       }
@@ -579,6 +579,31 @@ int orc_schedule(const orc_stage* st, int n_stages, int option, int n_subsets, u
   }
   free(perm);
   return i;
+}
+
+/* Option 4 (NEXT-4; "M_i is a randomly sampled minibatch", P:98
+ * "uniformly sampled minibatch"): every step draws m distinct
+ * views uniformly without replacement -- a partial Fisher-Yates shuffle of
+ * [0..V-1] (for q < m: j = q + next() mod (V - q), swap) driven by one
+ * SplitMix64 stream seeded with `seed` -- and uses them in ascending order.
+ * out receives n_steps * m view indices, step-major.                       */
+static int cmp_int(const void* a, const void* b) { return (*(const int*)a > *(const int*)b) - (*(const int*)a < *(const int*)b); }
+
+int orc_minibatch_views(int V, int m, uint64_t seed, int n_steps, int* out) {
+  if (m < 1 || m > V) return -1;
+  uint64_t state = seed;
+  int* arr = (int*)malloc(sizeof(int) * V);
+  for (int st = 0; st < n_steps; ++st) {
+    for (int q = 0; q < V; ++q) arr[q] = q;
+    for (int q = 0; q < m; ++q) {
+      int j = q + (int)(orc_splitmix64(&state) % (uint64_t)(V - q));
+      int tmp = arr[q]; arr[q] = arr[j]; arr[j] = tmp;
+    }
+    qsort(arr, m, sizeof(int), cmp_int);
+    memcpy(out + (size_t)st * m, arr, sizeof(int) * m);
+  }
+  free(arr);
+  return 0;
 }
 
 /* subset k = { v : v mod n_subsets == k }  ("8 interleaved subsets") */
@@ -626,6 +651,12 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
   double* mu = (option == 3) ? (double*)malloc(sizeof(double) * np) : NULL;
   double* dd = (option == 3) ? (double*)malloc(sizeof(double) * np) : NULL;
   double* zero = (option == 3) ? (double*)calloc((size_t)V * g->n_bins, sizeof(double)) : NULL;
+  /* Option 4: n_subsets carries the minibatch size m (views per step) */
+  int* mb = NULL;
+  if (option == 4) {
+    mb = (int*)malloc(sizeof(int) * (size_t)(total > 0 ? total : 1) * n_subsets);
+    if (orc_minibatch_views(V, n_subsets, seed, total, mb) != 0) { free(mb); free(sch); return 2; }
+  }
   memcpy(x, x0, sizeof(double) * np);
   memcpy(xp, x0, sizeof(double) * np);
   memcpy(y, x0, sizeof(double) * np);
@@ -634,12 +665,15 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
     double L = orc_power_iteration(g, st[k].factor, power_iters, nthreads);
     double eta = 1.0 / L;
     if (etas) etas[k] = eta;
-    int nk = (option == 1) ? st[k].n_iters : st[k].n_epochs * n_subsets;
+    int nk = (option == 1 || option == 4) ? st[k].n_iters : st[k].n_epochs * n_subsets;
     for (int j = 0; j < nk; ++j, ++step) {
       orc_sched_entry e = sch[step];
       int i = e.i;
       if (e.subset < 0) {
         orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, NULL, V, nthreads);
+      } else if (option == 4) {
+        orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, mb + (size_t)step * n_subsets, n_subsets,
+                               nthreads);
       } else if (option == 3) {
         if (j % n_subsets == 0) {                    /* epoch start: snapshot */
           memcpy(xs, y, sizeof(double) * np);
@@ -673,6 +707,6 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
   }
   memcpy(x_out, x, sizeof(double) * np);
   free(sch); free(x); free(xp); free(y); free(gr); free(z); free(dz); free(views);
-  free(xs); free(mu); free(dd); free(zero);
+  free(xs); free(mu); free(dd); free(zero); free(mb);
   return rc;
 }

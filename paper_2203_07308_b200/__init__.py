@@ -95,6 +95,7 @@ def load():
     L.ms2g_denoise.argtypes = [p, C.POINTER(Denoiser), p, p, p]
     L.ms2g_schedule.argtypes = [p, C.POINTER(SolveDesc), C.POINTER(SchedEntry), i, C.POINTER(C.c_int32)]
     L.ms2g_pnp_ms2g_solve.argtypes = [p, C.POINTER(SolveDesc), p, p, p, C.POINTER(SchedEntry), p]
+    L.ms2g_schedule_views.argtypes = [p, C.POINTER(SolveDesc), i, C.POINTER(C.c_int32), i, C.POINTER(C.c_int32)]
     L.ms2g_pnp_ms2g_solve_async.argtypes = [p, C.POINTER(SolveDesc), p, p, p, p]
     L.ms2g_solve_status.argtypes = [p, p]
     L.ms2g_last_error.restype = C.c_char_p
@@ -298,6 +299,16 @@ def schedule(plan: Plan | None, stages, option=1, n_subsets=1, seed=0):
     buf = (SchedEntry * max(1, n.value))()
     _check(load().ms2g_schedule(h, C.byref(desc), buf, n.value, C.byref(n)))
     return [buf[k].as_tuple() for k in range(n.value)]
+
+
+def schedule_views(plan: Plan, stages, step: int, option=1, n_subsets=1, seed=0):
+    """Global view indices used by schedule step `step` (host only)."""
+    desc, keep = _solve_desc(stages, option, n_subsets, seed, ("identity",), 1.0, 20)
+    n = C.c_int32(0)
+    _check(load().ms2g_schedule_views(plan.handle, C.byref(desc), step, None, 0, C.byref(n)))
+    buf = (C.c_int32 * max(1, n.value))()
+    _check(load().ms2g_schedule_views(plan.handle, C.byref(desc), step, buf, n.value, C.byref(n)))
+    return [buf[k] for k in range(n.value)]
 
 
 def pnp_ms2g_solve(plan: Plan, stages, b, x0=None, option=1, n_subsets=1, seed=0, den=("gauss", 0.8),

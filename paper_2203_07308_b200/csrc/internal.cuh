@@ -103,6 +103,8 @@ struct ms2g_plan {
   int* h_sel = nullptr;                // pinned host staging for subsets
   cudaEvent_t sel_ev = nullptr;
   int* w_subsets = nullptr;            // precomputed Option-2 subset lists
+  int* w_mb = nullptr;                 // precomputed Option-4 minibatch lists
+  std::vector<int> mb_off, mb_len;
   std::vector<int> subset_off, subset_len, subset_global_len;
   int subsets_n = 0;
   // NCCL

@@ -1,6 +1,7 @@
 // ms2g_api.cu -- C ABI of libms2g (include/ms2g.h): plan, geometry tables,
 // operator entry points, schedule, power iteration and the graph-captured
 // PnP-MS2G solve.  Host code only; kernels live in projector.cu/image_ops.cu.
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -168,6 +169,7 @@ static void free_plan(ms2g_plan* p) {
   cudaFree(p->w_flag);
   cudaFree(p->w_sel);
   cudaFree(p->w_subsets);
+  cudaFree(p->w_mb);
   if (p->h_sel) cudaFreeHost(p->h_sel);
   if (p->sel_ev) cudaEventDestroy(p->sel_ev);
   if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
@@ -289,9 +291,9 @@ static int make_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, std::vec
   out.clear();
   if (!sd || !sd->stages || sd->n_stages < 1 || sd->n_stages > 63)
     return set_error(MS2G_ERR_CONFIG, "solve needs 1..63 stages");
-  if (sd->option < 1 || sd->option > 3) return set_error(MS2G_ERR_CONFIG, "option must be 1, 2 or 3");
+  if (sd->option < 1 || sd->option > 4) return set_error(MS2G_ERR_CONFIG, "option must be 1, 2, 3 or 4");
   if (sd->option >= 2 && (sd->n_subsets < 1 || (p && sd->n_subsets > p->d.n_views)))
-    return set_error(MS2G_ERR_CONFIG, "n_subsets must be in [1, n_views]");
+    return set_error(MS2G_ERR_CONFIG, "n_subsets (option 4: views per minibatch) must be in [1, n_views]");
   uint64_t state = sd->seed;
   int i = 0;
   std::vector<int> perm(sd->option >= 2 ? sd->n_subsets : 1);
@@ -299,11 +301,11 @@ static int make_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, std::vec
     const ms2g_stage& st = sd->stages[k];
     if (st.factor < 1 || (p && p->d.n % st.factor != 0))
       return set_error(MS2G_ERR_CONFIG, "stage factor must divide n (S:127)");
-    if (sd->option == 1) {
+    if (sd->option == 1 || sd->option == 4) {
       if (st.n_iters < 0) return set_error(MS2G_ERR_CONFIG, "n_iters must be >= 0");
       for (int j = 0; j < st.n_iters; ++j) {
         ++i;
-        out.push_back({i, k, st.factor, -1, 0.0, (double)(i - 1) / (double)(i + 3)});
+        out.push_back({i, k, st.factor, sd->option == 4 ? i - 1 : -1, 0.0, (double)(i - 1) / (double)(i + 3)});
       }
     } else {
       if (st.n_epochs < 0) return set_error(MS2G_ERR_CONFIG, "n_epochs must be >= 0");
@@ -320,6 +322,47 @@ static int make_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, std::vec
       }
     }
   }
+  return MS2G_OK;
+}
+
+// Option 4: per step m distinct views drawn uniformly without
+// replacement by a partial Fisher-Yates shuffle of [0..V-1] on one SplitMix64
+// stream, ascending (independent of the oracle's copy; compared bit-exactly).
+static void minibatch_views(int V, int m, uint64_t seed, int n_steps, std::vector<int>& out) {
+  uint64_t state = seed;
+  std::vector<int> arr(V);
+  out.assign((size_t)n_steps * m, 0);
+  for (int st = 0; st < n_steps; ++st) {
+    for (int q = 0; q < V; ++q) arr[q] = q;
+    for (int q = 0; q < m; ++q) {
+      const int j = q + (int)(splitmix64(state) % (uint64_t)(V - q));
+      std::swap(arr[q], arr[j]);
+    }
+    std::sort(arr.begin(), arr.begin() + m);
+    std::copy(arr.begin(), arr.begin() + m, out.begin() + (size_t)st * m);
+  }
+}
+
+// Upload the per-step minibatch lists (rank-local) of an Option-4 solve.
+static int prepare_minibatches(ms2g_plan* p, const ms2g_solve_desc* sd, int n_steps) {
+  std::vector<int> g;
+  minibatch_views(p->d.n_views, sd->n_subsets, sd->seed, n_steps, g);
+  std::vector<int> all;
+  p->mb_off.assign(n_steps, 0);
+  p->mb_len.assign(n_steps, 0);
+  for (int st = 0; st < n_steps; ++st) {
+    p->mb_off[st] = (int)all.size();
+    for (int q = 0; q < sd->n_subsets; ++q) {
+      const int v = g[(size_t)st * sd->n_subsets + q];
+      if (v >= p->d.view_begin && v < p->d.view_end) all.push_back(v - p->d.view_begin);
+    }
+    p->mb_len[st] = (int)all.size() - p->mb_off[st];
+  }
+  cudaFree(p->w_mb);
+  p->w_mb = nullptr;
+  MS2G_CUDA(cudaMalloc(&p->w_mb, sizeof(int) * (all.size() + 1)));
+  if (!all.empty()) MS2G_CUDA(cudaMemcpy(p->w_mb, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice));
+  p->subsets_n = 0;   // the interleaved-subset cache is independent
   return MS2G_OK;
 }
 
@@ -369,7 +412,11 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
       const int* d_sel = nullptr;
       int n_sel = p->V_r;
       float c = 1.f;
-      if (e.subset >= 0) {
+      if (sd->option == 4) {
+        d_sel = p->w_mb + p->mb_off[step];
+        n_sel = p->mb_len[step];
+        c = (float)((double)p->d.n_views / (double)sd->n_subsets);
+      } else if (e.subset >= 0) {
         d_sel = p->w_subsets + p->subset_off[e.subset];
         n_sel = p->subset_len[e.subset];
         c = (float)((double)p->d.n_views / (double)p->subset_global_len[e.subset]);
@@ -452,8 +499,9 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
       return set_error(MS2G_ERR_CONFIG, "stage factor was not planned (ms2g_plan_geometry factors)");
   if (!find_factor(p, 1) && p->nmax_c < p->d.n)
     return set_error(MS2G_ERR_CONFIG, "the solve needs full-resolution workspaces: plan factor 1 as well");
-  if (sd->option >= 2) MS2G_TRY(prepare_subsets(p, sd->n_subsets));
+  if (sd->option == 2 || sd->option == 3) MS2G_TRY(prepare_subsets(p, sd->n_subsets));
   const std::string key = solve_key(sd, b, x0, x_out);
+  if (sd->option == 4 && (key != p->sg.key || !p->sg.exec)) MS2G_TRY(prepare_minibatches(p, sd, (int)sch.size()));
   if (key != p->sg.key || !p->sg.exec) {
     if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
     if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
@@ -745,6 +793,32 @@ int ms2g_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, ms2g_sched_entr
   MS2G_TRY(make_schedule(p, sd, sch));
   if (n_out) *n_out = (int32_t)sch.size();
   for (size_t k = 0; k < sch.size() && (int)k < cap && out; ++k) out[k] = sch[k];
+  return MS2G_OK;
+}
+
+int ms2g_schedule_views(const ms2g_plan* p, const ms2g_solve_desc* sd, int32_t step, int32_t* out, int32_t cap,
+                        int32_t* n_out) {
+  if (!p || !sd) return set_error(MS2G_ERR_INPUT, "NULL plan/desc");
+  std::vector<ms2g_sched_entry> sch;
+  MS2G_TRY(make_schedule(p, sd, sch));
+  if (step < 0 || step >= (int)sch.size()) return set_error(MS2G_ERR_INPUT, "step out of range");
+  std::vector<int> v;
+  int m = 0;
+  if (sd->option == 1) {
+    m = p->d.n_views;
+    v.resize(m);
+    for (int q = 0; q < m; ++q) v[q] = q;
+  } else if (sd->option == 4) {
+    std::vector<int> g;
+    minibatch_views(p->d.n_views, sd->n_subsets, sd->seed, step + 1, g);
+    m = sd->n_subsets;
+    v.assign(g.begin() + (size_t)step * m, g.begin() + (size_t)(step + 1) * m);
+  } else {
+    for (int q = sch[step].subset; q < p->d.n_views; q += sd->n_subsets) v.push_back(q);
+    m = (int)v.size();
+  }
+  if (n_out) *n_out = m;
+  for (int q = 0; q < m && q < cap && out; ++q) out[q] = v[q];
   return MS2G_OK;
 }
 

@@ -472,3 +472,22 @@ def test_batched_backward_shares_traversal(P, nb):
                 single = host(P.back_project(one, s, dev(rs[i])[None]))[0]
                 assert rel(got[i], single) <= 1e-6
             assert rel(got[nb - 1], O.backward(g, s, rs[nb - 1])) <= TOL_OP
+
+
+def test_option4_uniform_minibatch_solve(P):
+    """NEXT-4 uniform random view minibatches (Option 4): the per-step view
+    lists are bit-exact with the oracle's and the solve matches it."""
+    n, V, B = 128, 120, 192
+    g = O.Geometry(n, V, B)
+    xt = S.phantom(n, 12, 41)
+    b = S.gaussian_data(O.forward(g, 1, xt), 0.01, 41)
+    stages = [(4, 6, 0), (2, 6, 0), (1, 4, 0)]
+    m, seed = 17, 99
+    ref_views = O.minibatch_views(V, m, seed, 16)
+    with P.plan_geometry(n, V, B, factors=(4, 2, 1)) as plan:
+        for st in (0, 5, 15):
+            assert P.schedule_views(plan, stages, st, option=4, n_subsets=m, seed=seed) == ref_views[st].tolist()
+        xo = host(P.pnp_ms2g_solve(plan, stages, dev(b)[None], option=4, n_subsets=m, seed=seed,
+                                   den=("gauss", 0.8), alpha=0.5))[0]
+    xr, _, _ = O.pnp_ms2g(g, stages, b, option=4, n_subsets=m, seed=seed, den=("gauss", 0.8), alpha=0.5)
+    assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)

@@ -145,14 +145,17 @@ int ms2g_denoise(ms2g_plan* plan, const ms2g_denoiser* den, const float* z, floa
  * Option 4 (NEXT-4, "randomly sampled minibatch", "uniformly
  * sampled"): n_iters steps per stage, each on m = n_subsets views drawn
  * uniformly without replacement (partial Fisher-Yates on the SplitMix64
- * stream), scaled by V/m; ms2g_schedule_views returns a step's views. */
+ * stream), scaled by V/m; ms2g_schedule_views returns a step's views.
+ * Option 5 (NEXT-4, "SAGA"): the Option 2 schedule with a table of
+ * the K scaled subset gradients (filled at every stage start); a step on
+ * subset j uses G = new - phi_j + mean(phi) and stores phi_j = new. */
 typedef struct {
   int32_t factor, n_iters, n_epochs;
 } ms2g_stage;
 typedef struct {
   const ms2g_stage* stages;
   int32_t n_stages;
-  int32_t option;        /* 1 | 2 | 3 (SVRG) | 4 (uniform minibatches)      */
+  int32_t option;        /* 1 | 2 | 3 SVRG | 4 uniform minibatches | 5 SAGA */
   int32_t n_subsets;     /* Options 2/3: subsets; Option 4: views per step */
   uint64_t seed;
   ms2g_denoiser den;

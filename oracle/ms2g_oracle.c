@@ -556,7 +556,7 @@ int orc_schedule(const orc_stage* st, int n_stages, int option, int n_subsets, u
           out[i - 1] = e;
         }
       }
-    } else if (option == 2 || option == 3) {   /* 3 = SVRG on the same subset schedule */
+    } else if (option == 2 || option == 3 || option == 5) {   /* 3 SVRG, 5 SAGA: same subset schedule */
       if (n_subsets < 1) { free(perm); return -1; }
       for (int ep = 0; ep < st[k].n_epochs; ++ep) {
         for (int q = 0; q < n_subsets; ++q) perm[q] = q;
@@ -651,6 +651,13 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
   double* mu = (option == 3) ? (double*)malloc(sizeof(double) * np) : NULL;
   double* dd = (option == 3) ? (double*)malloc(sizeof(double) * np) : NULL;
   double* zero = (option == 3) ? (double*)calloc((size_t)V * g->n_bins, sizeof(double)) : NULL;
+  /* Option 5 (NEXT-4, "SAGA"): table phi_k of the scaled subset
+   * gradients g_k = (V/|M_k|) U A_{s,M_k}^T (A_{s,M_k} S y - b_{M_k}), filled
+   * at every stage start with all K subsets at the current y; a step on
+   * subset j with new = g_j(y) uses G = new - phi_j + mean_k phi_k and then
+   * stores phi_j = new.                                                    */
+  double* phi = (option == 5) ? (double*)malloc(sizeof(double) * np * (size_t)n_subsets) : NULL;
+  double* pavg = (option == 5) ? (double*)malloc(sizeof(double) * np) : NULL;
   /* Option 4: n_subsets carries the minibatch size m (views per step) */
   int* mb = NULL;
   if (option == 4) {
@@ -666,6 +673,15 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
     double eta = 1.0 / L;
     if (etas) etas[k] = eta;
     int nk = (option == 1 || option == 4) ? st[k].n_iters : st[k].n_epochs * n_subsets;
+    if (option == 5 && nk > 0) {              /* SAGA table at the stage start */
+      for (size_t p = 0; p < np; ++p) pavg[p] = 0.0;
+      for (int q = 0; q < n_subsets; ++q) {
+        int m = orc_subset_views(V, n_subsets, q, views);
+        double* ph = phi + np * (size_t)q;
+        orc_sketched_grad_kind(g, st[k].factor, g_resampler, y, b, ph, views, m, nthreads);
+        for (size_t p = 0; p < np; ++p) pavg[p] += ph[p] / n_subsets;
+      }
+    }
     for (int j = 0; j < nk; ++j, ++step) {
       orc_sched_entry e = sch[step];
       int i = e.i;
@@ -674,6 +690,16 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
       } else if (option == 4) {
         orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, mb + (size_t)step * n_subsets, n_subsets,
                                nthreads);
+      } else if (option == 5) {
+        int m = orc_subset_views(V, n_subsets, e.subset, views);
+        double* ph = phi + np * (size_t)e.subset;
+        orc_sketched_grad_kind(g, e.factor, g_resampler, y, b, gr, views, m, nthreads);   /* new */
+        for (size_t p = 0; p < np; ++p) {
+          double d = gr[p] - ph[p];
+          ph[p] = gr[p];
+          gr[p] = d + pavg[p];
+          pavg[p] += d / n_subsets;
+        }
       } else if (option == 3) {
         if (j % n_subsets == 0) {                    /* epoch start: snapshot */
           memcpy(xs, y, sizeof(double) * np);
@@ -707,6 +733,6 @@ int orc_pnp_ms2g(const orc_geom* g, const orc_stage* st, int n_stages, int optio
   }
   memcpy(x_out, x, sizeof(double) * np);
   free(sch); free(x); free(xp); free(y); free(gr); free(z); free(dz); free(views);
-  free(xs); free(mu); free(dd); free(zero); free(mb);
+  free(xs); free(mu); free(dd); free(zero); free(mb); free(phi); free(pavg);
   return rc;
 }

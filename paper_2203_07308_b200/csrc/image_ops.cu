@@ -306,6 +306,23 @@ int launch_axpby(float* out, const float* x, const float* y, float a, float b, s
   return check_launch("k_axpby");
 }
 
+// SAGA update (NEXT-4, Option 5): d = new - phi_j; phi_j = new;
+// G = d + avg (into `nw`); avg += d / K
+__global__ void k_saga(float* __restrict__ nw, float* __restrict__ phi, float* __restrict__ avg, float invK,
+                       size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    const float n_ = nw[i], d = n_ - phi[i];
+    phi[i] = n_;
+    nw[i] = d + avg[i];
+    avg[i] += d * invK;
+  }
+}
+
+int launch_saga(float* nw, float* phi, float* avg, int K, size_t count, cudaStream_t st) {
+  k_saga<<<grid1d(count), 256, 0, st>>>(nw, phi, avg, 1.f / (float)K, count);
+  return check_launch("k_saga");
+}
+
 __global__ void k_fill(float* __restrict__ x, size_t count, float value) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
     x[i] = value;

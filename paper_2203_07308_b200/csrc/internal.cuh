@@ -104,6 +104,8 @@ struct ms2g_plan {
   cudaEvent_t sel_ev = nullptr;
   int* w_subsets = nullptr;            // precomputed Option-2 subset lists
   int* w_mb = nullptr;                 // precomputed Option-4 minibatch lists
+  float* w_saga = nullptr;             // Option-5 table: K coarse gradients + their mean
+  size_t saga_elems = 0;
   std::vector<int> mb_off, mb_len;
   std::vector<int> subset_off, subset_len, subset_global_len;
   int subsets_n = 0;
@@ -184,6 +186,7 @@ int launch_copy_mix_mom(int n, int batch, const float* z, const float* xprev, fl
                         float a, int mode, int* flag, int iter, cudaStream_t st);
 int launch_fill(float* x, size_t count, float value, cudaStream_t st);
 int launch_axpby(float* out, const float* x, const float* y, float a, float b, size_t count, cudaStream_t st);
+int launch_saga(float* nw, float* phi, float* avg, int K, size_t count, cudaStream_t st);
 int launch_power_step(int nc, int batch, const float* v, const float* w, double* red, int red_blocks,
                       double* pw, double* L_out, float* vnext, double* eta_out,
                       float* etaf_out, cudaStream_t st);

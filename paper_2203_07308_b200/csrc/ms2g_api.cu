@@ -170,6 +170,7 @@ static void free_plan(ms2g_plan* p) {
   cudaFree(p->w_sel);
   cudaFree(p->w_subsets);
   cudaFree(p->w_mb);
+  cudaFree(p->w_saga);
   if (p->h_sel) cudaFreeHost(p->h_sel);
   if (p->sel_ev) cudaEventDestroy(p->sel_ev);
   if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
@@ -291,7 +292,7 @@ static int make_schedule(const ms2g_plan* p, const ms2g_solve_desc* sd, std::vec
   out.clear();
   if (!sd || !sd->stages || sd->n_stages < 1 || sd->n_stages > 63)
     return set_error(MS2G_ERR_CONFIG, "solve needs 1..63 stages");
-  if (sd->option < 1 || sd->option > 4) return set_error(MS2G_ERR_CONFIG, "option must be 1, 2, 3 or 4");
+  if (sd->option < 1 || sd->option > 5) return set_error(MS2G_ERR_CONFIG, "option must be 1..5");
   if (sd->option >= 2 && (sd->n_subsets < 1 || (p && sd->n_subsets > p->d.n_views)))
     return set_error(MS2G_ERR_CONFIG, "n_subsets (option 4: views per minibatch) must be in [1, n_views]");
   uint64_t state = sd->seed;
@@ -407,6 +408,27 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
     const FactorTables* f = find_factor(p, stg.factor);
     MS2G_TRY(enqueue_power(p, *f, sd->power_iters, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
     int step_in_stage = 0;
+    if (sd->option == 5 && step < sch.size() && sch[step].stage == k) {
+      // SAGA table at the stage start: phi_q = c_q A_{M_q}^T (A_{M_q} S y - b), avg = mean_q phi_q
+      const size_t ncimg = (size_t)f->nc * f->nc * batch;
+      float* avg = p->w_saga + (size_t)sd->n_subsets * ncimg;
+      MS2G_TRY(launch_fill(avg, ncimg, 0.f, st));
+      const float* v = p->w_y;
+      if (f->factor > 1) {
+        MS2G_TRY(launch_resample_down(p, *f, sd->resampler, batch, p->w_y, p->w_v, st));
+        v = p->w_v;
+      }
+      MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
+      for (int q = 0; q < sd->n_subsets; ++q) {
+        float* ph = p->w_saga + (size_t)q * ncimg;
+        const float cq = (float)((double)p->d.n_views / (double)p->subset_global_len[q]);
+        MS2G_TRY(launch_forward(p, *f, b, p->w_res, p->w_subsets + p->subset_off[q], p->subset_len[q], batch, st));
+        MS2G_TRY(launch_backward(p, *f, p->w_res, ph, cq, 0, p->w_subsets + p->subset_off[q], p->subset_len[q],
+                                 batch, st));
+        MS2G_TRY(allreduce(p, ph, ncimg, st));
+        MS2G_TRY(launch_axpby(avg, avg, ph, 1.f, 1.f / (float)sd->n_subsets, ncimg, st));
+      }
+    }
     while (step < sch.size() && sch[step].stage == k) {
       const ms2g_sched_entry& e = sch[step];
       const int* d_sel = nullptr;
@@ -460,6 +482,9 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
         MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st));
         MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
         MS2G_TRY(allreduce(p, p->w_G, ncimg, st));
+        if (sd->option == 5)   // G = new - phi_j + avg; phi_j = new; avg += (new - phi_j)/K
+          MS2G_TRY(launch_saga(p->w_G, p->w_saga + (size_t)e.subset * ncimg,
+                               p->w_saga + (size_t)sd->n_subsets * ncimg, sd->n_subsets, ncimg, st));
       }
       MS2G_TRY(launch_resample_up_step(p, *f, kind, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
       // x = (1-alpha) z + alpha D(z);  y = x + a_i (x - x_prev)
@@ -499,7 +524,17 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
       return set_error(MS2G_ERR_CONFIG, "stage factor was not planned (ms2g_plan_geometry factors)");
   if (!find_factor(p, 1) && p->nmax_c < p->d.n)
     return set_error(MS2G_ERR_CONFIG, "the solve needs full-resolution workspaces: plan factor 1 as well");
-  if (sd->option == 2 || sd->option == 3) MS2G_TRY(prepare_subsets(p, sd->n_subsets));
+  if (sd->option == 2 || sd->option == 3 || sd->option == 5) MS2G_TRY(prepare_subsets(p, sd->n_subsets));
+  if (sd->option == 5) {   // SAGA table (allocated outside capture)
+    const size_t need = (size_t)(sd->n_subsets + 1) * p->nmax_c * p->nmax_c * p->d.batch;
+    if (need > p->saga_elems) {
+      cudaFree(p->w_saga);
+      p->w_saga = nullptr;
+      p->saga_elems = 0;
+      MS2G_CUDA(cudaMalloc(&p->w_saga, sizeof(float) * need));
+      p->saga_elems = need;
+    }
+  }
   const std::string key = solve_key(sd, b, x0, x_out);
   if (sd->option == 4 && (key != p->sg.key || !p->sg.exec)) MS2G_TRY(prepare_minibatches(p, sd, (int)sch.size()));
   if (key != p->sg.key || !p->sg.exec) {

@@ -61,13 +61,13 @@ def test_schedule_random_descriptions(P):
     for _ in range(50):
         ns = int(rng.integers(1, 5))
         stages = [(int(rng.integers(1, 5)), int(rng.integers(0, 7)), int(rng.integers(0, 4))) for _ in range(ns)]
-        opt = int(rng.integers(1, 5)); nsub = int(rng.integers(1, 12)); seed = int(rng.integers(0, 2**63))
+        opt = int(rng.integers(1, 6)); nsub = int(rng.integers(1, 12)); seed = int(rng.integers(0, 2**63))
         assert P.schedule(None, stages, opt, nsub, seed) == O.schedule(stages, opt, nsub, seed)
 
 
 def test_schedule_config_errors(P):
     with pytest.raises(P.MS2GError) as e:
-        P.schedule(None, [(2, 3, 0)], option=5)
+        P.schedule(None, [(2, 3, 0)], option=6)
     assert e.value.code == 2
     with pytest.raises(P.MS2GError):
         P.schedule(None, [(0, 3, 0)])

@@ -491,3 +491,18 @@ def test_option4_uniform_minibatch_solve(P):
                                    den=("gauss", 0.8), alpha=0.5))[0]
     xr, _, _ = O.pnp_ms2g(g, stages, b, option=4, n_subsets=m, seed=seed, den=("gauss", 0.8), alpha=0.5)
     assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)
+
+
+def test_saga_option5_solve(P):
+    """NEXT-4 SAGA estimator (Option 5) on the interleaved-subset schedule:
+    GPU solve vs the oracle."""
+    n, V, B = 128, 160, 192
+    g = O.Geometry(n, V, B)
+    xt = S.phantom(n, 12, S.config_seed(3, 2))
+    b = S.gaussian_data(O.forward(g, 1, xt), 0.01, S.config_seed(3, 2))
+    stages = [(4, 0, 2), (2, 0, 1), (1, 0, 1)]
+    with P.plan_geometry(n, V, B, factors=(4, 2, 1)) as plan:
+        xo = host(P.pnp_ms2g_solve(plan, stages, dev(b)[None], option=5, n_subsets=8, seed=11,
+                                   den=("tv", 0.01, 10), alpha=1.0))[0]
+    xr, _, _ = O.pnp_ms2g(g, stages, b, option=5, n_subsets=8, seed=11, den=("tv", 0.01, 10), alpha=1.0)
+    assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)

@@ -32,3 +32,16 @@ def test_svrg_estimator_unbiased_over_partition():
     est = sum(O.sketched_grad(g, 2, y - xs, zero, views=O.subset_views(V, K, k)) for k in range(K)) / K + mu
     full = O.sketched_grad(g, 2, y, b)
     assert np.max(np.abs(est - full)) <= 1e-12 * np.max(np.abs(full))
+
+
+def test_saga_single_subset_equals_option1():
+    """SAGA (Option 5) with one subset: new - phi + mean(phi) = new, the
+    full gradient -> Option-1 iterates."""
+    n, V, B = 32, 24, 48
+    g = O.Geometry(n, V, B)
+    b = np.random.default_rng(0).random((V, B))
+    x5, _, _ = O.pnp_ms2g(g, [(2, 0, 2), (1, 0, 1)], b, option=5, n_subsets=1, seed=1, den=("gauss", 0.8),
+                          alpha=0.5)
+    x1, _, _ = O.pnp_ms2g(g, [(2, 2, 0), (1, 1, 0)], b, option=1, den=("gauss", 0.8), alpha=0.5)
+    assert np.max(np.abs(x5 - x1)) <= 1e-12 * np.max(np.abs(x1))
+

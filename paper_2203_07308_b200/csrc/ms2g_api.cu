@@ -3,6 +3,7 @@
 // PnP-MS2G solve.  Host code only; kernels live in projector.cu/image_ops.cu.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -136,10 +137,14 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     if (rc != MS2G_OK) return rc;
     if (herr) return set_error(MS2G_ERR_CONFIG, "a tile's shadow spans more than 2 ray classes (fan too wide)");
   }
-  // backprojector view chunks: enough blocks for ~4 waves of 148 SMs
+  // backprojector view chunks: enough blocks that the last partial wave is a
+  // small fraction of the launch (measured on B200, C4: 8 waves for 1024^2,
+  // 24 waves for coarser grids; the chunk partials are summed by
+  // k_chunk_reduce in fixed order)
   const int tiles_x = (nc + 31) / 32;
   const long long tiles = (long long)tiles_x * tiles_x * d.batch;
-  const long long target = 4LL * sm_count;
+  const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : (tiles >= 1024 ? 8 : 24);
+  const long long target = waves * sm_count;
   long long ch = (target + tiles - 1) / tiles;
   const long long maxch = (V_r + 3) / 4;
   if (ch > maxch) ch = maxch;

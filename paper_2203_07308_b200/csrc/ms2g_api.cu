@@ -85,10 +85,12 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
         m0c = (double)nc - m0c;
       }
       R.F0 = llround(m0c * kFix);
-      const long long Sq = llround(slope * kFix);          // slope in [0, 1]; 1 only at exactly 45 deg
-      R.S = (unsigned)(Sq > 0xFFFFFFFFLL ? 0xFFFFFFFFLL : Sq);
+      // slope in [0, 1]; 1 only at exactly 45 deg.  S >= 1 (a slope below
+      // 2^-32 is rounded up to 2^-32): the end-coordinate weights need S > 0.
+      const long long Sq = llround(slope * kFix);
+      R.S = (unsigned)(Sq > 0xFFFFFFFFLL ? 0xFFFFFFFFLL : (Sq < 1 ? 1 : Sq));
       R.Lc = (float)Lc;
-      R.Ly32 = R.S ? (float)(Lc / slope / kFix) : 0.f;
+      R.Ly32 = (float)(Lc / (double)R.S);                  // length per 2^-32 of minor travel
       R.flags = flags;
       R.pad = 0;
       if (flags != prev_cls) {                              // a new run of one ray class

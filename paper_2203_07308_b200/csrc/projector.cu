@@ -157,11 +157,96 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
   }
 }
 
+
+// End-coordinate form (v4).  Per column c the ray's minor coordinate runs from
+// F(c) to E(c) = F(c) + S.  With u = floor(E) + 1 (the pair index k of the
+// (lower, upper) rows k = floor(E) - 1, floor(E), shifted by the pair images'
+// 2-element pad) and m = min(frac32(E), S) (the part of the step above the
+// grid line floor(E); m = S when the column does not cross a line),
+//   upper row: m Ly32,   lower row: Lc - m Ly32,
+// so  sum_c w.x = Lc * sum_c x_lower + Ly32 * sum_c m (x_upper - x_lower):
+// the per-ray constants Lc, Ly32 leave the column loop.  Without a crossing
+// the lower-row weight is a rounding residual (|.| <= 2^-23 Lc), not an exact
+// zero; the adjoint uses the same formula, so the pair stays a transpose.
+template <int NB>
+__global__ void __launch_bounds__(256) k_forward_e(const RayEntry* __restrict__ rays, int B, int V_r,
+                                                   const int* __restrict__ sel, int n_sel,
+                                                   const float2* __restrict__ pairs, size_t pair_stride, int nc,
+                                                   const float* __restrict__ bsino, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = blockIdx.y * kFwdWarps + warp;
+  if (k >= n_sel) return;
+  const int t = blockIdx.x * 32 + lane;
+  const int bz0 = blockIdx.z * NB;
+  const int g = sel ? __ldg(sel + k) : k;
+  const bool valid = t < B;
+  long long F0 = 0;
+  unsigned S = 1;
+  float Lc = 0.f, Ly32 = 0.f;
+  int cls = 0, cl = INT_MAX, ch = INT_MIN;
+  if (valid) {
+    const RayEntry R = rays[(size_t)g * B + t];
+    F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; cls = R.flags & 3;
+    if (R.c_lo < R.c_hi) { cl = R.c_lo; ch = R.c_hi; }
+  }
+  const int wcl = __reduce_min_sync(0xffffffffu, cl);
+  const int wch = __reduce_max_sync(0xffffffffu, ch);
+  float sa[NB], sb[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) { sa[i] = 0.f; sb[i] = 0.f; }
+  if (wcl < wch) {
+    const int L = nc + 3;
+    const size_t istride = (size_t)nc * L;
+    const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
+    const bool mir = cls & kMirror;
+    const int kb = mir ? nc + 2 : 0, ks = mir ? -1 : 1;
+    const unsigned umax = (unsigned)(nc + 2);
+    const long long Es = F0 + (long long)wcl * (long long)S + (long long)S + (1LL << 32);
+    unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
+    int offk = wcl * L + kb;
+#pragma unroll 4
+    for (int c = wcl; c < wch; ++c) {
+      unsigned lo1, hi1;
+      asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
+      const float mf = (float)min(elo, S);
+      const int e = offk + ks * (int)min(ehi, umax);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        float pl, pu;
+        asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
+            : "=f"(pl), "=f"(pu) : "r"(e), "l"(base + i * istride));
+        sa[i] += pl;
+        sb[i] = fmaf(mf, pu - pl, sb[i]);
+      }
+      elo = lo1;
+      ehi = hi1;
+      offk += L;
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      float r = fmaf(Lc, sa[i], Ly32 * sb[i]);
+      if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
+      out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
+    }
+  }
+}
+
+static int kernel_version() {
+  static int v = getenv("MS2G_KV") ? atoi(getenv("MS2G_KV")) : 4;
+  return v;
+}
+
 template <int NB>
 static void fwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const int* d_sel, int n_sel,
                        const float* b, float* out) {
-  k_forward<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
-                                                f.nc, b, out);
+  if (kernel_version() >= 4)
+    k_forward_e<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
+                                                    f.nc, b, out);
+  else
+    k_forward<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
+                                                  f.nc, b, out);
 }
 
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
@@ -397,6 +482,186 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
   }
 }
 
+
+// End-coordinate adjoint (v4): the same traversal and round pipeline as
+// k_backward, with the forward's v4 weights.  In the warp's column step the
+// lane's end coordinate E = Et + lane*S gives u = floor(E) + 1 (tile-relative,
+// upper row u - 1, lower row u - 2) and m = min(frac32(E), S):
+//   T[u - 1] += m * (Ly32 r),   T[u - 2] += (S - m) * (Ly32 r)
+// (Lc = S Ly32 up to rounding, so the lower-row weight needs no Lc).
+// Rows outside the tile fall into pad rows: u is clamped to 34 (unsigned, so
+// negatives clamp too) and every warp window has two pad rows on each side
+// (shared between neighbouring windows), so no predicate is needed.
+// Record per ray: {lo(Et), hi(Et), S, Ly32 r}: one broadcast LDS.128 per step
+// (the kernel is bound by the L1/shared data pipe: 5 wavefronts per step).
+constexpr int kPadR = 2;
+constexpr int kWinR = 2 * (kBT + kPadR);                 // TX, pad, TY, pad (rows)
+constexpr int kAccRows = kPadR + kBW * kWinR;
+
+__global__ void __launch_bounds__(32 * kBW, 6) k_backward_e(const RayEntry* __restrict__ rays,
+                                                            const int4* __restrict__ ranges, int V_r, int B,
+                                                            const int* __restrict__ sel, int n_sel, int vpc,
+                                                            const float* __restrict__ sino, float* __restrict__ out,
+                                                            int nc, int tiles_x, float scale, int accumulate,
+                                                            int partial) {
+  __shared__ float acc[kAccRows * kBT];
+  __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int x0 = tx * kBT, y0 = ty * kBT;
+  float* TX = acc + (kPadR + warp * kWinR) * kBT;
+  float* TY = TX + (kBT + kPadR) * kBT;
+  for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * kBW) acc[i] = 0.f;
+  __syncthreads();
+  const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
+  const float* sb = sino + (size_t)bz * n_sel * B;
+  const int4* trange = ranges + (size_t)tile * V_r;
+
+  int vbase = kb + warp - 32 * kBW;
+  int g_lane = 0;
+  int4 rr_lane = make_int4(0, 0, 0, 0);
+  int j = 31;
+  int k = -1, g = 0, nr = 0, run = 0, tb = 0, te = -1, cls = 0;
+  int ra0 = 0, re0 = -1, ra1 = 0, re1 = -1, cls0 = 0, cls1 = 0;
+  auto next_round = [&]() -> bool {
+    tb += 32;
+    while (tb > te) {
+      ++run;
+      if (run >= nr) {
+        ++j;
+        if (j == 32) {
+          vbase += 32 * kBW;
+          if (vbase >= ke) return false;
+          const int kk = vbase + lane * kBW;
+          g_lane = (kk < ke) ? (sel ? __ldg(sel + kk) : kk) : 0;
+          rr_lane = (kk < ke) ? __ldg(trange + g_lane) : make_int4(0, 0, 0, 0);
+          j = 0;
+        }
+        k = vbase + j * kBW;
+        if (k >= ke) return false;
+        g = __shfl_sync(0xffffffffu, g_lane, j);
+        const int rx = __shfl_sync(0xffffffffu, rr_lane.x, j);
+        const int ry = __shfl_sync(0xffffffffu, rr_lane.y, j);
+        const int rz = __shfl_sync(0xffffffffu, rr_lane.z, j);
+        ra0 = rx & 0xffff; re0 = (short)(rx >> 16); ra1 = ry & 0xffff; re1 = (short)(ry >> 16);
+        cls0 = rz & 0xff; cls1 = (rz >> 8) & 0xff; nr = (rz >> 16) & 0xff;
+        run = -1;
+        continue;
+      }
+      tb = run ? ra1 : ra0;
+      te = run ? re1 : re0;
+      cls = run ? cls1 : cls0;
+    }
+    return true;
+  };
+
+  run = 0; nr = 0; te = -1; tb = 0;
+  bool have = next_round();
+  RayEntry Rn;
+  float rn = 0.f;
+  int tn = tb + lane;
+  if (have && tn <= te) {
+    Rn = rays[(size_t)g * B + tn];
+    rn = __ldg(sb + (size_t)k * B + tn);
+  }
+  while (have) {
+    const int ccls = cls, cte = te, ctb = tb;
+    const bool majY = ccls & kMajorY, mir = ccls & kMirror;
+    if (tn <= cte) {
+      const int c0 = majY ? y0 : x0;
+      const int mb = mir ? nc - (majY ? x0 : y0) - kBT : (majY ? x0 : y0);
+      const long long Et = Rn.F0 + (long long)c0 * (long long)Rn.S + (long long)Rn.S - ((long long)(mb - 1) << 32);
+      st4[warp][lane] = make_float4(__uint_as_float((unsigned)Et), __uint_as_float((unsigned)(Et >> 32)),
+                                    __uint_as_float(Rn.S), Rn.Ly32 * rn);
+    }
+    __syncwarp();
+    have = next_round();
+    tn = tb + lane;
+    if (have && tn <= te) {
+      Rn = rays[(size_t)g * B + tn];
+      rn = __ldg(sb + (size_t)k * B + tn);
+    }
+    // upper row u - 1 -> byte address sbase + u * sstride; lower = that - sstride
+    //   plain:  phys row = u - 1   (sbase at row -1)
+    //   mirror: phys row = 32 - u  (sbase at row 32, negative stride)
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(majY ? TY : TX) + 4u * (unsigned)lane +
+                           (mir ? 4u * kBT * kBT : (unsigned)(-4 * kBT));
+    const unsigned sstride = mir ? (unsigned)(-4 * kBT) : 4u * kBT;
+    const int nrays = min(32, cte - ctb + 1);
+    const float4* p4 = st4[warp];
+    float4 a = p4[0];
+#pragma unroll 2
+    for (int q = 0; q < nrays; ++q) {
+      const float4 an = p4[q + 1];
+      const unsigned S = __float_as_uint(a.z);
+      unsigned lo, u;
+      asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;"
+          : "=r"(lo), "=r"(u)
+          : "r"((unsigned)lane), "r"(S), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
+      const unsigned m = min(lo, S);
+      const float mu = (float)m, ml = (float)(S - m);
+      const unsigned adu = sbase + min(u, 34u) * sstride;
+      const unsigned adl = adu - sstride;
+      asm volatile("{\n\t.reg .f32 c0, c1;\n\t"
+                   "ld.shared.f32 c0, [%0];\n\t"
+                   "ld.shared.f32 c1, [%1];\n\t"
+                   "fma.rn.f32 c0, %2, %4, c0;\n\t"
+                   "fma.rn.f32 c1, %3, %4, c1;\n\t"
+                   "st.shared.f32 [%0], c0;\n\t"
+                   "st.shared.f32 [%1], c1;\n\t}"
+                   :: "r"(adu), "r"(adl), "f"(mu), "f"(ml), "f"(a.w) : "memory");
+      a = an;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // Sum the warp windows.  TX sums are read with lx = lane; TY (transposed)
+  // sums with ly = lane, then transposed through a 33-stride scratch (both
+  // passes bank-conflict free).
+  constexpr int kPer = kBT * kBT / (32 * kBW);
+  float sx[kPer], sy[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int idx = threadIdx.x + i * 32 * kBW;   // row idx / 32, lane idx % 32
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int w = 0; w < kBW; ++w) {
+      const float* tw = acc + (kPadR + w * kWinR) * kBT;
+      a0 += tw[idx];
+      a1 += tw[(kBT + kPadR) * kBT + idx];
+    }
+    sx[i] = a0;   // pixel (ly = idx / 32, lx = lane)
+    sy[i] = a1;   // pixel (ly = lane, lx = idx / 32)
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int idx = threadIdx.x + i * 32 * kBW;
+    acc[(idx & 31) * (kBT + 1) + (idx >> 5)] = sy[i];
+  }
+  __syncthreads();
+  const size_t np = (size_t)nc * nc;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int idx = threadIdx.x + i * 32 * kBW;
+    const int ly = idx / kBT, lx = idx % kBT;
+    const int yy = y0 + ly, xx = x0 + lx;
+    if (yy < nc && xx < nc) {
+      const float s = sx[i] + acc[ly * (kBT + 1) + lx];
+      const size_t o = (size_t)yy * nc + xx;
+      if (partial) {
+        out[((size_t)bz * gridDim.y + chunk) * np + o] = s;
+      } else {
+        float* dst = out + (size_t)bz * np + o;
+        float v = scale * s;
+        if (accumulate) v += *dst;
+        *dst = v;
+      }
+    }
+  }
+}
+
 __global__ void k_chunk_reduce(const float* __restrict__ part, int nchunks, size_t np, size_t total,
                                float* __restrict__ out, float scale, int accumulate) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -420,8 +685,18 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   const int vpc = (n_sel + nchunks - 1) / nchunks;
   const int partial = nchunks > 1;
   dim3 grid(tiles_x * tiles_x, nchunks, batch);
-  k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino,
-                                       partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
+  if (kernel_version() >= 4) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_backward_e, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      attr = true;
+    }
+    k_backward_e<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino,
+                                           partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
+  } else {
+    k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino,
+                                         partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
+  }
   MS2G_TRY(check_launch("k_backward"));
   if (partial) {
     const size_t np = (size_t)f.nc * f.nc, total = np * batch;

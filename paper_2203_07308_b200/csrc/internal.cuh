@@ -53,7 +53,7 @@ struct FactorTables {
   RayEntry* d_rays = nullptr;     // [V_r][B]
   ViewEntry* d_views = nullptr;   // [V_r]
   int bp_chunks = 1;              // view chunks of the backprojector
-  int4* d_bpr = nullptr;          // per (32x32 tile, view): bin runs meeting the tile
+  int4* d_bpr = nullptr;          // per (adjoint tile, view): bin runs meeting the tile
   // bicubic resampling tables (NEXT-1), [n_out][taps] clamped input index / weight
   int taps_down = 0, taps_up = 0;
   int* d_idx_down = nullptr;
@@ -85,7 +85,7 @@ struct ms2g_plan {
   float* w_rs = nullptr;               // separable-resampling intermediate [batch][n][n]
   float* w_G = nullptr;                // coarse gradient / backprojection
   float* w_res = nullptr;              // residual / projection [batch][V_r][B]
-  float* w_part = nullptr;             // backprojection chunk partials
+  float* w_part = nullptr;             // backprojection partial planes [batch][chunk][X/Y family][n_c^2]
   size_t part_elems = 0;
   float* w_x[2] = {nullptr, nullptr};  // iterate double buffer (full res)
   float* w_y = nullptr;                // extrapolated point
@@ -163,6 +163,7 @@ const FactorTables* find_factor(const ms2g_plan* p, int factor);
 int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s);
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s);
+int bp_tile_count(int nc);   // adjoint tiles (both families) of an n_c grid
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s);

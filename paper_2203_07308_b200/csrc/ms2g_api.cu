@@ -101,10 +101,8 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
         prev_cls = flags;
       }
       long long lo, hi;
-      if (R.S == 0u) {
-        lo = 0; hi = (R.F0 >= 0 && R.F0 < M) ? nc : 0;
-      } else {
-        const long long Sl = (long long)(unsigned long long)R.S;
+      {
+        const long long Sl = (long long)(unsigned long long)R.S;   // >= 1
         lo = floor_div(-R.F0, Sl);
         if (lo < 0) lo = 0;
         hi = ceil_div(M - R.F0, Sl);
@@ -124,9 +122,8 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   MS2G_CUDA(cudaMemcpy(f.d_views, views.data(), sizeof(ViewEntry) * views.size(), cudaMemcpyHostToDevice));
   MS2G_TRY(build_bicubic_tables(f, d.n));
   {  // adjoint tile/view bin ranges (geometry only, once per plan)
-    const int tx = (nc + 31) / 32;
     int* d_err = nullptr;
-    MS2G_CUDA(cudaMalloc(&f.d_bpr, sizeof(int4) * (size_t)tx * tx * V_r));
+    MS2G_CUDA(cudaMalloc(&f.d_bpr, sizeof(int4) * (size_t)bp_tile_count(nc) * V_r));
     MS2G_CUDA(cudaMalloc(&d_err, sizeof(int)));
     MS2G_CUDA(cudaMemset(d_err, 0, sizeof(int)));
     int rc = launch_bp_ranges(f, V_r, B, f.d_bpr, d_err, 0);
@@ -143,8 +140,7 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   // small fraction of the launch (measured on B200, C4: 8 waves for 1024^2,
   // 24 waves for coarser grids; the chunk partials are summed by
   // k_chunk_reduce in fixed order)
-  const int tiles_x = (nc + 31) / 32;
-  const long long tiles = (long long)tiles_x * tiles_x * d.batch;
+  const long long tiles = (long long)bp_tile_count(nc) * d.batch;
   const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : (tiles >= 1024 ? 8 : 24);
   const long long target = waves * sm_count;
   long long ch = (target + tiles - 1) / tiles;
@@ -660,8 +656,8 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
       return rc;
     }
     if (f.nc > p->nmax_c) p->nmax_c = f.nc;
-    const size_t need = (size_t)f.bp_chunks * f.nc * f.nc * d.batch;
-    if (f.bp_chunks > 1 && need > part) part = need;
+    const size_t need = (size_t)2 * f.bp_chunks * f.nc * f.nc * d.batch;   // X/Y families x chunks
+    if (need > part) part = need;
   }
   const size_t bt = d.batch;
   const size_t cimg = (size_t)p->nmax_c * p->nmax_c * bt, fimg = (size_t)d.n * d.n * bt;

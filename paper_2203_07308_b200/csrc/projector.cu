@@ -86,6 +86,16 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
 // line (coalesced).  The 8 warps of a block are 8 consecutive views over the
 // same bins, tracing nearly the same lines: L1 reuse.  Residual epilogue fused
 // ("A_s v - b").
+//
+// End-coordinate weights.  In column c the ray's minor coordinate runs from
+// F(c) to E(c) = F(c) + S.  With u = floor(E) + 1 (the pair index of the
+// (lower, upper) rows floor(E) - 1, floor(E), shifted by the pair images'
+// 2-element pad) and m = min(frac32(E), S) (the part of the step above the
+// grid line floor(E); m = S when the column crosses no line),
+//   upper row: m Ly32,   lower row: Lc - m Ly32   (Ly32 = Lc / S),
+// so  sum_c w.x = Lc sum_c x_lower + Ly32 sum_c m (x_upper - x_lower): the
+// per-ray constants leave the column loop.  Without a crossing the lower-row
+// weight is a rounding residual (|.| <= 2^-23 Lc), not an exact zero.
 constexpr int kFwdWarps = 8;
 
 // NB images of a batch share one traversal: the weights of a column are
@@ -95,84 +105,6 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k = blockIdx.y * kFwdWarps + warp;
-  if (k >= n_sel) return;
-  const int t = blockIdx.x * 32 + lane;
-  const int bz0 = blockIdx.z * NB;
-  const int g = sel ? __ldg(sel + k) : k;
-  const bool valid = t < B;
-  long long F0 = 0;
-  unsigned S = 0;
-  float Lc = 0.f, Ly32 = 0.f;
-  int cls = 0, cl = INT_MAX, ch = INT_MIN;
-  if (valid) {
-    const RayEntry R = rays[(size_t)g * B + t];
-    F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; cls = R.flags & 3;
-    if (R.c_lo < R.c_hi) { cl = R.c_lo; ch = R.c_hi; }
-  }
-  const int wcl = __reduce_min_sync(0xffffffffu, cl);
-  const int wch = __reduce_max_sync(0xffffffffu, ch);
-  float acc[NB];
-#pragma unroll
-  for (int i = 0; i < NB; ++i) acc[i] = 0.f;
-  if (wcl < wch) {
-    const int L = nc + 3;
-    const size_t istride = (size_t)nc * L;          // pair-image stride between batch images
-    const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride + 2;
-    const bool mir = cls & kMirror;
-    const int kb = mir ? nc - 2 : 0, ks = mir ? -1 : 1;
-    const long long Fs = F0 + (long long)wcl * (long long)S;
-    unsigned flo = (unsigned)Fs, fhi = (unsigned)(Fs >> 32);
-    int offk = wcl * L + kb;                 // element index of pair k = 0 on line c, plus kb
-#pragma unroll 4
-    for (int c = wcl; c < wch; ++c) {
-      unsigned lo1, hi1;
-      asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(flo), "r"(fhi), "r"(S));
-      const int q = (int)fhi;
-      const bool cross = hi1 != fhi;
-      float w0, w1;
-      seg_weights(flo, cross, Lc, Ly32, w0, w1);
-      const int e = offk + ks * min(max(q, -2), nc);
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        float px, py;
-        asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
-            : "=f"(px), "=f"(py) : "r"(e), "l"(base + i * istride));
-        acc[i] = fmaf(w0, px, acc[i]);
-        acc[i] = fmaf(w1, py, acc[i]);
-      }
-      flo = lo1;
-      fhi = hi1;
-      offk += L;
-    }
-  }
-  if (valid) {
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      float r = acc[i];
-      if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
-      out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
-    }
-  }
-}
-
-
-// End-coordinate form (v4).  Per column c the ray's minor coordinate runs from
-// F(c) to E(c) = F(c) + S.  With u = floor(E) + 1 (the pair index k of the
-// (lower, upper) rows k = floor(E) - 1, floor(E), shifted by the pair images'
-// 2-element pad) and m = min(frac32(E), S) (the part of the step above the
-// grid line floor(E); m = S when the column does not cross a line),
-//   upper row: m Ly32,   lower row: Lc - m Ly32,
-// so  sum_c w.x = Lc * sum_c x_lower + Ly32 * sum_c m (x_upper - x_lower):
-// the per-ray constants Lc, Ly32 leave the column loop.  Without a crossing
-// the lower-row weight is a rounding residual (|.| <= 2^-23 Lc), not an exact
-// zero; the adjoint uses the same formula, so the pair stays a transpose.
-template <int NB>
-__global__ void __launch_bounds__(256) k_forward_e(const RayEntry* __restrict__ rays, int B, int V_r,
-                                                   const int* __restrict__ sel, int n_sel,
-                                                   const float2* __restrict__ pairs, size_t pair_stride, int nc,
-                                                   const float* __restrict__ bsino, float* __restrict__ out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k = blockIdx.y * kFwdWarps + warp;
   if (k >= n_sel) return;
@@ -196,8 +128,11 @@ __global__ void __launch_bounds__(256) k_forward_e(const RayEntry* __restrict__ 
   for (int i = 0; i < NB; ++i) { sa[i] = 0.f; sb[i] = 0.f; }
   if (wcl < wch) {
     const int L = nc + 3;
-    const size_t istride = (size_t)nc * L;
+    const size_t istride = (size_t)nc * L;          // pair-image stride between batch images
     const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
+    // element of pair index u on line c: c L + u (plain) or c L + nc + 2 - u
+    // (mirrored images store (v[k+1], v[k]) at k + 2); u is clamped to the
+    // zero pads (unsigned: negatives clamp too)
     const bool mir = cls & kMirror;
     const int kb = mir ? nc + 2 : 0, ks = mir ? -1 : 1;
     const unsigned umax = (unsigned)(nc + 2);
@@ -233,20 +168,11 @@ __global__ void __launch_bounds__(256) k_forward_e(const RayEntry* __restrict__ 
   }
 }
 
-static int kernel_version() {
-  static int v = getenv("MS2G_KV") ? atoi(getenv("MS2G_KV")) : 4;
-  return v;
-}
-
 template <int NB>
 static void fwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const int* d_sel, int n_sel,
                        const float* b, float* out) {
-  if (kernel_version() >= 4)
-    k_forward_e<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
-                                                    f.nc, b, out);
-  else
-    k_forward<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
-                                                  f.nc, b, out);
+  k_forward<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
+                                                f.nc, b, out);
 }
 
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
@@ -262,36 +188,69 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 }
 
 // --------------------------------------------------------------- adjoint --
-// Tile-driven ray scatter.  A block owns a 32x32 pixel tile and a chunk of
-// views; each warp takes one view at a time and walks the rays that meet the
-// tile, one per step, with LANE = major index inside the tile.  A lane only
-// touches its own column (major-x rays) or row (major-y rays) of the warp's
-// private shared accumulators: no atomics, fixed order, deterministic.
-// Major-x rays accumulate in TX[row][col], major-y rays in TY[col][row]: the
-// lane is the fastest-varying coordinate, so every access of a step hits 32
-// distinct banks whatever the slope or mirroring.  The bins that meet each
-// (tile, view) are precomputed per plan (k_bp_ranges), split into <= 2 runs of
-// one ray class (major axis, mirror), so the addressing constants are
+// Tile-driven ray scatter.  Two tile families cover the image: X-tiles
+// (32 columns x kBH rows) take only the major-x rays, Y-tiles (32 rows x kBH
+// columns) only the major-y rays, so every block uses one accumulator layout
+// T[minor][major] whose long side is the MINOR axis: a ray of slope <= 1 then
+// crosses most of the 32 major lanes inside the tile (lane utilisation 0.84
+// at kBH = 64 against 0.73 for 32x32 tiles).  A block owns one tile and a
+// chunk of views; each warp takes one view at a time and walks the rays that
+// meet the tile, one per step, with LANE = major index inside the tile.  A
+// lane only touches its own major line of the warp's private accumulator (no
+// atomics, fixed order, deterministic) and the lane is the fastest-varying
+// coordinate, so every access of a step hits 32 distinct banks.  The bins
+// that meet each (tile, view) are precomputed per plan (k_bp_ranges), split
+// into <= 2 runs of one ray class, so the addressing constants are
 // loop-invariant.  The ray records of the next 32-ray round are fetched from
 // global memory while the current round is processed (software pipeline).
-// The warp tiles are summed in fixed order at the end.
-constexpr int kBT = 32;
-constexpr int kBW = 4;
-constexpr int kTS = kBT * kBT;
+//
+// Step (the forward's weights): the lane's end coordinate E = Et + lane*S
+// gives u = floor(E) + 1 (tile-relative; upper row u - 1, lower row u - 2) and
+// m = min(frac32(E), S):   T[u - 1] += m (Ly32 r),   T[u - 2] += (S - m)(Ly32 r)
+// (Lc = S Ly32 up to rounding).  u is clamped to kBH + 2 (unsigned, so
+// negatives clamp too) and every warp window has two pad rows on each side
+// (shared between neighbouring windows), so no predicate is needed.  Record
+// per ray: {lo(Et), hi(Et), S, Ly32 r}, one broadcast LDS.128 per step.  The
+// kernel is bound by the L1/shared data pipe (5 wavefronts per step).
+//
+// The X- and Y-families write separate partial planes (per view chunk too);
+// k_chunk_reduce sums them in fixed order.
+constexpr int kBT = 32;                          // major extent (lanes)
+constexpr int kBH = 64;                          // minor extent (rows)
+constexpr int kBW = 4;                           // warps per block
+constexpr int kPadR = 2;
+constexpr int kWinR = kBH + kPadR;               // rows per warp window (+ shared pads)
+constexpr int kAccRows = kPadR + kBW * kWinR;
 
-// Per (tile, view): bins [ta_r, te_r] of run r (r < n), class cls_r.
-__global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B, int nc, int tiles_x,
+struct BpTiling {
+  int maj, mnr, per;   // tiles along the major axis, along the minor axis, per family
+};
+static inline BpTiling bp_tiling(int nc) {
+  BpTiling t;
+  t.maj = (nc + kBT - 1) / kBT;
+  t.mnr = (nc + kBH - 1) / kBH;
+  t.per = t.maj * t.mnr;
+  return t;
+}
+int bp_tile_count(int nc) { return 2 * bp_tiling(nc).per; }
+
+// Per (tile, view): bins [ta_r, te_r] of run r (r < n) of the tile family's
+// major axis, class cls_r.
+__global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B, int nc, int tmaj, int per,
                             int4* __restrict__ out, int* __restrict__ err) {
-  const size_t n = (size_t)tiles_x * tiles_x * V_r;
+  const size_t n = (size_t)2 * per * V_r;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int g = (int)(i % V_r);
     const int tile = (int)(i / V_r);
-    const int x0 = (tile % tiles_x) * kBT, y0 = (tile / tiles_x) * kBT;
-    const int x1 = min(x0 + kBT, nc), y1 = min(y0 + kBT, nc);
+    const int fam = tile >= per;
+    const int ti = tile - fam * per;
+    const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * kBH;
+    const int c1 = min(c0 + kBT, nc), m1 = min(m0 + kBH, nc);
+    const float x0 = fam ? m0 : c0, x1 = fam ? m1 : c1, y0 = fam ? c0 : m0, y1 = fam ? c1 : m1;
     const ViewEntry V = views[g];
     float tmin = INFINITY, tmax = -INFINITY;
     for (int c = 0; c < 4; ++c) {
-      const float px = (c & 1) ? (float)x1 : (float)x0, py = (c & 2) ? (float)y1 : (float)y0;
+      const float px = (c & 1) ? x1 : x0, py = (c & 2) ? y1 : y0;
       const float dx = px - V.Sx, dy = py - V.Sy;
       const float tau = V.off + V.scale * (dx * V.ex + dy * V.ey) / (dx * V.nx + dy * V.ny);
       tmin = fminf(tmin, tau);
@@ -301,6 +260,7 @@ __global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B,
     const int t_hi = min(B - 1, (int)ceilf(tmax + 0.01f));
     int nr = 0, ta[2] = {0, 0}, te[2] = {-1, -1}, cl[2] = {0, 0};
     for (int sg = 0; sg < V.nseg; ++sg) {
+      if (((V.seg_cls[sg] & kMajorY) != 0) != (fam != 0)) continue;
       const int a = max(t_lo, (int)V.seg_t[sg]), e = min(t_hi, (int)V.seg_t[sg + 1] - 1);
       if (a > e) continue;
       if (nr == 2) { atomicExch(err, 1); break; }
@@ -312,33 +272,28 @@ __global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B,
 }
 
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s) {
-  const int tiles_x = (f.nc + kBT - 1) / kBT;
-  const size_t n = (size_t)tiles_x * tiles_x * V_r;
+  const BpTiling t = bp_tiling(f.nc);
+  const size_t n = (size_t)2 * t.per * V_r;
   const int blocks = (int)((n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192);
-  k_bp_ranges<<<blocks, 256, 0, s>>>(f.d_views, V_r, B, f.nc, tiles_x, out, err);
+  k_bp_ranges<<<blocks, 256, 0, s>>>(f.d_views, V_r, B, f.nc, t.maj, t.per, out, err);
   return check_launch("k_bp_ranges");
 }
 
-__global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restrict__ rays,
-                                                       const int4* __restrict__ ranges, int V_r, int B,
-                                                       const int* __restrict__ sel, int n_sel, int vpc,
-                                                       const float* __restrict__ sino, float* __restrict__ out,
-                                                       int nc, int tiles_x, float scale, int accumulate,
-                                                       int partial) {
-  __shared__ float acc[kBW][2][kTS];
+__global__ void __launch_bounds__(32 * kBW, 6) k_backward(const RayEntry* __restrict__ rays,
+                                                          const int4* __restrict__ ranges, int V_r, int B,
+                                                          const int* __restrict__ sel, int n_sel, int vpc,
+                                                          const float* __restrict__ sino, float* __restrict__ part,
+                                                          int nc, int tmaj, int per) {
+  __shared__ float acc[kAccRows * kBT];
   __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
-  __shared__ float4 st2[kBW][33];   // {Ly32, r, ~S, -}
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int x0 = tx * kBT, y0 = ty * kBT;
-  float* TX = acc[warp][0];
-  float* TY = acc[warp][1];
-  for (int i = lane; i < kTS; i += 32) {
-    TX[i] = 0.f;
-    TY[i] = 0.f;
-  }
-  __syncwarp();
+  const int fam = tile >= per;                     // 0: X-tile (major x), 1: Y-tile (major y)
+  const int ti = tile - fam * per;
+  const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * kBH;   // major / minor origin
+  float* T = acc + (kPadR + warp * kWinR) * kBT;
+  for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * kBW) acc[i] = 0.f;
+  __syncthreads();
   const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
   const float* sb = sino + (size_t)bz * n_sel * B;
   const int4* trange = ranges + (size_t)tile * V_r;
@@ -381,15 +336,9 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
     }
     return true;
   };
-  auto frame = [&](int c, int& c0, int& mb) {
-    const bool majY = c & kMajorY, mir = c & kMirror;
-    c0 = majY ? y0 : x0;
-    mb = mir ? nc - (majY ? x0 : y0) - kBT : (majY ? x0 : y0);
-  };
 
   run = 0; nr = 0; te = -1; tb = 0;
   bool have = next_round();
-  // prefetch the first round
   RayEntry Rn;
   float rn = 0.f;
   int tn = tb + lane;
@@ -397,18 +346,16 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
     Rn = rays[(size_t)g * B + tn];
     rn = __ldg(sb + (size_t)k * B + tn);
   }
+  const unsigned tbase = (unsigned)__cvta_generic_to_shared(T) + 4u * (unsigned)lane;
   while (have) {
-    // commit the prefetched round to shared memory (tile-relative coordinate)
-    const int ccls = cls, cte = te, ctb = tb;
-    {
-      int c0, mb;
-      frame(ccls, c0, mb);
-      if (tn <= cte) {
-        const long long Ft = Rn.F0 + (long long)c0 * (long long)Rn.S - ((long long)mb << 32);
-        st4[warp][lane] = make_float4(__uint_as_float((unsigned)Ft), __uint_as_float((unsigned)(Ft >> 32)),
-                                      __uint_as_float(Rn.S), Rn.Lc);
-        st2[warp][lane] = make_float4(Rn.Ly32, rn, __uint_as_float(~Rn.S), 0.f);
-      }
+    // commit the prefetched round to shared memory (tile-relative end coordinate, +1 row)
+    const int cte = te, ctb = tb;
+    const bool mir = cls & kMirror;
+    if (tn <= cte) {
+      const int mb = mir ? nc - m0 - kBH : m0;
+      const long long Et = Rn.F0 + (long long)c0 * (long long)Rn.S + (long long)Rn.S - ((long long)(mb - 1) << 32);
+      st4[warp][lane] = make_float4(__uint_as_float((unsigned)Et), __uint_as_float((unsigned)(Et >> 32)),
+                                    __uint_as_float(Rn.S), Rn.Ly32 * rn);
     }
     __syncwarp();
     // fetch the next round while this one is processed
@@ -418,175 +365,10 @@ __global__ void __launch_bounds__(32 * kBW) k_backward(const RayEntry* __restric
       Rn = rays[(size_t)g * B + tn];
       rn = __ldg(sb + (size_t)k * B + tn);
     }
-    const bool majY = ccls & kMajorY, mir = ccls & kMirror;
-    // cell (local minor l, lane) -> T[phys_minor * 32 + lane], phys_minor = mir ? 31 - l : l
-    // (byte addresses in the shared window)
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(majY ? TY : TX) +
-                           4u * (unsigned)(lane + (mir ? (kBT - 1) * kBT : 0));
-    const int sstride = mir ? -4 * kBT : 4 * kBT;
-    const int nrays = min(32, cte - ctb + 1);
-    const float4* p4 = st4[warp];
-    const float4* p2 = st2[warp];
-    float4 a = p4[0];
-    float4 b2 = p2[0];
-    for (int q = 0; q < nrays; ++q) {
-      const float4 an = p4[q + 1];
-      const float4 bn = p2[q + 1];
-      // F = Ft + lane * S as (lo, hi); the column crosses a grid line iff
-      // lo + S carries, i.e. lo > ~S
-      unsigned lo, hi;
-      asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;"
-          : "=r"(lo), "=r"(hi)
-          : "r"((unsigned)lane), "r"(__float_as_uint(a.z)), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
-      const bool cross = lo > __float_as_uint(b2.z);
-      float w0, w1;
-      seg_weights(lo, cross, a.w, b2.x, w0, w1);
-      const unsigned ad0 = sbase + hi * (unsigned)sstride;
-      const unsigned ad1 = ad0 + (unsigned)sstride;
-      const unsigned v0 = hi < (unsigned)kBT;
-      const unsigned v1 = cross && (hi + 1u) < (unsigned)kBT;
-      asm volatile("{\n\t.reg .pred p0, p1;\n\t.reg .f32 c0, c1;\n\t"
-                   "setp.ne.u32 p0, %5, 0;\n\t"
-                   "setp.ne.u32 p1, %6, 0;\n\t"
-                   "@p0 ld.shared.f32 c0, [%0];\n\t"
-                   "@p1 ld.shared.f32 c1, [%1];\n\t"
-                   "@p0 fma.rn.f32 c0, %2, %4, c0;\n\t"
-                   "@p1 fma.rn.f32 c1, %3, %4, c1;\n\t"
-                   "@p0 st.shared.f32 [%0], c0;\n\t"
-                   "@p1 st.shared.f32 [%1], c1;\n\t}"
-                   :: "r"(ad0), "r"(ad1), "f"(w0), "f"(w1), "f"(b2.y), "r"(v0), "r"(v1) : "memory");
-      a = an;
-      b2 = bn;
-    }
-    __syncwarp();
-  }
-  __syncthreads();
-  const size_t np = (size_t)nc * nc;
-  for (int idx = threadIdx.x; idx < kBT * kBT; idx += blockDim.x) {
-    const int ly = idx / kBT, lx = idx % kBT;
-    const int yy = y0 + ly, xx = x0 + lx;
-    if (yy < nc && xx < nc) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < kBW; ++w) s += acc[w][0][ly * kBT + lx] + acc[w][1][lx * kBT + ly];
-      const size_t o = (size_t)yy * nc + xx;
-      if (partial) {
-        out[((size_t)bz * gridDim.y + chunk) * np + o] = s;
-      } else {
-        float* dst = out + (size_t)bz * np + o;
-        float v = scale * s;
-        if (accumulate) v += *dst;
-        *dst = v;
-      }
-    }
-  }
-}
-
-
-// End-coordinate adjoint (v4): the same traversal and round pipeline as
-// k_backward, with the forward's v4 weights.  In the warp's column step the
-// lane's end coordinate E = Et + lane*S gives u = floor(E) + 1 (tile-relative,
-// upper row u - 1, lower row u - 2) and m = min(frac32(E), S):
-//   T[u - 1] += m * (Ly32 r),   T[u - 2] += (S - m) * (Ly32 r)
-// (Lc = S Ly32 up to rounding, so the lower-row weight needs no Lc).
-// Rows outside the tile fall into pad rows: u is clamped to 34 (unsigned, so
-// negatives clamp too) and every warp window has two pad rows on each side
-// (shared between neighbouring windows), so no predicate is needed.
-// Record per ray: {lo(Et), hi(Et), S, Ly32 r}: one broadcast LDS.128 per step
-// (the kernel is bound by the L1/shared data pipe: 5 wavefronts per step).
-constexpr int kPadR = 2;
-constexpr int kWinR = 2 * (kBT + kPadR);                 // TX, pad, TY, pad (rows)
-constexpr int kAccRows = kPadR + kBW * kWinR;
-
-__global__ void __launch_bounds__(32 * kBW, 6) k_backward_e(const RayEntry* __restrict__ rays,
-                                                            const int4* __restrict__ ranges, int V_r, int B,
-                                                            const int* __restrict__ sel, int n_sel, int vpc,
-                                                            const float* __restrict__ sino, float* __restrict__ out,
-                                                            int nc, int tiles_x, float scale, int accumulate,
-                                                            int partial) {
-  __shared__ float acc[kAccRows * kBT];
-  __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int x0 = tx * kBT, y0 = ty * kBT;
-  float* TX = acc + (kPadR + warp * kWinR) * kBT;
-  float* TY = TX + (kBT + kPadR) * kBT;
-  for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * kBW) acc[i] = 0.f;
-  __syncthreads();
-  const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
-  const float* sb = sino + (size_t)bz * n_sel * B;
-  const int4* trange = ranges + (size_t)tile * V_r;
-
-  int vbase = kb + warp - 32 * kBW;
-  int g_lane = 0;
-  int4 rr_lane = make_int4(0, 0, 0, 0);
-  int j = 31;
-  int k = -1, g = 0, nr = 0, run = 0, tb = 0, te = -1, cls = 0;
-  int ra0 = 0, re0 = -1, ra1 = 0, re1 = -1, cls0 = 0, cls1 = 0;
-  auto next_round = [&]() -> bool {
-    tb += 32;
-    while (tb > te) {
-      ++run;
-      if (run >= nr) {
-        ++j;
-        if (j == 32) {
-          vbase += 32 * kBW;
-          if (vbase >= ke) return false;
-          const int kk = vbase + lane * kBW;
-          g_lane = (kk < ke) ? (sel ? __ldg(sel + kk) : kk) : 0;
-          rr_lane = (kk < ke) ? __ldg(trange + g_lane) : make_int4(0, 0, 0, 0);
-          j = 0;
-        }
-        k = vbase + j * kBW;
-        if (k >= ke) return false;
-        g = __shfl_sync(0xffffffffu, g_lane, j);
-        const int rx = __shfl_sync(0xffffffffu, rr_lane.x, j);
-        const int ry = __shfl_sync(0xffffffffu, rr_lane.y, j);
-        const int rz = __shfl_sync(0xffffffffu, rr_lane.z, j);
-        ra0 = rx & 0xffff; re0 = (short)(rx >> 16); ra1 = ry & 0xffff; re1 = (short)(ry >> 16);
-        cls0 = rz & 0xff; cls1 = (rz >> 8) & 0xff; nr = (rz >> 16) & 0xff;
-        run = -1;
-        continue;
-      }
-      tb = run ? ra1 : ra0;
-      te = run ? re1 : re0;
-      cls = run ? cls1 : cls0;
-    }
-    return true;
-  };
-
-  run = 0; nr = 0; te = -1; tb = 0;
-  bool have = next_round();
-  RayEntry Rn;
-  float rn = 0.f;
-  int tn = tb + lane;
-  if (have && tn <= te) {
-    Rn = rays[(size_t)g * B + tn];
-    rn = __ldg(sb + (size_t)k * B + tn);
-  }
-  while (have) {
-    const int ccls = cls, cte = te, ctb = tb;
-    const bool majY = ccls & kMajorY, mir = ccls & kMirror;
-    if (tn <= cte) {
-      const int c0 = majY ? y0 : x0;
-      const int mb = mir ? nc - (majY ? x0 : y0) - kBT : (majY ? x0 : y0);
-      const long long Et = Rn.F0 + (long long)c0 * (long long)Rn.S + (long long)Rn.S - ((long long)(mb - 1) << 32);
-      st4[warp][lane] = make_float4(__uint_as_float((unsigned)Et), __uint_as_float((unsigned)(Et >> 32)),
-                                    __uint_as_float(Rn.S), Rn.Ly32 * rn);
-    }
-    __syncwarp();
-    have = next_round();
-    tn = tb + lane;
-    if (have && tn <= te) {
-      Rn = rays[(size_t)g * B + tn];
-      rn = __ldg(sb + (size_t)k * B + tn);
-    }
     // upper row u - 1 -> byte address sbase + u * sstride; lower = that - sstride
-    //   plain:  phys row = u - 1   (sbase at row -1)
-    //   mirror: phys row = 32 - u  (sbase at row 32, negative stride)
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(majY ? TY : TX) + 4u * (unsigned)lane +
-                           (mir ? 4u * kBT * kBT : (unsigned)(-4 * kBT));
+    //   plain:  phys row = u - 1      (sbase at row -1)
+    //   mirror: phys row = kBH - u    (sbase at row kBH, negative stride)
+    const unsigned sbase = tbase + (mir ? 4u * kBT * kBH : (unsigned)(-4 * kBT));
     const unsigned sstride = mir ? (unsigned)(-4 * kBT) : 4u * kBT;
     const int nrays = min(32, cte - ctb + 1);
     const float4* p4 = st4[warp];
@@ -601,7 +383,7 @@ __global__ void __launch_bounds__(32 * kBW, 6) k_backward_e(const RayEntry* __re
           : "r"((unsigned)lane), "r"(S), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
       const unsigned m = min(lo, S);
       const float mu = (float)m, ml = (float)(S - m);
-      const unsigned adu = sbase + min(u, 34u) * sstride;
+      const unsigned adu = sbase + min(u, (unsigned)(kBH + 2)) * sstride;
       const unsigned adl = adu - sstride;
       asm volatile("{\n\t.reg .f32 c0, c1;\n\t"
                    "ld.shared.f32 c0, [%0];\n\t"
@@ -616,59 +398,52 @@ __global__ void __launch_bounds__(32 * kBW, 6) k_backward_e(const RayEntry* __re
     __syncwarp();
   }
   __syncthreads();
-  // Sum the warp windows.  TX sums are read with lx = lane; TY (transposed)
-  // sums with ly = lane, then transposed through a 33-stride scratch (both
-  // passes bank-conflict free).
-  constexpr int kPer = kBT * kBT / (32 * kBW);
-  float sx[kPer], sy[kPer];
+  // Sum the warp windows in fixed order: element (row l, lane) of the tile.
+  constexpr int kPer = kBT * kBH / (32 * kBW);
+  float sum[kPer];
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
     const int idx = threadIdx.x + i * 32 * kBW;   // row idx / 32, lane idx % 32
-    float a0 = 0.f, a1 = 0.f;
+    float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < kBW; ++w) {
-      const float* tw = acc + (kPadR + w * kWinR) * kBT;
-      a0 += tw[idx];
-      a1 += tw[(kBT + kPadR) * kBT + idx];
-    }
-    sx[i] = a0;   // pixel (ly = idx / 32, lx = lane)
-    sy[i] = a1;   // pixel (ly = lane, lx = idx / 32)
+    for (int w = 0; w < kBW; ++w) s += acc[(kPadR + w * kWinR) * kBT + idx];
+    sum[i] = s;
   }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int idx = threadIdx.x + i * 32 * kBW;
-    acc[(idx & 31) * (kBT + 1) + (idx >> 5)] = sy[i];
-  }
-  __syncthreads();
   const size_t np = (size_t)nc * nc;
+  float* dst = part + ((size_t)(bz * gridDim.y + chunk) * 2 + fam) * np;
+  if (!fam) {       // X-tile: row l = y - m0, lane = x - c0 (coalesced)
 #pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int idx = threadIdx.x + i * 32 * kBW;
-    const int ly = idx / kBT, lx = idx % kBT;
-    const int yy = y0 + ly, xx = x0 + lx;
-    if (yy < nc && xx < nc) {
-      const float s = sx[i] + acc[ly * (kBT + 1) + lx];
-      const size_t o = (size_t)yy * nc + xx;
-      if (partial) {
-        out[((size_t)bz * gridDim.y + chunk) * np + o] = s;
-      } else {
-        float* dst = out + (size_t)bz * np + o;
-        float v = scale * s;
-        if (accumulate) v += *dst;
-        *dst = v;
-      }
+    for (int i = 0; i < kPer; ++i) {
+      const int idx = threadIdx.x + i * 32 * kBW;
+      const int yy = m0 + (idx >> 5), xx = c0 + (idx & 31);
+      if (yy < nc && xx < nc) dst[(size_t)yy * nc + xx] = sum[i];
+    }
+  } else {          // Y-tile: row l = x - m0, lane = y - c0; transpose through a (kBH+1)-stride scratch
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int idx = threadIdx.x + i * 32 * kBW;
+      acc[(idx & 31) * (kBH + 1) + (idx >> 5)] = sum[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int idx = threadIdx.x + i * 32 * kBW;   // y = idx / kBH, x = idx % kBH (tile-relative)
+      const int ly = idx / kBH, lx = idx % kBH;
+      const int yy = c0 + ly, xx = m0 + lx;
+      if (yy < nc && xx < nc) dst[(size_t)yy * nc + xx] = acc[ly * (kBH + 1) + lx];
     }
   }
 }
 
-__global__ void k_chunk_reduce(const float* __restrict__ part, int nchunks, size_t np, size_t total,
+// out = scale * sum of the nplanes partial planes (+ out if accumulate), fixed order.
+__global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size_t np, size_t total,
                                float* __restrict__ out, float scale, int accumulate) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t b = i / np, p = i % np;
-    const float* src = part + b * nchunks * np + p;
+    const float* src = part + b * nplanes * np + p;
     float s = 0.f;
-    for (int c = 0; c < nchunks; ++c) s += src[(size_t)c * np];
+    for (int c = 0; c < nplanes; ++c) s += src[(size_t)c * np];
     float v = scale * s;
     if (accumulate) v += out[i];
     out[i] = v;
@@ -677,34 +452,25 @@ __global__ void k_chunk_reduce(const float* __restrict__ part, int nchunks, size
 
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s) {
-  const int tiles_x = (f.nc + kBT - 1) / kBT;
+  const BpTiling t = bp_tiling(f.nc);
   int nchunks = f.bp_chunks;
   const int max_chunks = (n_sel + kBW - 1) / kBW;
   if (nchunks > max_chunks) nchunks = max_chunks;
   if (nchunks < 1) nchunks = 1;
   const int vpc = (n_sel + nchunks - 1) / nchunks;
-  const int partial = nchunks > 1;
-  dim3 grid(tiles_x * tiles_x, nchunks, batch);
-  if (kernel_version() >= 4) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_backward_e, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      attr = true;
-    }
-    k_backward_e<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino,
-                                           partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
-  } else {
-    k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino,
-                                         partial ? p->w_part : img, f.nc, tiles_x, scale, accumulate, partial);
+  static bool attr = false;
+  if (!attr) {   // 6 blocks of 37 KB per SM need the maximum shared-memory carveout
+    cudaFuncSetAttribute(k_backward, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr = true;
   }
+  dim3 grid(2 * t.per, nchunks, batch);
+  k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino, p->w_part, f.nc,
+                                       t.maj, t.per);
   MS2G_TRY(check_launch("k_backward"));
-  if (partial) {
-    const size_t np = (size_t)f.nc * f.nc, total = np * batch;
-    const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-    k_chunk_reduce<<<blocks, 256, 0, s>>>(p->w_part, nchunks, np, total, img, scale, accumulate);
-    MS2G_TRY(check_launch("k_chunk_reduce"));
-  }
-  return MS2G_OK;
+  const size_t np = (size_t)f.nc * f.nc, total = np * batch;
+  const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  k_chunk_reduce<<<blocks, 256, 0, s>>>(p->w_part, 2 * nchunks, np, total, img, scale, accumulate);
+  return check_launch("k_chunk_reduce");
 }
 
 }  // namespace ms2g

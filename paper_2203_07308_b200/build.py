@@ -36,17 +36,20 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Build libms2g.so (or, for kernel-variant experiments, `out` with extra -D defines)."""
+    target = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     inc, lib = nccl_dirs()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
            "-Xptxas", "-v" if verbose else "-O3",
+           *[f"-D{d}" for d in defines],
            f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}", *sources(),
-           f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", LIB + ".tmp"]
+           f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-o", target + ".tmp"]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

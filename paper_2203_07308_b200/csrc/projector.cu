@@ -189,11 +189,11 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 
 // --------------------------------------------------------------- adjoint --
 // Tile-driven ray scatter.  Two tile families cover the image: X-tiles
-// (32 columns x kBH rows) take only the major-x rays, Y-tiles (32 rows x kBH
+// (32 columns x H rows) take only the major-x rays, Y-tiles (32 rows x H
 // columns) only the major-y rays, so every block uses one accumulator layout
 // T[minor][major] whose long side is the MINOR axis: a ray of slope <= 1 then
-// crosses most of the 32 major lanes inside the tile (lane utilisation 0.84
-// at kBH = 64 against 0.73 for 32x32 tiles).  A block owns one tile and a
+// crosses most of the 32 major lanes inside the tile (modelled lane
+// utilisation 0.84 at H = 64, 0.88 at H = 96, against 0.73 for 32x32 tiles).  A block owns one tile and a
 // chunk of views; each warp takes one view at a time and walks the rays that
 // meet the tile, one per step, with LANE = major index inside the tile.  A
 // lane only touches its own major line of the warp's private accumulator (no
@@ -207,7 +207,7 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 // Step (the forward's weights): the lane's end coordinate E = Et + lane*S
 // gives u = floor(E) + 1 (tile-relative; upper row u - 1, lower row u - 2) and
 // m = min(frac32(E), S):   T[u - 1] += m (Ly32 r),   T[u - 2] += (S - m)(Ly32 r)
-// (Lc = S Ly32 up to rounding).  u is clamped to kBH + 2 (unsigned, so
+// (Lc = S Ly32 up to rounding).  u is clamped to H + 2 (unsigned, so
 // negatives clamp too) and every warp window has two pad rows on each side
 // (shared between neighbouring windows), so no predicate is needed.  Record
 // per ray: {lo(Et), hi(Et), S, Ly32 r}, one broadcast LDS.128 per step.  The
@@ -216,27 +216,35 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 // The X- and Y-families write separate partial planes (per view chunk too);
 // k_chunk_reduce sums them in fixed order.
 constexpr int kBT = 32;                          // major extent (lanes)
-constexpr int kBH = 64;                          // minor extent (rows)
 constexpr int kBW = 4;                           // warps per block
 constexpr int kPadR = 2;
-constexpr int kWinR = kBH + kPadR;               // rows per warp window (+ shared pads)
-constexpr int kAccRows = kPadR + kBW * kWinR;
+// minor extent H of the tiles: 64 (6 blocks of 36 KB per SM) or, for n_c >=
+// 1024, 96 (4 blocks of 51 KB; lane utilisation 0.88, measured 10 % faster
+// at 1024^2 and slower on coarser grids)
+int bp_height(int nc) { return nc >= 1024 ? 96 : 64; }
+template <int H>
+struct BpShape {
+  static constexpr int kWinR = H + kPadR;                // rows per warp window (+ shared pads)
+  static constexpr int kAccRows = kPadR + kBW * kWinR;
+  static constexpr size_t kSmem = sizeof(float) * kAccRows * kBT;
+  static constexpr int kMinBlocks = H <= 64 ? 6 : 4;
+};
 
 struct BpTiling {
   int maj, mnr, per;   // tiles along the major axis, along the minor axis, per family
 };
-static inline BpTiling bp_tiling(int nc) {
+static inline BpTiling bp_tiling(int nc, int H) {
   BpTiling t;
   t.maj = (nc + kBT - 1) / kBT;
-  t.mnr = (nc + kBH - 1) / kBH;
+  t.mnr = (nc + H - 1) / H;
   t.per = t.maj * t.mnr;
   return t;
 }
-int bp_tile_count(int nc) { return 2 * bp_tiling(nc).per; }
+int bp_tile_count(int nc) { return 2 * bp_tiling(nc, bp_height(nc)).per; }
 
 // Per (tile, view): bins [ta_r, te_r] of run r (r < n) of the tile family's
 // major axis, class cls_r.
-__global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B, int nc, int tmaj, int per,
+__global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B, int nc, int H, int tmaj, int per,
                             int4* __restrict__ out, int* __restrict__ err) {
   const size_t n = (size_t)2 * per * V_r;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -244,8 +252,8 @@ __global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B,
     const int tile = (int)(i / V_r);
     const int fam = tile >= per;
     const int ti = tile - fam * per;
-    const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * kBH;
-    const int c1 = min(c0 + kBT, nc), m1 = min(m0 + kBH, nc);
+    const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * H;
+    const int c1 = min(c0 + kBT, nc), m1 = min(m0 + H, nc);
     const float x0 = fam ? m0 : c0, x1 = fam ? m1 : c1, y0 = fam ? c0 : m0, y1 = fam ? c1 : m1;
     const ViewEntry V = views[g];
     float tmin = INFINITY, tmax = -INFINITY;
@@ -272,19 +280,23 @@ __global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B,
 }
 
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s) {
-  const BpTiling t = bp_tiling(f.nc);
+  const int H = bp_height(f.nc);
+  const BpTiling t = bp_tiling(f.nc, H);
   const size_t n = (size_t)2 * t.per * V_r;
   const int blocks = (int)((n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192);
-  k_bp_ranges<<<blocks, 256, 0, s>>>(f.d_views, V_r, B, f.nc, t.maj, t.per, out, err);
+  k_bp_ranges<<<blocks, 256, 0, s>>>(f.d_views, V_r, B, f.nc, H, t.maj, t.per, out, err);
   return check_launch("k_bp_ranges");
 }
 
-__global__ void __launch_bounds__(32 * kBW, 6) k_backward(const RayEntry* __restrict__ rays,
+template <int H>
+__global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(const RayEntry* __restrict__ rays,
                                                           const int4* __restrict__ ranges, int V_r, int B,
                                                           const int* __restrict__ sel, int n_sel, int vpc,
                                                           const float* __restrict__ sino, float* __restrict__ part,
                                                           int nc, int tmaj, int per) {
-  __shared__ float acc[kAccRows * kBT];
+  extern __shared__ float4 dyn_smem[];
+  float* acc = reinterpret_cast<float*>(dyn_smem);   // kAccRows x kBT (dynamic: may exceed 48 KB)
+  constexpr int kBH = H, kWinR = BpShape<H>::kWinR, kAccRows = BpShape<H>::kAccRows;
   __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
@@ -450,22 +462,33 @@ __global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size
   }
 }
 
+template <int H>
+static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const float* sino,
+                      const int* d_sel, int n_sel, int vpc, const BpTiling& t) {
+  constexpr size_t smem = BpShape<H>::kSmem;
+  static bool attr = false;
+  if (!attr) {   // several blocks of 36-51 KB per SM need the maximum shared-memory carveout
+    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    attr = true;
+  }
+  k_backward<H><<<grid, 32 * kBW, smem, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino, p->w_part,
+                                             f.nc, t.maj, t.per);
+  return MS2G_OK;
+}
+
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s) {
-  const BpTiling t = bp_tiling(f.nc);
+  const int H = bp_height(f.nc);
+  const BpTiling t = bp_tiling(f.nc, H);
   int nchunks = f.bp_chunks;
   const int max_chunks = (n_sel + kBW - 1) / kBW;
   if (nchunks > max_chunks) nchunks = max_chunks;
   if (nchunks < 1) nchunks = 1;
   const int vpc = (n_sel + nchunks - 1) / nchunks;
-  static bool attr = false;
-  if (!attr) {   // 6 blocks of 37 KB per SM need the maximum shared-memory carveout
-    cudaFuncSetAttribute(k_backward, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr = true;
-  }
   dim3 grid(2 * t.per, nchunks, batch);
-  k_backward<<<grid, 32 * kBW, 0, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino, p->w_part, f.nc,
-                                       t.maj, t.per);
+  if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, vpc, t));
+  else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, vpc, t));
   MS2G_TRY(check_launch("k_backward"));
   const size_t np = (size_t)f.nc * f.nc, total = np * batch;
   const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);

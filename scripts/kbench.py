@@ -17,7 +17,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=4)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--lib", default=None, help="alternative libms2g build (kernel-variant experiments)")
 a = ap.parse_args()
+if a.lib:
+    P._LIBPATH = a.lib
 pr = S.PRESETS[a.cfg]
 nnz = json.load(open(os.path.join(ROOT, "profiles", "nnz_counts.json")))[f"C{a.cfg}"]
 plan = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(4, 2, 1), batch=a.batch)

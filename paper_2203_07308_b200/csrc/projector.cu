@@ -41,8 +41,10 @@ __device__ __forceinline__ void seg_weights(unsigned lo, bool cross, float Lc, f
 // the grid.  Four images, indexed by the ray class (flags & 3):
 //   0 major-x      : lines = columns j of x, pairs along rows     (x^T)
 //   1 major-y      : lines = rows i of x,    pairs along columns
-//   2 major-x, mirrored: as 0 with each pair reversed (v[k+1], v[k])
-//   3 major-y, mirrored: as 1 reversed
+//   2 major-x, mirrored: as 0 with each pair reversed (v[k+1], v[k]) and
+//      each line stored back to front (element nc - k holds it), so that the
+//      forward indexes every class the same way
+//   3 major-y, mirrored: as 1, reversed likewise
 __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pairs, size_t pair_stride, int nc) {
   __shared__ float T[33][33];
   const int bz = blockIdx.z;
@@ -63,14 +65,15 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
     if (line >= nc) break;
     const size_t e = ib + (size_t)line * L + o;
     const float a = T[threadIdx.x][jj], b = T[threadIdx.x + 1][jj];   // x[o-2][line], x[o-1][line]
+    const size_t er = ib + (size_t)line * L + (nc + 2 - o);   // back-to-front line
     pairs[e] = make_float2(a, b);
-    pairs[2 * pair_stride + e] = make_float2(b, a);
+    pairs[2 * pair_stride + er] = make_float2(b, a);
     const int k = o - 2;
     const float* row = xb + (size_t)line * nc;
     const float c = (k >= 0 && k < nc) ? row[k] : 0.f;
     const float d = (k + 1 >= 0 && k + 1 < nc) ? row[k + 1] : 0.f;
     pairs[pair_stride + e] = make_float2(c, d);
-    pairs[3 * pair_stride + e] = make_float2(d, c);
+    pairs[3 * pair_stride + er] = make_float2(d, c);
   }
 }
 
@@ -130,25 +133,23 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
     const int L = nc + 3;
     const size_t istride = (size_t)nc * L;          // pair-image stride between batch images
     const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
-    // element of pair index u on line c: c L + u (plain) or c L + nc + 2 - u
-    // (mirrored images store (v[k+1], v[k]) at k + 2); u is clamped to the
-    // zero pads (unsigned: negatives clamp too)
-    const bool mir = cls & kMirror;
-    const int kb = mir ? nc + 2 : 0, ks = mir ? -1 : 1;
+    // element of pair index u on line c: c L + u for every class (the
+    // mirrored images are stored back to front); u is clamped to the zero
+    // pads (unsigned: negatives clamp too)
     const unsigned umax = (unsigned)(nc + 2);
     const long long Es = F0 + (long long)wcl * (long long)S + (long long)S + (1LL << 32);
     unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
-    int offk = wcl * L + kb;
+    unsigned offk = (unsigned)(wcl * L);
 #pragma unroll 4
     for (int c = wcl; c < wch; ++c) {
       unsigned lo1, hi1;
       asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
       const float mf = (float)min(elo, S);
-      const int e = offk + ks * (int)min(ehi, umax);
+      const unsigned e = offk + min(ehi, umax);
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
         float pl, pu;
-        asm("{\n\t.reg .u64 ad;\n\tmad.wide.s32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
+        asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
             : "=f"(pl), "=f"(pu) : "r"(e), "l"(base + i * istride));
         sa[i] += pl;
         sb[i] = fmaf(mf, pu - pl, sb[i]);

@@ -160,7 +160,11 @@ typedef struct {
   uint64_t seed;
   ms2g_denoiser den;
   float alpha;           /* RED-PRO mix weight, 0 < alpha <= 1      */
-  int32_t power_iters;   /* per-stage power iterations (20 in the configs) */
+  int32_t power_iters;   /* per-stage power iterations (20 in the configs); 0 = reuse, for
+                            each stage factor, the step L, eta = 1/L of the last power
+                            iteration run on this plan for that factor (by an earlier solve
+                            or ms2g_power_iteration): L depends on the geometry only
+                            (SURVEY 8(e)).  MS2G_ERR_CONFIG if none has run. */
   int32_t check_every;   /* unused by the graph path: every step is checked on device */
   int32_t resampler;     /* MS2G_RESAMPLE_MEAN (configs) | MS2G_RESAMPLE_BICUBIC (paper) */
 } ms2g_solve_desc;

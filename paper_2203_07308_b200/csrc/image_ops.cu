@@ -434,6 +434,19 @@ int launch_power_step(int nc, int /*batch*/, const float* v, const float* w, dou
   return MS2G_OK;
 }
 
+// {L, eta, (float) eta} from a factor's cache into a stage's slots (each may be NULL)
+__global__ void k_cached_step(const double* __restrict__ cache, double* L_out, double* eta_out, float* etaf_out) {
+  if (L_out) *L_out = cache[0];
+  if (eta_out) *eta_out = cache[1];
+  if (etaf_out) *etaf_out = reinterpret_cast<const float*>(cache + 2)[0];
+}
+
+int launch_cached_step(const double* cache, double* L_out, double* eta_out, float* etaf_out, cudaStream_t st) {
+  if (!L_out && !eta_out && !etaf_out) return MS2G_OK;
+  k_cached_step<<<1, 1, 0, st>>>(cache, L_out, eta_out, etaf_out);
+  return check_launch("k_cached_step");
+}
+
 __global__ void k_init_flag(int* flag) { *flag = INT_MAX; }
 
 int launch_init_flag(int* flag, cudaStream_t st) {

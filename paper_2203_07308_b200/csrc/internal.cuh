@@ -53,6 +53,11 @@ struct FactorTables {
   RayEntry* d_rays = nullptr;     // [V_r][B]
   ViewEntry* d_views = nullptr;   // [V_r]
   int bp_chunks = 1;              // view chunks of the backprojector
+  // step size cached per factor by the last power iteration on this plan:
+  // d_Lcache = {L, eta} (double), then eta as float; L_iters = its iteration
+  // count as enqueued (0 = none yet).  L depends on the geometry only.
+  double* d_Lcache = nullptr;
+  mutable int L_iters = 0;
   int4* d_bpr = nullptr;          // per (adjoint tile, view): bin runs meeting the tile
   // bicubic resampling tables (NEXT-1), [n_out][taps] clamped input index / weight
   int taps_down = 0, taps_up = 0;
@@ -192,5 +197,6 @@ int launch_power_step(int nc, int batch, const float* v, const float* w, double*
                       double* pw, double* L_out, float* vnext, double* eta_out,
                       float* etaf_out, cudaStream_t st);
 int launch_init_flag(int* flag, cudaStream_t st);
+int launch_cached_step(const double* cache, double* L_out, double* eta_out, float* etaf_out, cudaStream_t st);
 
 }  // namespace ms2g

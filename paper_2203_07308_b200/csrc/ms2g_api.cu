@@ -121,6 +121,8 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   MS2G_CUDA(cudaMemcpy(f.d_rays, rays.data(), sizeof(RayEntry) * rays.size(), cudaMemcpyHostToDevice));
   MS2G_CUDA(cudaMemcpy(f.d_views, views.data(), sizeof(ViewEntry) * views.size(), cudaMemcpyHostToDevice));
   MS2G_TRY(build_bicubic_tables(f, d.n));
+  MS2G_CUDA(cudaMalloc(&f.d_Lcache, 3 * sizeof(double)));
+  MS2G_CUDA(cudaMemset(f.d_Lcache, 0, 3 * sizeof(double)));
   {  // adjoint tile/view bin ranges (geometry only, once per plan)
     int* d_err = nullptr;
     MS2G_CUDA(cudaMalloc(&f.d_bpr, sizeof(int4) * (size_t)bp_tile_count(nc) * V_r));
@@ -162,6 +164,7 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(f.d_idx_up);
     cudaFree(f.d_w_up);
   }
+  for (auto& f : p->ft) cudaFree(f.d_Lcache);
   cudaFree(p->w_pair);
   float* fl[] = {p->w_v, p->w_rs, p->w_snap, p->w_mu, p->w_G, p->w_res, p->w_part, p->w_x[0], p->w_x[1],
                  p->w_y, p->w_z, p->w_p[0], p->w_p[1], p->w_etaf};
@@ -249,11 +252,16 @@ static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double*
     MS2G_TRY(launch_backward(p, f, p->w_res, p->w_G, 1.f, 0, nullptr, p->V_r, 1, st));
     MS2G_TRY(allreduce(p, p->w_G, np, st));
     const bool last = (k == iters - 1);
-    MS2G_TRY(launch_power_step(f.nc, 1, p->w_v, p->w_G, p->w_red, p->red_blocks, p->w_pw, last ? L_out : nullptr,
-                               last ? nullptr : p->w_v, last ? eta_out : nullptr, last ? etaf_out : nullptr, st));
+    double* cache = f.d_Lcache;
+    MS2G_TRY(launch_power_step(f.nc, 1, p->w_v, p->w_G, p->w_red, p->red_blocks, p->w_pw, last ? cache : nullptr,
+                               last ? nullptr : p->w_v, last ? cache + 1 : nullptr,
+                               last ? reinterpret_cast<float*>(cache + 2) : nullptr, st));
     if (!last) MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_v, st));
   }
-  return MS2G_OK;
+  // the last Rayleigh quotient went to the factor's cache (reused by solves
+  // with power_iters = 0); hand it to the caller's slots
+  f.L_iters = iters;
+  return launch_cached_step(f.d_Lcache, L_out, eta_out, etaf_out, st);
 }
 
 static int denoise_mix(ms2g_plan* p, const ms2g_denoiser& den, const float* z, const float* xprev, float* xout,
@@ -409,7 +417,10 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
   for (int k = 0; k < sd->n_stages; ++k) {
     const ms2g_stage& stg = sd->stages[k];
     const FactorTables* f = find_factor(p, stg.factor);
-    MS2G_TRY(enqueue_power(p, *f, sd->power_iters, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
+    if (sd->power_iters > 0)
+      MS2G_TRY(enqueue_power(p, *f, sd->power_iters, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
+    else   // reuse the plan's cached step for this factor (geometry-only, S8(e))
+      MS2G_TRY(launch_cached_step(f->d_Lcache, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
     int step_in_stage = 0;
     if (sd->option == 5 && step < sch.size() && sch[step].stage == k) {
       // SAGA table at the stage start: phi_q = c_q A_{M_q}^T (A_{M_q} S y - b), avg = mean_q phi_q
@@ -517,14 +528,18 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
                         cudaStream_t st) {
   if (!b || !x0 || !x_out) return set_error(MS2G_ERR_INPUT, "NULL b/x0/x_out");
   if (!(sd->alpha > 0.f && sd->alpha <= 1.f)) return set_error(MS2G_ERR_CONFIG, "alpha must be in (0, 1] (S:197)");
-  if (sd->power_iters < 1) return set_error(MS2G_ERR_CONFIG, "power_iters must be >= 1");
+  if (sd->power_iters < 0) return set_error(MS2G_ERR_CONFIG, "power_iters must be >= 0");
   if (sd->resampler != 0 && sd->resampler != 1) return set_error(MS2G_ERR_CONFIG, "resampler must be 0 or 1");
   MS2G_TRY(check_denoiser(sd->den));
   std::vector<ms2g_sched_entry> sch;
   MS2G_TRY(make_schedule(p, sd, sch));
-  for (int k = 0; k < sd->n_stages; ++k)
-    if (!find_factor(p, sd->stages[k].factor))
-      return set_error(MS2G_ERR_CONFIG, "stage factor was not planned (ms2g_plan_geometry factors)");
+  for (int k = 0; k < sd->n_stages; ++k) {
+    const FactorTables* f = find_factor(p, sd->stages[k].factor);
+    if (!f) return set_error(MS2G_ERR_CONFIG, "stage factor was not planned (ms2g_plan_geometry factors)");
+    if (sd->power_iters == 0 && f->L_iters == 0)
+      return set_error(MS2G_ERR_CONFIG, "power_iters = 0 reuses a cached step, but no power iteration has run "
+                                        "on this plan for a stage factor");
+  }
   if (!find_factor(p, 1) && p->nmax_c < p->d.n)
     return set_error(MS2G_ERR_CONFIG, "the solve needs full-resolution workspaces: plan factor 1 as well");
   if (sd->option == 2 || sd->option == 3 || sd->option == 5) MS2G_TRY(prepare_subsets(p, sd->n_subsets));

@@ -48,7 +48,9 @@ def full(rep, out, traffic_json=None):
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread",
-            "launch__grid_size", "sm__inst_executed_pipe_fp64.sum"]
+            "launch__grid_size", "sm__inst_executed_pipe_fp64.sum",
+            "l1tex__data_pipe_lsu_wavefronts.sum", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__throughput.avg.pct_of_peak_sustained_active"]
     lines = [f"# ncu --set full summary ({rep})", "", "| id | kernel | " + " | ".join(w for w in want) + " |",
              "|" + "---|" * (len(want) + 2)]
     traffic = {}
@@ -63,13 +65,19 @@ def full(rep, out, traffic_json=None):
                 v = float(r[hdr.index(w)]); u = units[hdr.index(w)]
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             key = name.split("::")[-1].replace("void ", "").split("<")[0].strip()
-            traffic.setdefault(key, []).append(tob("dram__bytes_read.sum") + tob("dram__bytes_write.sum"))
+            traffic.setdefault(key, []).append(
+                (tob("dram__bytes_read.sum") + tob("dram__bytes_write.sum"),
+                 float(r[hdr.index("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")]) / 100.0))
         except Exception:
             pass
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
-    if traffic_json:
-        json.dump({k: v for k, v in traffic.items()}, open(traffic_json, "w"), indent=1)
+    if traffic_json:   # launches of each kernel in capture order: factor 2, then factor 1 (profile_run.py)
+        out_t = {"source": f"{rep} (scripts/profile_run.py --mode kernels; C4); dram read+write bytes per launch"}
+        for k, v in traffic.items():
+            out_t[k] = {str(f): b for f, (b, _) in zip((2, 1), v)}
+            out_t[k + ":l1_pipe_frac"] = {str(f): q for f, (_, q) in zip((2, 1), v)}
+        json.dump(out_t, open(traffic_json, "w"), indent=1)
 
 
 if __name__ == "__main__":

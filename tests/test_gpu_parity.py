@@ -506,3 +506,24 @@ def test_saga_option5_solve(P):
                                    den=("tv", 0.01, 10), alpha=1.0))[0]
     xr, _, _ = O.pnp_ms2g(g, stages, b, option=5, n_subsets=8, seed=11, den=("tv", 0.01, 10), alpha=1.0)
     assert rel(xo, xr) <= TOL_SOLVE, rel(xo, xr)
+
+
+def test_solve_reuses_cached_step(P):
+    """power_iters = 0 reuses the plan's per-factor step (L depends on the
+    geometry only): same iterates bit for bit as the solve that
+    computed it, same trace; a plan with no power iteration yet refuses."""
+    pr = S.PRESETS[1]
+    g, xt, b = _make_data(pr, 1)
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1)) as plan:
+        with pytest.raises(P.MS2GError) as e:
+            P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha, power_iters=0)
+        assert e.value.code == 2
+        x1, tr1 = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha, trace=True)
+        x2, tr2 = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha, trace=True,
+                                   power_iters=0)
+        assert torch.equal(x1, x2)
+        assert tr1 == tr2
+        L = P.power_iteration(plan, 2, 20)   # refreshes the cache with the same value
+        x3 = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha, power_iters=0)
+        assert torch.equal(x1, x3)
+        assert abs(L - tr1[0][4] ** -1) <= 1e-12 * L

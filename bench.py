@@ -229,6 +229,37 @@ def detail_512(P, dev):
     return out
 
 
+def shard_estimate(P, dev, pr, b_full, t_solve_1):
+    """Multi-GPU scaling ESTIMATE for view sharding (only one GPU
+    here): the solve on rank 0's contiguous view shard [0, V/N) timed on this
+    GPU without a communicator (same kernels, 1/N of the views), plus a
+    modelled allreduce per gradient and per power iteration: 20 us latency +
+    2 x bytes at 450 GB/s (NVLink 5 ring bus bandwidth, conservative vs NVLS).
+    Not measured scaling: labelled estimated."""
+    import torch
+    out = {}
+    n_ar = {2: pr.power_iters + sum(s_[1] for s_ in pr.stages if s_[0] == 2),
+            1: pr.power_iters + sum(s_[1] for s_ in pr.stages if s_[0] == 1)}
+    t_ar = sum(n * (20e-6 + 2 * 4 * (pr.n // f) ** 2 / 450e9) for f, n in n_ar.items())
+    for nr in (2, 4, 8):
+        vb, ve = P.view_shard(pr.n_views, 0, nr)
+        with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve) as plan:
+            b = torch.from_numpy(np.ascontiguousarray(b_full[vb:ve])).to(dev)[None].contiguous()
+            x0 = torch.zeros((1, pr.n, pr.n), device=dev); xo = torch.empty_like(x0)
+            kw = dict(den=pr.den, alpha=pr.alpha, power_iters=pr.power_iters)
+            ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr.stages, b, x0, xo, **kw), 3, warm=2)
+            try:
+                P.solve_status(plan)
+            except P.MS2GError:
+                pass      # a shard's partial operator alone may drive the toy iterate anywhere; timing only
+        t = ts + t_ar
+        out[f"N{nr}"] = {"shard_solve_ms": ts * 1e3, "allreduce_model_ms": t_ar * 1e3,
+                         "est_iters_per_s": pr.n_steps / t, "est_speedup": t_solve_1 / t}
+    out["note"] = ("estimated: rank-0 shard timed on 1 GPU (L2 not flushed) + modelled allreduce; "
+                   "not measured scaling")
+    return out
+
+
 def run_ms2g(args, rank, nranks, local_rank):
     import torch
     import torch.distributed as dist
@@ -395,6 +426,7 @@ def run_ms2g(args, rank, nranks, local_rank):
 
     if nranks == 1 and not args.no_detail:
         detail.update(detail_512(P, dev))
+        detail["C4_view_shard_estimate"] = shard_estimate(P, dev, pr, b_full, t_total / args.steps)
 
     cpu = None
     if rank == 0 and nranks == 1 and not args.no_cpu:

@@ -52,7 +52,7 @@ struct FactorTables {
   int factor = 0, nc = 0;
   RayEntry* d_rays = nullptr;     // [V_r][B]
   ViewEntry* d_views = nullptr;   // [V_r]
-  int bp_chunks = 1;              // view chunks of the backprojector
+  int bp_chunks[2] = {1, 1};      // view chunks of the backprojector per tile family (X, Y)
   // step size cached per factor by the last power iteration on this plan:
   // d_Lcache = {L, eta} (double), then eta as float; L_iters = its iteration
   // count as enqueued (0 = none yet).  L depends on the geometry only.
@@ -90,7 +90,7 @@ struct ms2g_plan {
   float* w_rs = nullptr;               // separable-resampling intermediate [batch][n][n]
   float* w_G = nullptr;                // coarse gradient / backprojection
   float* w_res = nullptr;              // residual / projection [batch][V_r][B]
-  float* w_part = nullptr;             // backprojection partial planes [batch][chunk][X/Y family][n_c^2]
+  float* w_part = nullptr;             // backprojection partial planes [batch][X chunks, Y chunks][n_c^2]
   size_t part_elems = 0;
   float* w_x[2] = {nullptr, nullptr};  // iterate double buffer (full res)
   float* w_y = nullptr;                // extrapolated point

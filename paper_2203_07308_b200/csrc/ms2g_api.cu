@@ -142,14 +142,28 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   // small fraction of the launch (measured on B200, C4: 8 waves for 1024^2,
   // 24 waves for coarser grids; the chunk partials are summed by
   // k_chunk_reduce in fixed order)
+  // The X- and Y-tile families only see the views with major-x / major-y
+  // rays; a contiguous view shard (e.g. 45 degrees at P = 8) is almost all
+  // one class, so each family gets view chunks in proportion to its views.
   const long long tiles = (long long)bp_tile_count(nc) * d.batch;
+  const long long per = tiles / 2;
   const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : (tiles >= 1024 ? 8 : 24);
   const long long target = waves * sm_count;
-  long long ch = (target + tiles - 1) / tiles;
+  long long nv[2] = {0, 0};
+  for (const ViewEntry& ve : views) {
+    int mask = 0;
+    for (int k = 0; k < ve.nseg; ++k) mask |= (ve.seg_cls[k] & kMajorY) ? 2 : 1;
+    nv[0] += mask & 1;
+    nv[1] += (mask >> 1) & 1;
+  }
   const long long maxch = (V_r + 3) / 4;
-  if (ch > maxch) ch = maxch;
-  if (ch < 1) ch = 1;
-  f.bp_chunks = (int)ch;
+  for (int fam = 0; fam < 2; ++fam) {
+    const long long share = (target * nv[fam] + (nv[0] + nv[1]) - 1) / std::max(1LL, nv[0] + nv[1]);
+    long long ch = (share + per - 1) / per;
+    if (ch > maxch) ch = maxch;
+    if (ch < 1) ch = 1;
+    f.bp_chunks[fam] = (int)ch;
+  }
   return MS2G_OK;
 }
 
@@ -671,7 +685,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
       return rc;
     }
     if (f.nc > p->nmax_c) p->nmax_c = f.nc;
-    const size_t need = (size_t)2 * f.bp_chunks * f.nc * f.nc * d.batch;   // X/Y families x chunks
+    const size_t need = (size_t)(f.bp_chunks[0] + f.bp_chunks[1]) * f.nc * f.nc * d.batch;   // family chunks
     if (need > part) part = need;
   }
   const size_t bt = d.batch;

@@ -86,7 +86,7 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
 // ---------------------------------------------------------------- forward --
 // One thread per ray; a warp holds 32 consecutive bins of one view, so at a
 // given column the lanes read adjacent minor indices of the same pair-image
-// line (coalesced).  The 8 warps of a block are 8 consecutive views over the
+// line (coalesced).  The 4 warps of a block are 4 consecutive views over the
 // same bins, tracing nearly the same lines: L1 reuse.  Residual epilogue fused
 // ("A_s v - b").
 //
@@ -99,22 +99,37 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
 // so  sum_c w.x = Lc sum_c x_lower + Ly32 sum_c m (x_upper - x_lower): the
 // per-ray constants leave the column loop.  Without a crossing the lower-row
 // weight is a rounding residual (|.| <= 2^-23 Lc), not an exact zero.
-constexpr int kFwdWarps = 8;
+#ifndef MS2G_FWD_WARPS
+#define MS2G_FWD_WARPS 4
+#endif
+constexpr int kFwdWarps = MS2G_FWD_WARPS;
+#ifndef MS2G_FWD_UNROLL
+#define MS2G_FWD_UNROLL 4
+#endif
+constexpr int kFwdUnroll = MS2G_FWD_UNROLL;
 
 // NB images of a batch share one traversal: the weights of a column are
 // computed once and applied to NB pair images (C5: 8 reconstructions per GPU).
-template <int NB>
-__global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
+// SPLIT > 1 cuts each warp's column range into SPLIT equal segments taken by
+// SPLIT warps of the block (the same 32 rays), summed through shared memory in
+// fixed order: more, shorter work units for launches with few views (a view
+// shard, a minibatch) whose single wave would otherwise wait on its longest
+// rays.
+template <int NB, int SPLIT>
+__global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out) {
+  constexpr int VPB = kFwdWarps / SPLIT;             // views per block
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k = blockIdx.y * kFwdWarps + warp;
-  if (k >= n_sel) return;
+  const int q = warp % SPLIT;                        // column segment of this warp
+  const int k = blockIdx.y * VPB + warp / SPLIT;
+  if (SPLIT == 1 && k >= n_sel) return;
+  const bool vk = k < n_sel;
   const int t = blockIdx.x * 32 + lane;
   const int bz0 = blockIdx.z * NB;
-  const int g = sel ? __ldg(sel + k) : k;
-  const bool valid = t < B;
+  const int g = (sel && vk) ? __ldg(sel + k) : k;
+  const bool valid = vk && t < B;
   long long F0 = 0;
   unsigned S = 1;
   float Lc = 0.f, Ly32 = 0.f;
@@ -124,8 +139,14 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
     F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; cls = R.flags & 3;
     if (R.c_lo < R.c_hi) { cl = R.c_lo; ch = R.c_hi; }
   }
-  const int wcl = __reduce_min_sync(0xffffffffu, cl);
-  const int wch = __reduce_max_sync(0xffffffffu, ch);
+  int wcl = __reduce_min_sync(0xffffffffu, cl);
+  int wch = __reduce_max_sync(0xffffffffu, ch);
+  if (SPLIT > 1 && wcl < wch) {
+    const int len = wch - wcl;
+    const int c0 = wcl + (q * len) / SPLIT, c1 = wcl + ((q + 1) * len) / SPLIT;
+    wcl = c0;
+    wch = c1;
+  }
   float sa[NB], sb[NB];
 #pragma unroll
   for (int i = 0; i < NB; ++i) { sa[i] = 0.f; sb[i] = 0.f; }
@@ -140,7 +161,7 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
     const long long Es = F0 + (long long)wcl * (long long)S + (long long)S + (1LL << 32);
     unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
     unsigned offk = (unsigned)(wcl * L);
-#pragma unroll 4
+#pragma unroll kFwdUnroll
     for (int c = wcl; c < wch; ++c) {
       unsigned lo1, hi1;
       asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
@@ -159,6 +180,25 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
       offk += L;
     }
   }
+  if (SPLIT > 1) {   // segment partials -> the q = 0 warp of each view, fixed order
+    __shared__ float2 red[kFwdWarps][NB][32];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) red[warp][i][lane] = make_float2(sa[i], sb[i]);
+    __syncthreads();
+    if (q != 0) return;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int j = 0; j < SPLIT; ++j) {
+        const float2 v = red[warp + j][i][lane];
+        a += v.x;
+        b += v.y;
+      }
+      sa[i] = a;
+      sb[i] = b;
+    }
+  }
   if (valid) {
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -169,22 +209,37 @@ __global__ void __launch_bounds__(256) k_forward(const RayEntry* __restrict__ ra
   }
 }
 
+template <int NB, int SPLIT>
+static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
+                        const int* d_sel, const float* b, float* out) {
+  constexpr int VPB = kFwdWarps / SPLIT;
+  dim3 grid((p->B + 31) / 32, (n_sel + VPB - 1) / VPB, batch / NB);
+  k_forward<NB, SPLIT><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
+                                                       p->pair_stride, f.nc, b, out);
+}
+
 template <int NB>
-static void fwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const int* d_sel, int n_sel,
-                       const float* b, float* out) {
-  k_forward<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair, p->pair_stride,
-                                                f.nc, b, out);
+static void fwd_launch(int split, int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
+                       const int* d_sel, const float* b, float* out) {
+  if (split >= 4) fwd_launch2<NB, 4>(n_sel, batch, s, p, f, d_sel, b, out);
+  else if (split == 2) fwd_launch2<NB, 2>(n_sel, batch, s, p, f, d_sel, b, out);
+  else fwd_launch2<NB, 1>(n_sel, batch, s, p, f, d_sel, b, out);
 }
 
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s) {
   if (n_sel <= 0) return MS2G_OK;
   const int nb = (batch % 8 == 0) ? 8 : (batch % 4 == 0) ? 4 : (batch % 2 == 0) ? 2 : 1;
-  dim3 grid((p->B + 31) / 32, (n_sel + kFwdWarps - 1) / kFwdWarps, batch / nb);
-  if (nb == 8) fwd_launch<8>(grid, s, p, f, d_sel, n_sel, b, out);
-  else if (nb == 4) fwd_launch<4>(grid, s, p, f, d_sel, n_sel, b, out);
-  else if (nb == 2) fwd_launch<2>(grid, s, p, f, d_sel, n_sel, b, out);
-  else fwd_launch<1>(grid, s, p, f, d_sel, n_sel, b, out);
+  // column split (measured on B200: 4 for single images -- C4 s=1 0.80 ->
+  // 0.78 ms, its 180-view shard 0.18 -> 0.14 ms, C3 0.14 -> 0.12 ms -- and 2
+  // for batched traversals, C5 batch 8: 1.03 -> 0.73 ms); MS2G_FWD_SPLIT
+  // overrides it for experiments
+  int split = nb > 1 ? 2 : 4;
+  if (const char* e = getenv("MS2G_FWD_SPLIT")) split = atoi(e);
+  if (nb == 8) fwd_launch<8>(split, n_sel, batch, s, p, f, d_sel, b, out);
+  else if (nb == 4) fwd_launch<4>(split, n_sel, batch, s, p, f, d_sel, b, out);
+  else if (nb == 2) fwd_launch<2>(split, n_sel, batch, s, p, f, d_sel, b, out);
+  else fwd_launch<1>(split, n_sel, batch, s, p, f, d_sel, b, out);
   return check_launch("k_forward");
 }
 
@@ -292,17 +347,22 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
 template <int H>
 __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(const RayEntry* __restrict__ rays,
                                                           const int4* __restrict__ ranges, int V_r, int B,
-                                                          const int* __restrict__ sel, int n_sel, int vpc,
+                                                          const int* __restrict__ sel, int n_sel,
                                                           const float* __restrict__ sino, float* __restrict__ part,
-                                                          int nc, int tmaj, int per) {
+                                                          int nc, int tmaj, int per, int chx, int vpcx, int vpcy) {
   extern __shared__ float4 dyn_smem[];
   float* acc = reinterpret_cast<float*>(dyn_smem);   // kAccRows x kBT (dynamic: may exceed 48 KB)
   constexpr int kBH = H, kWinR = BpShape<H>::kWinR, kAccRows = BpShape<H>::kAccRows;
   __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile = blockIdx.x, chunk = blockIdx.y, bz = blockIdx.z;
-  const int fam = tile >= per;                     // 0: X-tile (major x), 1: Y-tile (major y)
-  const int ti = tile - fam * per;
+  // blockIdx.x = (family, view chunk, tile): X-family blocks first
+  const int bx = blockIdx.x, bz = blockIdx.z;
+  const int fam = bx >= per * chx;                 // 0: X-tile (major x), 1: Y-tile (major y)
+  const int bi = bx - fam * per * chx;
+  const int ti = bi % per, chunk = bi / per;
+  const int tile = fam * per + ti;                 // index into the range table
+  const int vpc = fam ? vpcy : vpcx;
+  const int plane = fam ? chx + chunk : chunk;
   const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * kBH;   // major / minor origin
   float* T = acc + (kPadR + warp * kWinR) * kBT;
   for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * kBW) acc[i] = 0.f;
@@ -423,7 +483,8 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     sum[i] = s;
   }
   const size_t np = (size_t)nc * nc;
-  float* dst = part + ((size_t)(bz * gridDim.y + chunk) * 2 + fam) * np;
+  const int nplanes = chx + (int)((gridDim.x - per * chx) / per);
+  float* dst = part + ((size_t)bz * nplanes + plane) * np;
   if (!fam) {       // X-tile: row l = y - m0, lane = x - c0 (coalesced)
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
@@ -465,7 +526,7 @@ __global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size
 
 template <int H>
 static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const float* sino,
-                      const int* d_sel, int n_sel, int vpc, const BpTiling& t) {
+                      const int* d_sel, int n_sel, const int* ch, const int* vpc, const BpTiling& t) {
   constexpr size_t smem = BpShape<H>::kSmem;
   static bool attr = false;
   if (!attr) {   // several blocks of 36-51 KB per SM need the maximum shared-memory carveout
@@ -473,8 +534,8 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
-  k_backward<H><<<grid, 32 * kBW, smem, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, vpc, sino, p->w_part,
-                                             f.nc, t.maj, t.per);
+  k_backward<H><<<grid, 32 * kBW, smem, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, sino, p->w_part,
+                                             f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1]);
   return MS2G_OK;
 }
 
@@ -482,18 +543,21 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s) {
   const int H = bp_height(f.nc);
   const BpTiling t = bp_tiling(f.nc, H);
-  int nchunks = f.bp_chunks;
-  const int max_chunks = (n_sel + kBW - 1) / kBW;
-  if (nchunks > max_chunks) nchunks = max_chunks;
-  if (nchunks < 1) nchunks = 1;
-  const int vpc = (n_sel + nchunks - 1) / nchunks;
-  dim3 grid(2 * t.per, nchunks, batch);
-  if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, vpc, t));
-  else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, vpc, t));
+  int ch[2], vpc[2];
+  for (int fam = 0; fam < 2; ++fam) {
+    ch[fam] = f.bp_chunks[fam];
+    const int max_chunks = (n_sel + kBW - 1) / kBW;
+    if (ch[fam] > max_chunks) ch[fam] = max_chunks;
+    if (ch[fam] < 1) ch[fam] = 1;
+    vpc[fam] = (n_sel + ch[fam] - 1) / ch[fam];
+  }
+  dim3 grid(t.per * (ch[0] + ch[1]), 1, batch);
+  if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t));
+  else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t));
   MS2G_TRY(check_launch("k_backward"));
   const size_t np = (size_t)f.nc * f.nc, total = np * batch;
   const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-  k_chunk_reduce<<<blocks, 256, 0, s>>>(p->w_part, 2 * nchunks, np, total, img, scale, accumulate);
+  k_chunk_reduce<<<blocks, 256, 0, s>>>(p->w_part, ch[0] + ch[1], np, total, img, scale, accumulate);
   return check_launch("k_chunk_reduce");
 }
 

@@ -17,13 +17,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=4)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--shard", type=int, default=1, help="time rank 0's contiguous view shard of N")
 ap.add_argument("--lib", default=None, help="alternative libms2g build (kernel-variant experiments)")
 a = ap.parse_args()
 if a.lib:
     P._LIBPATH = a.lib
 pr = S.PRESETS[a.cfg]
 nnz = json.load(open(os.path.join(ROOT, "profiles", "nnz_counts.json")))[f"C{a.cfg}"]
-plan = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(4, 2, 1), batch=a.batch)
+vb, ve = P.view_shard(pr.n_views, 0, a.shard)
+plan = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(4, 2, 1), batch=a.batch, view_begin=vb, view_end=ve)
 x = torch.from_numpy(S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg))).cuda()[None].repeat(a.batch, 1, 1).contiguous()
 
 
@@ -45,6 +47,6 @@ for s in (4, 2, 1):
     img = P.back_project(plan, s, out)
     tf = t(lambda: P.forward_project(plan, s, xs, out=out))
     tb = t(lambda: P.back_project(plan, s, out, img=img))
-    seg = nnz[str(s)] * a.batch
+    seg = nnz[str(s)] * a.batch * (ve - vb) / pr.n_views
     res[s] = dict(fwd_ms=round(tf, 4), bwd_ms=round(tb, 4), fwd_gnnz=round(seg / tf / 1e6, 1), bwd_gnnz=round(seg / tb / 1e6, 1))
 print(json.dumps(res))

@@ -86,6 +86,8 @@ def load():
     L.ms2g_plan_destroy.restype = None
     L.ms2g_nccl_unique_id.argtypes = [p]
     L.ms2g_attach_nccl.argtypes = [p, p, i, i]
+    L.ms2g_peer_export.argtypes = [p, p]
+    L.ms2g_attach_peers.argtypes = [p, p, i, i]
     L.ms2g_forward_project.argtypes = [p, i, p, p, p, C.POINTER(C.c_int32), i, p]
     L.ms2g_back_project.argtypes = [p, i, p, p, f, i, C.POINTER(C.c_int32), i, i, p]
     L.ms2g_sketch_down.argtypes = [p, i, i, p, p, p]
@@ -379,6 +381,31 @@ def attach_nccl(plan: Plan, rank: int, nranks: int, group=None):
     _check(L.ms2g_attach_nccl(plan.handle, (C.c_uint8 * 128).from_buffer_copy(uid), rank, nranks))
     plan.rank, plan.nranks = rank, nranks
     return plan
+
+
+def gather_blobs(blob: bytes, rank: int, nranks: int, group=None) -> bytes:
+    """All-gather one fixed-size byte blob per rank (torch.distributed, any
+    backend; plumbing only) and return them concatenated in rank order."""
+    if nranks == 1:
+        return blob
+    import torch.distributed as dist
+    out = [None] * nranks
+    dist.all_gather_object(out, blob, group=group)
+    if any(not isinstance(b, (bytes, bytearray)) or len(b) != len(blob) for b in out):
+        raise MS2GError(MS2G_ERR_CONFIG, "peer blob exchange: blobs of different sizes")
+    return b"".join(bytes(b) for b in out)
+
+
+def attach_peers(plan: Plan, rank: int, nranks: int, group=None):
+    """NEXT-3: sum backprojections over NVLink peer memory (fused, fixed rank
+    order) instead of NCCL.  Every rank of the group must call it."""
+    L = load()
+    size = L.ms2g_peer_blob_size()
+    mine = C.create_string_buffer(size)
+    _check(L.ms2g_peer_export(plan.handle, mine))
+    allb = gather_blobs(mine.raw, rank, nranks, group)
+    buf = C.create_string_buffer(allb, len(allb))
+    _check(L.ms2g_attach_peers(plan.handle, buf, rank, nranks))
 
 
 def view_shard(n_views: int, rank: int, nranks: int):

@@ -117,6 +117,17 @@ struct ms2g_plan {
   // NCCL
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  // peer-memory allreduce (NEXT-3): exchange buffer of two slots, signal pad
+  // (words 0..63: per-rank epochs written by the peers, 64: local epoch,
+  // 65: time-out), device tables of every rank's buffer / pad
+  float* xch_buf = nullptr;
+  size_t xch_slot = 0;                 // floats per slot
+  unsigned* xch_pad = nullptr;
+  float** d_peer_bufs = nullptr;
+  unsigned** d_peer_pads = nullptr;
+  int* w_peer_err = nullptr;
+  int peer_rank = 0, peer_n = 0;       // peer_n > 0: attached
+  std::vector<void*> peer_opened;      // IPC mappings to close
   // graph cache
   ms2g::SolveGraph sg;
   int last_total_steps = 0;
@@ -170,8 +181,15 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
                    int batch, cudaStream_t s);
 int bp_tile_count(int nc);   // adjoint tiles (both families) of an n_c grid
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
+// publish != 0: write scale * A_s^T sino into the peer exchange slot (not img)
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
-                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s);
+                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish = 0);
+
+// ---- peer-memory allreduce (peer_reduce.cu, NEXT-3) ----
+int launch_peer_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st);
+int launch_peer_finish(ms2g_plan* p, float* out, size_t count, cudaStream_t st);
+int launch_chunk_reduce_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
+                                cudaStream_t st);
 
 // ---- image kernels (image_ops.cu) ----
 int launch_sketch_down(int n, int s, int batch, const float* x, float* v, cudaStream_t st);

@@ -195,6 +195,12 @@ static void free_plan(ms2g_plan* p) {
   if (p->sel_ev) cudaEventDestroy(p->sel_ev);
   if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
   if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
+  for (void* q : p->peer_opened) cudaIpcCloseMemHandle(q);
+  cudaFree(p->xch_buf);
+  cudaFree(p->xch_pad);
+  cudaFree(p->d_peer_bufs);
+  cudaFree(p->d_peer_pads);
+  cudaFree(p->w_peer_err);
   if (p->comm) ncclCommDestroy(p->comm);
   delete p;
 }
@@ -230,9 +236,24 @@ static int resolve_subset(ms2g_plan* p, const int32_t* subset, int n_subset, cud
 }
 
 static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
+  if (p->peer_n > 0) return launch_peer_allreduce(p, buf, count, st);   // NEXT-3 peer path wins
   if (!p->comm) return MS2G_OK;   // attached communicators are always used (1 rank: NCCL identity)
   MS2G_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, p->comm, st));
   return MS2G_OK;
+}
+
+// G = c A_s^T r summed over ranks.  With peers attached the backprojector's
+// chunk reduction publishes straight into the exchange slot (fused, no
+// separate collective); otherwise backprojection then NCCL (or nothing).
+static int backward_sum(ms2g_plan* p, const FactorTables& f, const float* sino, float* G, float c, const int* d_sel,
+                        int n_sel, int batch, cudaStream_t st) {
+  const size_t count = (size_t)f.nc * f.nc * batch;
+  if (p->peer_n > 0) {
+    MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st, 1));
+    return launch_peer_finish(p, G, count, st);
+  }
+  MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st));
+  return allreduce(p, G, count, st);
 }
 
 // g = c U_s A_s^T (A_s S_s x - b), into a full-resolution image.
@@ -247,8 +268,7 @@ static int enqueue_grad(ms2g_plan* p, const FactorTables& f, int kind, const flo
   MS2G_TRY(launch_pair_prep(p, f.nc, batch, v, st));
   MS2G_TRY(launch_forward(p, f, b, p->w_res, d_sel, n_sel, batch, st));  // r = A_s v - b
   float* G = (s > 1) ? p->w_G : g;
-  MS2G_TRY(launch_backward(p, f, p->w_res, G, c, 0, d_sel, n_sel, batch, st));      // G = c A_s^T r
-  MS2G_TRY(allreduce(p, G, (size_t)f.nc * f.nc * batch, st));
+  MS2G_TRY(backward_sum(p, f, p->w_res, G, c, d_sel, n_sel, batch, st));      // G = c A_s^T r (+ ranks)
   if (s > 1) MS2G_TRY(launch_resample_up_step(p, f, kind, batch, G, nullptr, nullptr, 0.f, g, st));  // U G
   return MS2G_OK;
 }
@@ -263,8 +283,7 @@ static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double*
   MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_v, st));
   for (int k = 0; k < iters; ++k) {
     MS2G_TRY(launch_forward(p, f, nullptr, p->w_res, nullptr, p->V_r, 1, st));
-    MS2G_TRY(launch_backward(p, f, p->w_res, p->w_G, 1.f, 0, nullptr, p->V_r, 1, st));
-    MS2G_TRY(allreduce(p, p->w_G, np, st));
+    MS2G_TRY(backward_sum(p, f, p->w_res, p->w_G, 1.f, nullptr, p->V_r, 1, st));
     const bool last = (k == iters - 1);
     double* cache = f.d_Lcache;
     MS2G_TRY(launch_power_step(f.nc, 1, p->w_v, p->w_G, p->w_red, p->red_blocks, p->w_pw, last ? cache : nullptr,
@@ -451,9 +470,7 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
         float* ph = p->w_saga + (size_t)q * ncimg;
         const float cq = (float)((double)p->d.n_views / (double)p->subset_global_len[q]);
         MS2G_TRY(launch_forward(p, *f, b, p->w_res, p->w_subsets + p->subset_off[q], p->subset_len[q], batch, st));
-        MS2G_TRY(launch_backward(p, *f, p->w_res, ph, cq, 0, p->w_subsets + p->subset_off[q], p->subset_len[q],
-                                 batch, st));
-        MS2G_TRY(allreduce(p, ph, ncimg, st));
+        MS2G_TRY(backward_sum(p, *f, p->w_res, ph, cq, p->w_subsets + p->subset_off[q], p->subset_len[q], batch, st));
         MS2G_TRY(launch_axpby(avg, avg, ph, 1.f, 1.f / (float)sd->n_subsets, ncimg, st));
       }
     }
@@ -486,8 +503,7 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
           }
           MS2G_TRY(launch_pair_prep(p, f->nc, batch, vs, st));
           MS2G_TRY(launch_forward(p, *f, b, p->w_res, nullptr, p->V_r, batch, st));
-          MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_mu, 1.f, 0, nullptr, p->V_r, batch, st));
-          MS2G_TRY(allreduce(p, p->w_mu, ncimg, st));
+          MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_mu, 1.f, nullptr, p->V_r, batch, st));
         }
         MS2G_TRY(launch_axpby(p->w_z, p->w_y, p->w_snap, 1.f, -1.f, img, st));   // d = y - xs
         const float* vd = p->w_z;
@@ -497,8 +513,7 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
         }
         MS2G_TRY(launch_pair_prep(p, f->nc, batch, vd, st));
         MS2G_TRY(launch_forward(p, *f, nullptr, p->w_res, d_sel, n_sel, batch, st));
-        MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
-        MS2G_TRY(allreduce(p, p->w_G, ncimg, st));
+        MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st));
         MS2G_TRY(launch_axpby(p->w_G, p->w_G, p->w_mu, 1.f, 1.f, ncimg, st));  // + mu
       } else {
         const float* v = p->w_y;
@@ -508,8 +523,7 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
         }
         MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
         MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st));
-        MS2G_TRY(launch_backward(p, *f, p->w_res, p->w_G, c, 0, d_sel, n_sel, batch, st));
-        MS2G_TRY(allreduce(p, p->w_G, ncimg, st));
+        MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st));
         if (sd->option == 5)   // G = new - phi_j + avg; phi_j = new; avg += (new - phi_j)/K
           MS2G_TRY(launch_saga(p->w_G, p->w_saga + (size_t)e.subset * ncimg,
                                p->w_saga + (size_t)sd->n_subsets * ncimg, sd->n_subsets, ncimg, st));
@@ -610,9 +624,11 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
 }
 
 static int solve_status(ms2g_plan* p, cudaStream_t st) {
-  int flag = INT_MAX;
+  int flag = INT_MAX, perr = 0;
   MS2G_CUDA(cudaMemcpyAsync(&flag, p->w_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (p->w_peer_err) MS2G_CUDA(cudaMemcpyAsync(&perr, p->w_peer_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   MS2G_CUDA(cudaStreamSynchronize(st));
+  if (perr) return set_error(MS2G_ERR_NCCL, "peer allreduce: barrier timed out (a rank never arrived)");
   if (flag != INT_MAX) {
     int stage = -1;
     for (const auto& e : p->last_sched)
@@ -772,6 +788,83 @@ int ms2g_attach_nccl(ms2g_plan* p, const void* uid, int32_t rank, int32_t nranks
   return MS2G_OK;
 }
 
+// ---- NEXT-3: peer-memory allreduce (peer_reduce.cu) ----
+namespace {
+struct PeerBlob {
+  uint64_t magic;
+  uint64_t slot;                 // floats per exchange slot
+  cudaIpcMemHandle_t buf, pad;
+};
+constexpr uint64_t kPeerMagic = 0x4d53324750454552ULL;   // "MS2GPEER"
+constexpr int kPadWords = 128;
+}  // namespace
+
+static int ensure_exchange(ms2g_plan* p) {
+  if (p->xch_buf) return MS2G_OK;
+  p->xch_slot = (size_t)p->nmax_c * p->nmax_c * p->d.batch;
+  MS2G_CUDA(cudaMalloc(&p->xch_buf, sizeof(float) * 2 * p->xch_slot));
+  MS2G_CUDA(cudaMalloc(&p->xch_pad, sizeof(unsigned) * kPadWords));
+  MS2G_CUDA(cudaMemset(p->xch_pad, 0, sizeof(unsigned) * kPadWords));
+  MS2G_CUDA(cudaMalloc(&p->w_peer_err, sizeof(int)));
+  MS2G_CUDA(cudaMemset(p->w_peer_err, 0, sizeof(int)));
+  return MS2G_OK;
+}
+
+int ms2g_peer_blob_size(void) { return (int)sizeof(PeerBlob); }
+
+int ms2g_peer_export(ms2g_plan* p, void* blob) {
+  if (!p || !blob) return set_error(MS2G_ERR_INPUT, "NULL plan/blob");
+  MS2G_TRY(ensure_exchange(p));
+  PeerBlob b{};
+  b.magic = kPeerMagic;
+  b.slot = p->xch_slot;
+  MS2G_CUDA(cudaIpcGetMemHandle(&b.buf, p->xch_buf));
+  MS2G_CUDA(cudaIpcGetMemHandle(&b.pad, p->xch_pad));
+  memcpy(blob, &b, sizeof(b));
+  return MS2G_OK;
+}
+
+int ms2g_attach_peers(ms2g_plan* p, const void* blobs, int32_t rank, int32_t nranks) {
+  if (!p || !blobs) return set_error(MS2G_ERR_INPUT, "NULL plan/blobs");
+  if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) return set_error(MS2G_ERR_CONFIG, "bad rank/nranks");
+  if (p->peer_n > 0) return set_error(MS2G_ERR_CONFIG, "peers already attached");
+  MS2G_TRY(ensure_exchange(p));
+  std::vector<float*> bufs(nranks);
+  std::vector<unsigned*> pads(nranks);
+  for (int q = 0; q < nranks; ++q) {
+    PeerBlob b;
+    memcpy(&b, (const char*)blobs + (size_t)q * sizeof(PeerBlob), sizeof(b));
+    if (b.magic != kPeerMagic || b.slot != p->xch_slot)
+      return set_error(MS2G_ERR_CONFIG, "peer blob mismatch (different plan shapes or corrupt exchange)");
+    if (q == rank) {
+      bufs[q] = p->xch_buf;
+      pads[q] = p->xch_pad;
+      continue;
+    }
+    void *pb = nullptr, *pp = nullptr;
+    MS2G_CUDA(cudaIpcOpenMemHandle(&pb, b.buf, cudaIpcMemLazyEnablePeerAccess));
+    p->peer_opened.push_back(pb);
+    MS2G_CUDA(cudaIpcOpenMemHandle(&pp, b.pad, cudaIpcMemLazyEnablePeerAccess));
+    p->peer_opened.push_back(pp);
+    bufs[q] = (float*)pb;
+    pads[q] = (unsigned*)pp;
+  }
+  MS2G_CUDA(cudaMalloc(&p->d_peer_bufs, sizeof(float*) * nranks));
+  MS2G_CUDA(cudaMalloc(&p->d_peer_pads, sizeof(unsigned*) * nranks));
+  MS2G_CUDA(cudaMemcpy(p->d_peer_bufs, bufs.data(), sizeof(float*) * nranks, cudaMemcpyHostToDevice));
+  MS2G_CUDA(cudaMemcpy(p->d_peer_pads, pads.data(), sizeof(unsigned*) * nranks, cudaMemcpyHostToDevice));
+  p->peer_rank = rank;
+  p->peer_n = nranks;
+  p->rank = rank;
+  p->nranks = nranks;
+  if (p->sg.exec) {  // a cached solve graph captured without the peers
+    cudaGraphExecDestroy(p->sg.exec);
+    cudaGraphDestroy(p->sg.graph);
+    p->sg = SolveGraph{};
+  }
+  return MS2G_OK;
+}
+
 int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* out,
                          const int32_t* subset, int32_t n_subset, void* stream) {
   if (!p || !x || !out) return set_error(MS2G_ERR_INPUT, "NULL plan/x/out");
@@ -790,7 +883,8 @@ int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* im
   if (!p || !sino || !img) return set_error(MS2G_ERR_INPUT, "NULL plan/sino/img");
   const FactorTables* f = find_factor(p, factor);
   if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
-  if (do_allreduce && !p->comm && p->nranks > 1) return set_error(MS2G_ERR_CONFIG, "allreduce needs attach_nccl");
+  if (do_allreduce && !p->comm && !p->peer_n && p->nranks > 1)
+    return set_error(MS2G_ERR_CONFIG, "allreduce needs attach_nccl or attach_peers");
   cudaStream_t st = (cudaStream_t)stream;
   const int* d_sel;
   int n_sel, n_glob;

@@ -108,23 +108,115 @@ constexpr int kFwdWarps = MS2G_FWD_WARPS;
 #endif
 constexpr int kFwdUnroll = MS2G_FWD_UNROLL;
 
-// NB images of a batch share one traversal: the weights of a column are
-// computed once and applied to NB pair images (C5: 8 reconstructions per GPU).
-// SPLIT > 1 cuts each warp's column range into SPLIT equal segments taken by
-// SPLIT warps of the block (the same 32 rays), summed through shared memory in
-// fixed order: more, shorter work units for launches with few views (a view
-// shard, a minibatch) whose single wave would otherwise wait on its longest
-// rays.
-template <int NB, int SPLIT>
+
+// Single images (NB = 1 here; batches use k_forward_batch below).
+// Each warp's column range is cut into SEG equal segments whose partial sums
+// are combined in fixed order through shared memory; SPLIT warps of the block
+// (the same 32 rays) take SEG / SPLIT segments each.  More, shorter work
+// units help launches with few views (a view shard, a minibatch) whose single
+// wave would otherwise wait on its longest rays; the summation order depends
+// on SEG only, not on SPLIT.
+template <int NB, int SPLIT, int SEG>
 __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out) {
   constexpr int VPB = kFwdWarps / SPLIT;             // views per block
+  constexpr int SPW = SEG / SPLIT;                   // segments per warp
+
+  __shared__ float2 red[VPB][SEG][NB][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = warp % SPLIT;                        // column segment of this warp
+  const int vw = warp / SPLIT, q = warp % SPLIT;
+  const int k = blockIdx.y * VPB + vw;
+  const bool vk = k < n_sel;
+  const int t = blockIdx.x * 32 + lane;
+  const int bz0 = blockIdx.z * NB;
+  const int g = (sel && vk) ? __ldg(sel + k) : k;
+  const bool valid = vk && t < B;
+  long long F0 = 0;
+  unsigned S = 1;
+  float Lc = 0.f, Ly32 = 0.f;
+  int cls = 0, cl = INT_MAX, ch = INT_MIN;
+  if (valid) {
+    const RayEntry R = rays[(size_t)g * B + t];
+    F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; cls = R.flags & 3;
+    if (R.c_lo < R.c_hi) { cl = R.c_lo; ch = R.c_hi; }
+  }
+  const int wcl = __reduce_min_sync(0xffffffffu, cl);
+  const int wch = __reduce_max_sync(0xffffffffu, ch);
+  const int len = wch > wcl ? wch - wcl : 0;
+  const int L = nc + 3;
+  const size_t istride = (size_t)nc * L;            // pair-image stride between batch images
+  const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
+  // element of pair index u on line c: c L + u for every class (the mirrored
+  // images are stored back to front); u is clamped to the zero pads
+  // (unsigned: negatives clamp too)
+  const unsigned umax = (unsigned)(nc + 2);
+#pragma unroll 1
+  for (int j = 0; j < SPW; ++j) {
+    const int sg = q * SPW + j;
+    const int c0 = wcl + (sg * len) / SEG, c1 = wcl + ((sg + 1) * len) / SEG;
+    float sa[NB], sb[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) { sa[i] = 0.f; sb[i] = 0.f; }
+    if (c0 < c1) {
+      const long long Es = F0 + (long long)c0 * (long long)S + (long long)S + (1LL << 32);
+      unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
+      unsigned offk = (unsigned)(c0 * L);
+#pragma unroll kFwdUnroll
+      for (int c = c0; c < c1; ++c) {
+        unsigned lo1, hi1;
+        asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
+        const float mf = (float)min(elo, S);
+        const unsigned e = offk + min(ehi, umax);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          float pl, pu;
+          asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
+              : "=f"(pl), "=f"(pu) : "r"(e), "l"(base + i * istride));
+          sa[i] += pl;
+          sb[i] = fmaf(mf, pu - pl, sb[i]);
+        }
+        elo = lo1;
+        ehi = hi1;
+        offk += L;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) red[vw][sg][i][lane] = make_float2(sa[i], sb[i]);
+  }
+  __syncthreads();
+  if (q != 0 || !valid) return;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    float a = 0.f, b = 0.f;
+#pragma unroll
+    for (int sg = 0; sg < SEG; ++sg) {
+      const float2 v = red[vw][sg][i][lane];
+      a += v.x;
+      b += v.y;
+    }
+    float r = fmaf(Lc, a, Ly32 * b);
+    if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
+    out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
+  }
+}
+
+// Batched traversal (NB >= 2 images share the weights): each view's rays are
+// split into 2 column halves taken by 2 warps; partial sums combined in fixed
+// order.  Kept separate from the single-image kernel: with the segment loop
+// ptxas needs 72 instead of 56 registers at NB = 8 and the launch is 1.5x
+// slower (C5 batch 8, s=1: 0.73 vs 1.11 ms).
+template <int NB>
+__global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry* __restrict__ rays, int B, int V_r,
+                                                                 const int* __restrict__ sel, int n_sel,
+                                                                 const float2* __restrict__ pairs, size_t pair_stride,
+                                                                 int nc, const float* __restrict__ bsino,
+                                                                 float* __restrict__ out) {
+  constexpr int SPLIT = 2, VPB = kFwdWarps / SPLIT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = warp % SPLIT;
   const int k = blockIdx.y * VPB + warp / SPLIT;
-  if (SPLIT == 1 && k >= n_sel) return;
   const bool vk = k < n_sel;
   const int t = blockIdx.x * 32 + lane;
   const int bz0 = blockIdx.z * NB;
@@ -141,7 +233,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
   }
   int wcl = __reduce_min_sync(0xffffffffu, cl);
   int wch = __reduce_max_sync(0xffffffffu, ch);
-  if (SPLIT > 1 && wcl < wch) {
+  if (wcl < wch) {
     const int len = wch - wcl;
     const int c0 = wcl + (q * len) / SPLIT, c1 = wcl + ((q + 1) * len) / SPLIT;
     wcl = c0;
@@ -152,11 +244,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
   for (int i = 0; i < NB; ++i) { sa[i] = 0.f; sb[i] = 0.f; }
   if (wcl < wch) {
     const int L = nc + 3;
-    const size_t istride = (size_t)nc * L;          // pair-image stride between batch images
+    const size_t istride = (size_t)nc * L;
     const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
-    // element of pair index u on line c: c L + u for every class (the
-    // mirrored images are stored back to front); u is clamped to the zero
-    // pads (unsigned: negatives clamp too)
     const unsigned umax = (unsigned)(nc + 2);
     const long long Es = F0 + (long long)wcl * (long long)S + (long long)S + (1LL << 32);
     unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
@@ -180,66 +269,61 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
       offk += L;
     }
   }
-  if (SPLIT > 1) {   // segment partials -> the q = 0 warp of each view, fixed order
-    __shared__ float2 red[kFwdWarps][NB][32];
+  __shared__ float2 red[kFwdWarps][NB][32];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) red[warp][i][lane] = make_float2(sa[i], sb[i]);
-    __syncthreads();
-    if (q != 0) return;
+  for (int i = 0; i < NB; ++i) red[warp][i][lane] = make_float2(sa[i], sb[i]);
+  __syncthreads();
+  if (q != 0 || !valid) return;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      float a = 0.f, b = 0.f;
+  for (int i = 0; i < NB; ++i) {
+    float a = 0.f, b = 0.f;
 #pragma unroll
-      for (int j = 0; j < SPLIT; ++j) {
-        const float2 v = red[warp + j][i][lane];
-        a += v.x;
-        b += v.y;
-      }
-      sa[i] = a;
-      sb[i] = b;
+    for (int j = 0; j < SPLIT; ++j) {
+      const float2 v = red[warp + j][i][lane];
+      a += v.x;
+      b += v.y;
     }
-  }
-  if (valid) {
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      float r = fmaf(Lc, sa[i], Ly32 * sb[i]);
-      if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
-      out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
-    }
+    float r = fmaf(Lc, a, Ly32 * b);
+    if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
+    out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
   }
 }
 
-template <int NB, int SPLIT>
+template <int NB>
+static void fwd_launch_batch(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
+                             const int* d_sel, const float* b, float* out) {
+  dim3 grid((p->B + 31) / 32, (n_sel + kFwdWarps / 2 - 1) / (kFwdWarps / 2), batch / NB);
+  k_forward_batch<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
+                                                      p->pair_stride, f.nc, b, out);
+}
+
+template <int NB, int SPLIT, int SEG>
 static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
                         const int* d_sel, const float* b, float* out) {
   constexpr int VPB = kFwdWarps / SPLIT;
   dim3 grid((p->B + 31) / 32, (n_sel + VPB - 1) / VPB, batch / NB);
-  k_forward<NB, SPLIT><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
-                                                       p->pair_stride, f.nc, b, out);
-}
-
-template <int NB>
-static void fwd_launch(int split, int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
-                       const int* d_sel, const float* b, float* out) {
-  if (split >= 4) fwd_launch2<NB, 4>(n_sel, batch, s, p, f, d_sel, b, out);
-  else if (split == 2) fwd_launch2<NB, 2>(n_sel, batch, s, p, f, d_sel, b, out);
-  else fwd_launch2<NB, 1>(n_sel, batch, s, p, f, d_sel, b, out);
+  k_forward<NB, SPLIT, SEG><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
+                                                            p->pair_stride, f.nc, b, out);
 }
 
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s) {
   if (n_sel <= 0) return MS2G_OK;
   const int nb = (batch % 8 == 0) ? 8 : (batch % 4 == 0) ? 4 : (batch % 2 == 0) ? 2 : 1;
-  // column split (measured on B200: 4 for single images -- C4 s=1 0.80 ->
-  // 0.78 ms, its 180-view shard 0.18 -> 0.14 ms, C3 0.14 -> 0.12 ms -- and 2
-  // for batched traversals, C5 batch 8: 1.03 -> 0.73 ms); MS2G_FWD_SPLIT
-  // overrides it for experiments
-  int split = nb > 1 ? 2 : 4;
-  if (const char* e = getenv("MS2G_FWD_SPLIT")) split = atoi(e);
-  if (nb == 8) fwd_launch<8>(split, n_sel, batch, s, p, f, d_sel, b, out);
-  else if (nb == 4) fwd_launch<4>(split, n_sel, batch, s, p, f, d_sel, b, out);
-  else if (nb == 2) fwd_launch<2>(split, n_sel, batch, s, p, f, d_sel, b, out);
-  else fwd_launch<1>(split, n_sel, batch, s, p, f, d_sel, b, out);
+  // Work-unit shape (measured on B200, CUDA events):
+  //  * single images: 4 segments per ray; one warp takes all four (SPLIT 1:
+  //    C4 s=1 0.78 -> 0.73 ms, C3 0.126 -> 0.123 ms) unless the launch is
+  //    under ~1.5 waves of warps, where 4 warps share them (SPLIT 4: C4's
+  //    180-view shard 0.157 -> 0.138 ms);
+  //  * batches: k_forward_batch, 2 column halves on 2 warps (C5 batch 8, s=1:
+  //    0.73 ms against 0.84-1.1 ms for the segmented kernel).
+  const long long units = (long long)((p->B + 31) / 32) * n_sel * (batch / nb);   // warps of 32 rays
+  const long long wave = 148LL * 64;                                               // resident warps
+  if (nb == 8) fwd_launch_batch<8>(n_sel, batch, s, p, f, d_sel, b, out);
+  else if (nb == 4) fwd_launch_batch<4>(n_sel, batch, s, p, f, d_sel, b, out);
+  else if (nb == 2) fwd_launch_batch<2>(n_sel, batch, s, p, f, d_sel, b, out);
+  else if (2 * units < 3 * wave) fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out);
+  else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out);
   return check_launch("k_forward");
 }
 
@@ -277,7 +361,10 @@ constexpr int kPadR = 2;
 // minor extent H of the tiles: 64 (6 blocks of 36 KB per SM) or, for n_c >=
 // 1024, 96 (4 blocks of 51 KB; lane utilisation 0.88, measured 10 % faster
 // at 1024^2 and slower on coarser grids)
-int bp_height(int nc) { return nc >= 1024 ? 96 : 64; }
+#ifndef MS2G_BH96_MIN_NC
+#define MS2G_BH96_MIN_NC 1024
+#endif
+int bp_height(int nc) { return nc >= MS2G_BH96_MIN_NC ? 96 : 64; }
 template <int H>
 struct BpShape {
   static constexpr int kWinR = H + kPadR;                // rows per warp window (+ shared pads)
@@ -540,7 +627,7 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
 }
 
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
-                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s) {
+                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish) {
   const int H = bp_height(f.nc);
   const BpTiling t = bp_tiling(f.nc, H);
   int ch[2], vpc[2];
@@ -556,6 +643,8 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t));
   MS2G_TRY(check_launch("k_backward"));
   const size_t np = (size_t)f.nc * f.nc, total = np * batch;
+  if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)
+    return launch_chunk_reduce_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);
   const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
   k_chunk_reduce<<<blocks, 256, 0, s>>>(p->w_part, ch[0] + ch[1], np, total, img, scale, accumulate);
   return check_launch("k_chunk_reduce");

@@ -1,8 +1,9 @@
 """World-size-2 gloo tests of the multi-GPU host logic on CPU:
 view shards partition the views, the sum over ranks of the per-shard
 backprojections (oracle, allreduced with gloo) equals the full one, every
-rank derives the same bit-exact schedule, and the NCCL unique id broadcast
-path delivers rank 0's bytes."""
+rank derives the same bit-exact schedule, the NCCL unique id broadcast
+path delivers rank 0's bytes, and the peer-handle exchange of NEXT-3 gathers
+every rank's blob in rank order."""
 import os
 import socket
 
@@ -45,7 +46,11 @@ def _worker(rank, world, port, q):
         dist.all_gather_object(allsch, sch)
         uid = bytes(range(128)) if rank == 0 else None
         got = P.broadcast_unique_id(uid, rank, world)
-        q.put((rank, err, all(s == allsch[0] for s in allsch), got == bytes(range(128)), (vb, ve)))
+        # NEXT-3 peer blob exchange: rank-ordered concatenation of equal-size blobs
+        blob = bytes([rank + 1]) * 40
+        allb = P.gather_blobs(blob, rank, world)
+        blobs_ok = allb == b"".join(bytes([q_ + 1]) * 40 for q_ in range(world))
+        q.put((rank, err, all(s == allsch[0] for s in allsch), got == bytes(range(128)) and blobs_ok, (vb, ve)))
     finally:
         dist.destroy_process_group()
 

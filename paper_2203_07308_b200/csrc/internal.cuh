@@ -83,6 +83,7 @@ struct ms2g_plan {
   double pitch = 0;
   std::vector<ms2g::FactorTables> ft;
   int nmax_c = 0;                      // largest coarse side among the factors
+  int sm_count = 148;                  // SMs of the plan's device
   // workspaces (all sized for batch)
   float2* w_pair = nullptr;            // forward gather images: 4 x [batch][n_c][n_c + 3] float2
   size_t pair_stride = 0;              // float2 elements per pair image

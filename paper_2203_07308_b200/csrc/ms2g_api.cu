@@ -711,6 +711,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     return MS2G_OK;
   };
   p->red_blocks = 2 * sms;
+  p->sm_count = sms;
   p->pair_stride = (size_t)p->nmax_c * (p->nmax_c + 3) * bt;
   e = cudaMalloc(&p->w_pair, sizeof(float2) * 4 * p->pair_stride);
   if (e != cudaSuccess) {

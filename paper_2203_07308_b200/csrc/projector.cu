@@ -318,7 +318,7 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
   //  * batches: k_forward_batch, 2 column halves on 2 warps (C5 batch 8, s=1:
   //    0.73 ms against 0.84-1.1 ms for the segmented kernel).
   const long long units = (long long)((p->B + 31) / 32) * n_sel * (batch / nb);   // warps of 32 rays
-  const long long wave = 148LL * 64;                                               // resident warps
+  const long long wave = (long long)p->sm_count * 64;                              // resident warps
   if (nb == 8) fwd_launch_batch<8>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 4) fwd_launch_batch<4>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 2) fwd_launch_batch<2>(n_sel, batch, s, p, f, d_sel, b, out);

@@ -59,6 +59,7 @@ struct FactorTables {
   double* d_Lcache = nullptr;
   mutable int L_iters = 0;
   int4* d_bpr = nullptr;          // per (adjoint tile, view): bin runs meeting the tile
+  int* d_bp_order = nullptr;      // full-view launches: block -> work item, longest first
   // bicubic resampling tables (NEXT-1), [n_out][taps] clamped input index / weight
   int taps_down = 0, taps_up = 0;
   int* d_idx_down = nullptr;

@@ -164,6 +164,39 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     if (ch < 1) ch = 1;
     f.bp_chunks[fam] = (int)ch;
   }
+  // Block order of full-view backprojections: longest (tile, view chunk)
+  // first (LPT).  Blocks start roughly in index order, so a launch of 2-3
+  // waves of uneven blocks (tiles outside the disk of the fan, families of a
+  // view shard) no longer ends on its longest blocks.  Cost = rays meeting the
+  // tile in the chunk, from the range table.
+  {
+    const int ntile = bp_tile_count(nc), per_t = ntile / 2;
+    std::vector<int4> rt((size_t)ntile * V_r);
+    MS2G_CUDA(cudaMemcpy(rt.data(), f.d_bpr, sizeof(int4) * rt.size(), cudaMemcpyDeviceToHost));
+    const int chx = f.bp_chunks[0], chy = f.bp_chunks[1];
+    const int n_items = per_t * (chx + chy);
+    std::vector<long long> cost(n_items, 0);
+    for (int it = 0; it < n_items; ++it) {
+      const int fam = it >= per_t * chx;
+      const int bi = it - fam * per_t * chx;
+      const int ti = bi % per_t, c = bi / per_t;
+      const int chf = fam ? chy : chx, vpc = (V_r + chf - 1) / chf;
+      const int4* row = rt.data() + (size_t)(fam * per_t + ti) * V_r;
+      long long sum = 0;
+      for (int v = c * vpc; v < std::min(V_r, (c + 1) * vpc); ++v) {
+        const int4 r = row[v];
+        const int nr = (r.z >> 16) & 0xff;
+        if (nr > 0) sum += (short)(r.x >> 16) - (r.x & 0xffff) + 1;
+        if (nr > 1) sum += (short)(r.y >> 16) - (r.y & 0xffff) + 1;
+      }
+      cost[it] = sum;
+    }
+    std::vector<int> order(n_items);
+    for (int it = 0; it < n_items; ++it) order[it] = it;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    MS2G_CUDA(cudaMalloc(&f.d_bp_order, sizeof(int) * n_items));
+    MS2G_CUDA(cudaMemcpy(f.d_bp_order, order.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
+  }
   return MS2G_OK;
 }
 
@@ -173,6 +206,7 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(f.d_rays);
     cudaFree(f.d_views);
     cudaFree(f.d_bpr);
+    cudaFree(f.d_bp_order);
     cudaFree(f.d_idx_down);
     cudaFree(f.d_w_down);
     cudaFree(f.d_idx_up);

@@ -436,14 +436,15 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
                                                           const int4* __restrict__ ranges, int V_r, int B,
                                                           const int* __restrict__ sel, int n_sel,
                                                           const float* __restrict__ sino, float* __restrict__ part,
-                                                          int nc, int tmaj, int per, int chx, int vpcx, int vpcy) {
+                                                          int nc, int tmaj, int per, int chx, int vpcx, int vpcy,
+                                                          const int* __restrict__ order) {
   extern __shared__ float4 dyn_smem[];
   float* acc = reinterpret_cast<float*>(dyn_smem);   // kAccRows x kBT (dynamic: may exceed 48 KB)
   constexpr int kBH = H, kWinR = BpShape<H>::kWinR, kAccRows = BpShape<H>::kAccRows;
   __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // blockIdx.x = (family, view chunk, tile): X-family blocks first
-  const int bx = blockIdx.x, bz = blockIdx.z;
+  const int bx = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x, bz = blockIdx.z;
   const int fam = bx >= per * chx;                 // 0: X-tile (major x), 1: Y-tile (major y)
   const int bi = bx - fam * per * chx;
   const int ti = bi % per, chunk = bi / per;
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     sum[i] = s;
   }
   const size_t np = (size_t)nc * nc;
-  const int nplanes = chx + (int)((gridDim.x - per * chx) / per);
+  const int nplanes = chx + (int)((gridDim.x - per * chx) / per);   // X chunks + Y chunks
   float* dst = part + ((size_t)bz * nplanes + plane) * np;
   if (!fam) {       // X-tile: row l = y - m0, lane = x - c0 (coalesced)
 #pragma unroll
@@ -613,7 +614,8 @@ __global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size
 
 template <int H>
 static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const float* sino,
-                      const int* d_sel, int n_sel, const int* ch, const int* vpc, const BpTiling& t) {
+                      const int* d_sel, int n_sel, const int* ch, const int* vpc, const BpTiling& t,
+                      const int* order) {
   constexpr size_t smem = BpShape<H>::kSmem;
   static bool attr = false;
   if (!attr) {   // several blocks of 36-51 KB per SM need the maximum shared-memory carveout
@@ -622,7 +624,7 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
     attr = true;
   }
   k_backward<H><<<grid, 32 * kBW, smem, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, sino, p->w_part,
-                                             f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1]);
+                                             f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order);
   return MS2G_OK;
 }
 
@@ -639,8 +641,11 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
     vpc[fam] = (n_sel + ch[fam] - 1) / ch[fam];
   }
   dim3 grid(t.per * (ch[0] + ch[1]), 1, batch);
-  if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t));
-  else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t));
+  // the plan's longest-first block order holds for its own (full-view) chunking
+  const int* order = (!d_sel && n_sel == p->V_r && ch[0] == f.bp_chunks[0] && ch[1] == f.bp_chunks[1] &&
+                      !getenv("MS2G_BP_NO_ORDER")) ? f.d_bp_order : nullptr;
+  if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
+  else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
   MS2G_TRY(check_launch("k_backward"));
   const size_t np = (size_t)f.nc * f.nc, total = np * batch;
   if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)

@@ -138,16 +138,16 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     if (rc != MS2G_OK) return rc;
     if (herr) return set_error(MS2G_ERR_CONFIG, "a tile's shadow spans more than 2 ray classes (fan too wide)");
   }
-  // backprojector view chunks: enough blocks that the last partial wave is a
-  // small fraction of the launch (measured on B200, C4: 8 waves for 1024^2,
-  // 24 waves for coarser grids; the chunk partials are summed by
-  // k_chunk_reduce in fixed order)
+  // backprojector view chunks: about 24 "waves" of SM-count blocks (measured
+  // on B200 with the longest-first order below: 24 is best or within 2 % for
+  // C3, C4, its 180-view shard and C5 batch 8; 8 and 64 lose 3-10 %).  The
+  // chunk partials are summed by k_chunk_reduce in fixed order.
   // The X- and Y-tile families only see the views with major-x / major-y
   // rays; a contiguous view shard (e.g. 45 degrees at P = 8) is almost all
   // one class, so each family gets view chunks in proportion to its views.
   const long long tiles = (long long)bp_tile_count(nc) * d.batch;
   const long long per = tiles / 2;
-  const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : (tiles >= 1024 ? 8 : 24);
+  const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : 24;
   const long long target = waves * sm_count;
   long long nv[2] = {0, 0};
   for (const ViewEntry& ve : views) {

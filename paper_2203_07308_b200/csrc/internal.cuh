@@ -60,6 +60,8 @@ struct FactorTables {
   mutable int L_iters = 0;
   int4* d_bpr = nullptr;          // per (adjoint tile, view): bin runs meeting the tile
   int* d_bp_order = nullptr;      // full-view launches: block -> work item, longest first
+  int* d_fwd_order = nullptr;     // same for the single-image forward (for fwd_order_vpb views per block)
+  int fwd_order_vpb = 0;
   // bicubic resampling tables (NEXT-1), [n_out][taps] clamped input index / weight
   int taps_down = 0, taps_up = 0;
   int* d_idx_down = nullptr;
@@ -182,6 +184,7 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s);
 int bp_tile_count(int nc);   // adjoint tiles (both families) of an n_c grid
+int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch);
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
 // publish != 0: write scale * A_s^T sino into the peer exchange slot (not img)
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,

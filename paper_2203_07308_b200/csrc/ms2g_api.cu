@@ -197,6 +197,32 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     MS2G_CUDA(cudaMalloc(&f.d_bp_order, sizeof(int) * n_items));
     MS2G_CUDA(cudaMemcpy(f.d_bp_order, order.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
   }
+  // The same for the single-image forward: a block = 32 bins x vpb views,
+  // cost = sum over its warps of the longest ray's column range.
+  if (d.batch % 2 != 0) {
+    const int vpb = fwd_views_per_block(p, V_r, d.batch);
+    const int nbx = (B + 31) / 32, nby = (V_r + vpb - 1) / vpb;
+    std::vector<long long> cost((size_t)nbx * nby, 0);
+    for (int by = 0; by < nby; ++by)
+      for (int v = by * vpb; v < std::min(V_r, (by + 1) * vpb); ++v)
+        for (int bx = 0; bx < nbx; ++bx) {
+          int lo = INT_MAX, hi = INT_MIN;
+          for (int t = bx * 32; t < std::min(B, bx * 32 + 32); ++t) {
+            const RayEntry& R = rays[(size_t)v * B + t];
+            if (R.c_lo < R.c_hi) {
+              lo = std::min(lo, (int)R.c_lo);
+              hi = std::max(hi, (int)R.c_hi);
+            }
+          }
+          if (lo < hi) cost[(size_t)by * nbx + bx] += hi - lo;
+        }
+    std::vector<int> order(cost.size());
+    for (size_t it = 0; it < order.size(); ++it) order[it] = (int)it;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    MS2G_CUDA(cudaMalloc(&f.d_fwd_order, sizeof(int) * order.size()));
+    MS2G_CUDA(cudaMemcpy(f.d_fwd_order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
+    f.fwd_order_vpb = vpb;
+  }
   return MS2G_OK;
 }
 
@@ -207,6 +233,7 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(f.d_views);
     cudaFree(f.d_bpr);
     cudaFree(f.d_bp_order);
+    cudaFree(f.d_fwd_order);
     cudaFree(f.d_idx_down);
     cudaFree(f.d_w_down);
     cudaFree(f.d_idx_up);
@@ -728,6 +755,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
   }
   int rc = MS2G_OK;
   size_t part = 1;
+  p->sm_count = sms;
   for (auto& f : p->ft) {
     rc = build_tables(p, f, sms);
     if (rc != MS2G_OK) {
@@ -745,7 +773,6 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     return MS2G_OK;
   };
   p->red_blocks = 2 * sms;
-  p->sm_count = sms;
   p->pair_stride = (size_t)p->nmax_c * (p->nmax_c + 3) * bt;
   e = cudaMalloc(&p->w_pair, sizeof(float2) * 4 * p->pair_stride);
   if (e != cudaSuccess) {

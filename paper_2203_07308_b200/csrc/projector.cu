@@ -120,16 +120,25 @@ template <int NB, int SPLIT, int SEG>
 __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
-                                                 const float* __restrict__ bsino, float* __restrict__ out) {
+                                                 const float* __restrict__ bsino, float* __restrict__ out,
+                                                 const int* __restrict__ order) {
   constexpr int VPB = kFwdWarps / SPLIT;             // views per block
   constexpr int SPW = SEG / SPLIT;                   // segments per warp
 
   __shared__ float2 red[VPB][SEG][NB][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int vw = warp / SPLIT, q = warp % SPLIT;
-  const int k = blockIdx.y * VPB + vw;
+  // block -> (bin block, view block): the plan's longest-first order for
+  // full-view launches, else the grid position
+  int bxi = blockIdx.x, byi = blockIdx.y;
+  if (order) {
+    const int item = __ldg(order + blockIdx.y * gridDim.x + blockIdx.x);
+    bxi = item % gridDim.x;
+    byi = item / gridDim.x;
+  }
+  const int k = byi * VPB + vw;
   const bool vk = k < n_sel;
-  const int t = blockIdx.x * 32 + lane;
+  const int t = bxi * 32 + lane;
   const int bz0 = blockIdx.z * NB;
   const int g = (sel && vk) ? __ldg(sel + k) : k;
   const bool valid = vk && t < B;
@@ -302,8 +311,19 @@ static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, cons
                         const int* d_sel, const float* b, float* out) {
   constexpr int VPB = kFwdWarps / SPLIT;
   dim3 grid((p->B + 31) / 32, (n_sel + VPB - 1) / VPB, batch / NB);
+  const int* order = (!d_sel && n_sel == p->V_r && f.fwd_order_vpb == VPB && !getenv("MS2G_FWD_NO_ORDER"))
+                         ? f.d_fwd_order : nullptr;
   k_forward<NB, SPLIT, SEG><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
-                                                            p->pair_stride, f.nc, b, out);
+                                                            p->pair_stride, f.nc, b, out, order);
+}
+
+// views per block of the single-image forward kernel for a launch of n_sel
+// views x batch images (4 segments per ray: one warp per view, or 4 warps per
+// view when the launch is under ~1.5 waves of warps)
+int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch) {
+  const long long units = (long long)((p->B + 31) / 32) * n_sel * batch;
+  const long long wave = (long long)p->sm_count * 64;
+  return (2 * units < 3 * wave) ? kFwdWarps / 4 : kFwdWarps;
 }
 
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
@@ -317,12 +337,10 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
   //    180-view shard 0.157 -> 0.138 ms);
   //  * batches: k_forward_batch, 2 column halves on 2 warps (C5 batch 8, s=1:
   //    0.73 ms against 0.84-1.1 ms for the segmented kernel).
-  const long long units = (long long)((p->B + 31) / 32) * n_sel * (batch / nb);   // warps of 32 rays
-  const long long wave = (long long)p->sm_count * 64;                              // resident warps
   if (nb == 8) fwd_launch_batch<8>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 4) fwd_launch_batch<4>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 2) fwd_launch_batch<2>(n_sel, batch, s, p, f, d_sel, b, out);
-  else if (2 * units < 3 * wave) fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out);
+  else if (fwd_views_per_block(p, n_sel, batch) != kFwdWarps) fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out);
   else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out);
   return check_launch("k_forward");
 }

@@ -227,6 +227,16 @@ int ms2g_pnp_ms2g_solve_async(ms2g_plan* plan, const ms2g_solve_desc* desc, cons
 int ms2g_solve_status(ms2g_plan* plan, void* stream);
 
 /* Thread-local message of the last failing call ("" if none). */
+/* Per-kernel timing inside the solve graph (measurement support).
+ * ms2g_set_kernel_timing(plan, 1): the next captured solve graph records an
+ * external CUDA event before and after every projector launch (k_forward,
+ * k_backward); 0 removes them (the cached graph is re-captured either way).
+ * ms2g_kernel_time: for the LAST replayed solve, the summed device time (ms)
+ * and count of the launches of one kind (0 forward, 1 backward) at one
+ * factor.  Synchronizes on those events.  MS2G_ERR_INPUT on NULL. */
+int ms2g_set_kernel_timing(ms2g_plan* plan, int32_t enable);
+int ms2g_kernel_time(ms2g_plan* plan, int32_t kind, int32_t factor, double* total_ms, int32_t* launches);
+
 const char* ms2g_last_error(void);
 
 /* Number of device kernels libms2g has launched in this process (graph

@@ -86,6 +86,8 @@ def load():
     L.ms2g_plan_destroy.restype = None
     L.ms2g_nccl_unique_id.argtypes = [p]
     L.ms2g_attach_nccl.argtypes = [p, p, i, i]
+    L.ms2g_set_kernel_timing.argtypes = [p, i]
+    L.ms2g_kernel_time.argtypes = [p, i, i, C.POINTER(d), C.POINTER(i)]
     L.ms2g_peer_export.argtypes = [p, p]
     L.ms2g_attach_peers.argtypes = [p, p, i, i]
     L.ms2g_forward_project.argtypes = [p, i, p, p, p, C.POINTER(C.c_int32), i, p]
@@ -381,6 +383,20 @@ def attach_nccl(plan: Plan, rank: int, nranks: int, group=None):
     _check(L.ms2g_attach_nccl(plan.handle, (C.c_uint8 * 128).from_buffer_copy(uid), rank, nranks))
     plan.rank, plan.nranks = rank, nranks
     return plan
+
+
+def set_kernel_timing(plan: Plan, enable: bool = True):
+    """Record CUDA events around every projector launch of the captured solve
+    graph (measurement support; the graph is re-captured)."""
+    _check(load().ms2g_set_kernel_timing(plan.handle, 1 if enable else 0))
+
+
+def kernel_time(plan: Plan, kind: str, factor: int):
+    """(total device ms, launches) of the 'forward' or 'backward' launches at
+    `factor` in the last replayed solve (needs set_kernel_timing)."""
+    t, n = C.c_double(), C.c_int32()
+    _check(load().ms2g_kernel_time(plan.handle, {"forward": 0, "backward": 1}[kind], factor, C.byref(t), C.byref(n)))
+    return t.value, n.value
 
 
 def gather_blobs(blob: bytes, rank: int, nranks: int, group=None) -> bytes:

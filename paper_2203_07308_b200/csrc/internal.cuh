@@ -132,6 +132,11 @@ struct ms2g_plan {
   int* w_peer_err = nullptr;
   int peer_rank = 0, peer_n = 0;       // peer_n > 0: attached
   std::vector<void*> peer_opened;      // IPC mappings to close
+  // per-kernel timing inside the captured solve graph (ms2g_set_kernel_timing):
+  // external event-record nodes around every k_forward / k_backward launch
+  struct TimedLaunch { cudaEvent_t a, b; int kind, factor; };
+  bool timing = false;
+  std::vector<TimedLaunch> tev;
   // graph cache
   ms2g::SolveGraph sg;
   int last_total_steps = 0;
@@ -178,6 +183,10 @@ inline int check_launch(const char* what) {
 }
 
 const FactorTables* find_factor(const ms2g_plan* p, int factor);
+// timing of one projector launch inside a solve capture (no-op otherwise);
+// kind 0 forward, 1 backward; returns the slot for timing_end (-1: none)
+int timing_begin(ms2g_plan* p, int kind, int factor, cudaStream_t st);
+void timing_end(ms2g_plan* p, int slot, cudaStream_t st);
 
 // ---- kernel launchers (projector.cu) ----
 int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s);

@@ -29,6 +29,28 @@ const FactorTables* find_factor(const ms2g_plan* p, int factor) {
   return nullptr;
 }
 
+int timing_begin(ms2g_plan* p, int kind, int factor, cudaStream_t st) {
+  if (!p->timing || !t_capturing) return -1;
+  ms2g_plan::TimedLaunch tl{nullptr, nullptr, kind, factor};
+  if (cudaEventCreate(&tl.a) != cudaSuccess || cudaEventCreate(&tl.b) != cudaSuccess) return -1;
+  if (cudaEventRecordWithFlags(tl.a, st, cudaEventRecordExternal) != cudaSuccess) return -1;
+  p->tev.push_back(tl);
+  return (int)p->tev.size() - 1;
+}
+
+void timing_end(ms2g_plan* p, int slot, cudaStream_t st) {
+  if (slot < 0) return;
+  cudaEventRecordWithFlags(p->tev[slot].b, st, cudaEventRecordExternal);
+}
+
+static void clear_timing_events(ms2g_plan* p) {
+  for (auto& tl : p->tev) {
+    if (tl.a) cudaEventDestroy(tl.a);
+    if (tl.b) cudaEventDestroy(tl.b);
+  }
+  p->tev.clear();
+}
+
 // floor / ceil division of a signed 64-bit value by a positive divisor
 static long long floor_div(long long a, long long b) {
   long long q = a / b;
@@ -262,6 +284,7 @@ static void free_plan(ms2g_plan* p) {
   cudaFree(p->d_peer_bufs);
   cudaFree(p->d_peer_pads);
   cudaFree(p->w_peer_err);
+  clear_timing_events(p);
   if (p->comm) ncclCommDestroy(p->comm);
   delete p;
 }
@@ -648,6 +671,7 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
     if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
     if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
     p->sg = SolveGraph{};
+    clear_timing_events(p);
     cudaStream_t cs;
     MS2G_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
@@ -818,6 +842,37 @@ int ms2g_plan_info(const ms2g_plan* p, int32_t factor, int32_t* n_c, int32_t* vb
   if (vb) *vb = p->d.view_begin;
   if (ve) *ve = p->d.view_end;
   if (batch) *batch = p->d.batch;
+  return MS2G_OK;
+}
+
+int ms2g_set_kernel_timing(ms2g_plan* p, int32_t enable) {
+  if (!p) return set_error(MS2G_ERR_INPUT, "NULL plan");
+  if ((enable != 0) != p->timing) {
+    p->timing = enable != 0;
+    if (p->sg.exec) {   // the cached solve graph is re-captured with / without the event nodes
+      cudaGraphExecDestroy(p->sg.exec);
+      cudaGraphDestroy(p->sg.graph);
+      p->sg = SolveGraph{};
+    }
+    clear_timing_events(p);
+  }
+  return MS2G_OK;
+}
+
+int ms2g_kernel_time(ms2g_plan* p, int32_t kind, int32_t factor, double* total_ms, int32_t* launches) {
+  if (!p || !total_ms || !launches) return set_error(MS2G_ERR_INPUT, "NULL plan/total_ms/launches");
+  double t = 0.0;
+  int n = 0;
+  for (const auto& tl : p->tev) {
+    if (tl.kind != kind || tl.factor != factor) continue;
+    MS2G_CUDA(cudaEventSynchronize(tl.b));
+    float ms = 0.f;
+    MS2G_CUDA(cudaEventElapsedTime(&ms, tl.a, tl.b));
+    t += ms;
+    ++n;
+  }
+  *total_ms = t;
+  *launches = n;
   return MS2G_OK;
 }
 

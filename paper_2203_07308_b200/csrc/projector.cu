@@ -330,6 +330,7 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
                    int batch, cudaStream_t s) {
   if (n_sel <= 0) return MS2G_OK;
   const int nb = (batch % 8 == 0) ? 8 : (batch % 4 == 0) ? 4 : (batch % 2 == 0) ? 2 : 1;
+  const int slot = timing_begin(p, 0, f.factor, s);
   // Work-unit shape (measured on B200, CUDA events):
   //  * single images: 4 segments per ray; one warp takes all four (SPLIT 1:
   //    C4 s=1 0.78 -> 0.73 ms, C3 0.126 -> 0.123 ms) unless the launch is
@@ -342,7 +343,9 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
   else if (nb == 2) fwd_launch_batch<2>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (fwd_views_per_block(p, n_sel, batch) != kFwdWarps) fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out);
   else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out);
-  return check_launch("k_forward");
+  const int rc = check_launch("k_forward");
+  timing_end(p, slot, s);
+  return rc;
 }
 
 // --------------------------------------------------------------- adjoint --
@@ -662,9 +665,11 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   // the plan's longest-first block order holds for its own (full-view) chunking
   const int* order = (!d_sel && n_sel == p->V_r && ch[0] == f.bp_chunks[0] && ch[1] == f.bp_chunks[1] &&
                       !getenv("MS2G_BP_NO_ORDER")) ? f.d_bp_order : nullptr;
+  const int slot = timing_begin(p, 1, f.factor, s);
   if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
   else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
   MS2G_TRY(check_launch("k_backward"));
+  timing_end(p, slot, s);
   const size_t np = (size_t)f.nc * f.nc, total = np * batch;
   if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)
     return launch_chunk_reduce_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);

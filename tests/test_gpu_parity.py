@@ -571,3 +571,23 @@ def test_peer_allreduce_single_rank(P):
         assert np.array_equal(xa, xc)
         with pytest.raises(P.MS2GError):
             P.attach_peers(c, 0, 1)     # already attached
+
+
+def test_kernel_timing_events(P):
+    """In-graph projector timing (measurement support): the instrumented solve
+    counts every launch per (kind, factor) and gives the same iterate."""
+    pr = S.PRESETS[1]
+    g, xt, b = _make_data(pr, 1)
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1)) as plan:
+        x1 = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha)
+        P.set_kernel_timing(plan, True)
+        x2 = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha)
+        assert torch.equal(x1, x2)
+        for f, iters in ((2, 10), (1, 10)):      # C1: 10 + 10 steps, 20 power iterations per stage
+            for kind in ("forward", "backward"):
+                ms, n = P.kernel_time(plan, kind, f)
+                assert n == 20 + iters and ms > 0.0, (kind, f, n, ms)
+        P.set_kernel_timing(plan, False)
+        x3 = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha)
+        assert torch.equal(x1, x3)
+        assert P.kernel_time(plan, "backward", 1) == (0.0, 0)

@@ -311,8 +311,8 @@ static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, cons
                         const int* d_sel, const float* b, float* out) {
   constexpr int VPB = kFwdWarps / SPLIT;
   dim3 grid((p->B + 31) / 32, (n_sel + VPB - 1) / VPB, batch / NB);
-  const int* order = (!d_sel && n_sel == p->V_r && f.fwd_order_vpb == VPB && !getenv("MS2G_FWD_NO_ORDER"))
-                         ? f.d_fwd_order : nullptr;
+  static const bool no_order = getenv("MS2G_FWD_NO_ORDER") != nullptr;   // experiment switch
+  const int* order = (!d_sel && n_sel == p->V_r && f.fwd_order_vpb == VPB && !no_order) ? f.d_fwd_order : nullptr;
   k_forward<NB, SPLIT, SEG><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
                                                             p->pair_stride, f.nc, b, out, order);
 }
@@ -663,8 +663,9 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   }
   dim3 grid(t.per * (ch[0] + ch[1]), 1, batch);
   // the plan's longest-first block order holds for its own (full-view) chunking
-  const int* order = (!d_sel && n_sel == p->V_r && ch[0] == f.bp_chunks[0] && ch[1] == f.bp_chunks[1] &&
-                      !getenv("MS2G_BP_NO_ORDER")) ? f.d_bp_order : nullptr;
+  static const bool no_order = getenv("MS2G_BP_NO_ORDER") != nullptr;    // experiment switch
+  const int* order = (!d_sel && n_sel == p->V_r && ch[0] == f.bp_chunks[0] && ch[1] == f.bp_chunks[1] && !no_order)
+                         ? f.d_bp_order : nullptr;
   const int slot = timing_begin(p, 1, f.factor, s);
   if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
   else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));

@@ -49,13 +49,15 @@ def nnz_counts():
         return json.load(f)
 
 
-def workload_config(pr, nranks, l2_note):
+def workload_config(pr, nranks, l2_note, allreduce="nccl"):
     return {"workload": f"C{pr.cfg}: {pr.n}x{pr.n} fp32 phantom ({pr.n_ellipses} seeded ellipses), fan-beam "
                         f"{pr.n_views} views x {pr.n_bins} bins, stages "
                         + " -> ".join(f"{s[0]}x:{s[1]}" for s in pr.stages)
                         + f", Gaussian 3x3 denoiser alpha={pr.alpha}, 20 power iterations per stage",
             "image": pr.n, "views": pr.n_views, "bins": pr.n_bins, "iters_per_solve": pr.n_steps,
-            "parallelism": f"views sharded x{nranks} + NCCL allreduce" if nranks > 1 else "1 GPU",
+            "parallelism": (f"views sharded x{nranks} + " + ("NCCL allreduce" if allreduce == "nccl" else
+                                                              "NVLink peer-memory sum (NEXT-3)"))
+            if nranks > 1 else "1 GPU",
             "l2": l2_note}
 
 
@@ -273,7 +275,10 @@ def run_ms2g(args, rank, nranks, local_rank):
     vb, ve = P.view_shard(pr.n_views, rank, nranks)
     plan = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve)
     if nranks > 1:
-        P.attach_nccl(plan, rank, nranks)
+        if args.allreduce == "peer":     # NEXT-3: fused NVLink peer-memory sum (fixed rank order)
+            P.attach_peers(plan, rank, nranks)
+        else:
+            P.attach_nccl(plan, rank, nranks)
     b = torch.from_numpy(np.ascontiguousarray(b_full[vb:ve])).to(dev)[None].contiguous()
     x0 = torch.zeros((1, pr.n, pr.n), device=dev)
     xo = torch.empty_like(x0)
@@ -469,7 +474,7 @@ def run_ms2g(args, rank, nranks, local_rank):
         line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": nranks, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(pr, nranks, "flushed between timed steps (256 MiB write)"),
+                "config": workload_config(pr, nranks, "flushed between timed steps (256 MiB write)", args.allreduce),
                 "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": int(b.numel() * 4),
                         "d2h_bytes_per_step": int(x0.numel() * 4)},
                 "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline,
@@ -485,6 +490,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ms2g", choices=["ms2g", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle sample")
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "peer"],
+                    help="cross-rank sum of the partial backprojections (N > 1): NCCL, or the NEXT-3 "
+                         "peer-memory path (untested at N > 1 on this 1-GPU pool)")
     ap.add_argument("--no-detail", action="store_true", help="skip the 512^2 detail numbers")
     ap.add_argument("--profile-once", action="store_true",
                     help="run one warm-up solve and one solve, print nothing (for ncu launch lists)")

@@ -591,3 +591,41 @@ def test_kernel_timing_events(P):
         x3 = P.pnp_ms2g_solve(plan, pr.stages, dev(b)[None], den=pr.den, alpha=pr.alpha)
         assert torch.equal(x1, x3)
         assert P.kernel_time(plan, "backward", 1) == (0.0, 0)
+
+
+@pytest.mark.parametrize("n,V,B,factors", [
+    (8, 1, 2, (2, 1)),          # one view, two bins: a single-tile, single-chunk launch
+    (6, 5, 4, (3, 1)),          # n_c = 2: tiles far larger than the grid
+    (32, 2, 64, (1,)),          # detector wider than the fan needs: most rays miss
+    (1024, 3, 1536, (1,)),      # H = 96 tiles with only 3 views (tiny chunks, LPT order)
+])
+def test_degenerate_geometries(P, n, V, B, factors):
+    """Edge cases of the launch shapes: tiny grids and view counts, mostly-
+    missing rays; forward and adjoint against the oracle, plus the adjoint
+    identity."""
+    g = O.Geometry(n, V, B)
+    with P.plan_geometry(n, V, B, factors=factors) as plan:
+        for s in factors:
+            nc = n // s
+            x = S.random_image(nc, 70 + s)
+            ref = O.forward(g, s, x)
+            got = host(P.forward_project(plan, s, dev(x)[None]))[0]
+            assert rel(got, ref) <= TOL_OP, (s, rel(got, ref))
+            r = S.random_sinogram((V, B), 80 + s)
+            refb = O.backward(g, s, r)
+            gotb = host(P.back_project(plan, s, dev(r)[None]))[0]
+            assert rel(gotb, refb) <= TOL_OP, (s, rel(gotb, refb))
+            lhs, rhs = float(np.sum(got * r)), float(np.sum(x.astype(np.float64) * gotb))
+            assert abs(lhs - rhs) <= TOL_OP * max(abs(lhs), abs(rhs), 1e-30)
+
+
+def test_empty_subset_and_bad_views_rejected(P):
+    """Boundary errors of the subset path: empty, unsorted,
+    out-of-range view lists are input errors (code 7) and launch nothing."""
+    n, V, B = 32, 10, 48
+    with P.plan_geometry(n, V, B, factors=(1,)) as plan:
+        x = torch.zeros((1, n, n), device="cuda")
+        for bad in ([], [3, 3], [11], [-1, 2]):
+            with pytest.raises(P.MS2GError) as e:
+                P.forward_project(plan, 1, x, subset=bad)
+            assert e.value.code == 7, bad

@@ -655,7 +655,11 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   const BpTiling t = bp_tiling(f.nc, H);
   int ch[2], vpc[2];
   for (int fam = 0; fam < 2; ++fam) {
-    ch[fam] = f.bp_chunks[fam];
+    // the plan's chunking is for all V_r views; a view subset (Option 2, a
+    // minibatch) keeps the views per chunk, not the chunk count: otherwise a
+    // 90-view subset would be cut into 4-view chunks whose fixed cost
+    // (accumulator zeroing, partial planes, their reduction) dominates
+    ch[fam] = (int)(((long long)f.bp_chunks[fam] * n_sel + p->V_r - 1) / p->V_r);
     const int max_chunks = (n_sel + kBW - 1) / kBW;
     if (ch[fam] > max_chunks) ch[fam] = max_chunks;
     if (ch[fam] < 1) ch[fam] = 1;

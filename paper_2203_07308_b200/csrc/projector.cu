@@ -638,11 +638,16 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
                       const int* d_sel, int n_sel, const int* ch, const int* vpc, const BpTiling& t,
                       const int* order) {
   constexpr size_t smem = BpShape<H>::kSmem;
-  static bool attr = false;
-  if (!attr) {   // several blocks of 36-51 KB per SM need the maximum shared-memory carveout
+  // several blocks of 36-51 KB per SM need the maximum shared-memory carveout;
+  // function attributes are per device, so remember which devices have them
+  static std::atomic<uint64_t> attr_devices{0};
+  int dev = 0;
+  MS2G_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_devices.load() & bit)) {
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    attr = true;
+    attr_devices.fetch_or(bit);
   }
   k_backward<H><<<grid, 32 * kBW, smem, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, sino, p->w_part,
                                              f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order);

@@ -102,6 +102,9 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- oracle arm --
+_last_s2 = [None]   # seconds of the last all-core factor-2 oracle gradient (for the 1-core ratio)
+
+
 def oracle_sample(pr, b_full, nthreads):
     """Time the fp64 oracle on a bounded sample of the C4 solve: one factor-2
     gradient, one full gradient and one Gaussian denoise; compose the solve
@@ -123,6 +126,7 @@ def oracle_sample(pr, b_full, nthreads):
     n2 = sum(st[1] for st in pr.stages if st[0] == 2)
     n1 = sum(st[1] for st in pr.stages if st[0] == 1)
     solve = (pr.power_iters + n2) * t[2] + (pr.power_iters + n1) * t[1] + pr.n_steps * t["den"]
+    _last_s2[0] = t[2]
     desc = (f"C{pr.cfg} oracle, {nthreads} threads: 1 factor-2 gradient ({t[2]:.2f} s) + 1 full gradient "
             f"({t[1]:.2f} s) + 1 Gaussian denoise ({t['den']:.3f} s), composed into one solve "
             f"({pr.power_iters}+{n2} factor-2 and {pr.power_iters}+{n1} full gradient-equivalents, "
@@ -469,6 +473,15 @@ def run_ms2g(args, rank, nranks, local_rank):
         nth = O.default_threads()
         v, secs, desc = oracle_sample(pr, b_full.astype(np.float64), nth)
         cpu = {"value": v, "unit": "iters/s", "cores": nth, "kind": "oracle", "sample": desc}
+        # one core: a factor-2 gradient on every 16th view, scaled to the solve
+        g_ = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+        xs_ = S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg, 9)).astype(np.float64)
+        views_ = np.arange(0, pr.n_views, 16)
+        a_ = time.perf_counter()
+        O.sketched_grad(g_, 2, xs_, b_full.astype(np.float64), views=views_, nthreads=1)
+        t1_ = (time.perf_counter() - a_) * 16          # all views, factor 2, one core
+        cpu["one_core"] = {"s2_gradient_s": t1_, "sample": "1 factor-2 gradient on 90 of 1440 views x 16",
+                           "speedup_all_cores": t1_ / secs_s2 if (secs_s2 := _last_s2[0]) else None}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": nranks, "steps": args.steps,

@@ -218,6 +218,7 @@ def sketch_up(gc, s: int):
 
 def sketched_grad(g: Geometry, factor: int, x, b, views=None, nthreads: int | None = None, resampler: int = 0):
     """O6/O7: g = (V/|M|) U A_s^T (A_s S x - b_M)  (Eqs. 6-7).
+    b is the full [V][B] sinogram, indexed by view (b_M = its rows `views`).
     resampler 0: average pool + replication (O4/O5); 1: bicubic (NEXT-1)."""
     x = _f64(x); b = _f64(b)
     vv, n_sel = _views(views, g.n_views)

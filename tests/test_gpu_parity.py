@@ -629,3 +629,26 @@ def test_empty_subset_and_bad_views_rejected(P):
             with pytest.raises(P.MS2GError) as e:
                 P.forward_project(plan, 1, x, subset=bad)
             assert e.value.code == 7, bad
+
+
+def test_plan_lifecycle_releases_memory(P):
+    """Plans own every workspace (no allocation inside a solve) and release it:
+    repeated plan / solve / destroy cycles leave device memory where it was."""
+    n, V, B = 128, 60, 192
+    b = torch.from_numpy(S.random_sinogram((V, B), 3, zero_mean=False)).cuda()[None].contiguous()
+
+    def cycle():
+        with P.plan_geometry(n, V, B, factors=(2, 1)) as plan:
+            P.pnp_ms2g_solve(plan, [(2, 2, 0), (1, 1, 0)], b, den=("tv", 0.02, 5), alpha=1.0)
+            P.set_kernel_timing(plan, True)
+            P.pnp_ms2g_solve(plan, [(2, 2, 0), (1, 1, 0)], b, den=("tv", 0.02, 5), alpha=1.0)
+            P.attach_peers(plan, 0, 1)
+            P.sketched_grad(plan, 2, torch.zeros((1, n, n), device="cuda"), b)
+        torch.cuda.synchronize()
+
+    cycle()                                   # first-use allocations (libraries, module load)
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(10):
+        cycle()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 <= 8 << 20, (free0 - free1) / 2**20

@@ -16,8 +16,9 @@
  *  - `stream` is a cudaStream_t passed as void*.  Every call is asynchronous
  *    and ordered on that stream, except where "synchronous" is stated.
  *  - A plan is used by one host thread at a time.  No call allocates device
- *    memory after ms2g_plan_geometry / ms2g_attach_nccl, so sequences of calls
- *    are CUDA-graph capturable.
+ *    memory after ms2g_plan_geometry / ms2g_attach_nccl / ms2g_attach_peers
+ *    (except a first Option-5 solve's SAGA table, allocated before capture),
+ *    so sequences of calls are CUDA-graph capturable.
  *  - Configuration errors are detected on the host before any launch.
  */
 #ifndef MS2G_H
@@ -108,7 +109,8 @@ int ms2g_forward_project(ms2g_plan* plan, int32_t factor, const float* x, const 
 /* Exact adjoint ("A_s^T"):  img[b] = scale * A_s^T sino[b]
  * (accumulate != 0: img += ...).  sino is compacted [batch][n_sel][B] in the
  * same view order forward_project used.  allreduce != 0 sums the partial
- * images over the attached NCCL ranks in place (requires attach_nccl). */
+ * images over the ranks in place (requires attach_nccl or attach_peers; with
+ * one rank and neither attached it is a no-op). */
 int ms2g_back_project(ms2g_plan* plan, int32_t factor, const float* sino, float* img, float scale,
                       int32_t accumulate, const int32_t* subset, int32_t n_subset, int32_t allreduce,
                       void* stream);
@@ -131,8 +133,8 @@ int ms2g_sketch_up(ms2g_plan* plan, int32_t factor, int32_t kind, const float* g
 /* Sketched data-fidelity gradient (Eq. 6, Eq. 7):
  *   g = (V/|M|) U A_s^T (A_s S x - b_M)      (full resolution n x n)
  * factor 1 gives A^T(Ax - b).  subset NULL = all views (|M| = V).
- * kind selects S/U (see MS2G_RESAMPLE_*).  With NCCL attached the partial
- * A_s^T is allreduced before U. */
+ * kind selects S/U (see MS2G_RESAMPLE_*).  With NCCL or peers attached the
+ * partial A_s^T is summed over the ranks before U. */
 int ms2g_sketched_grad(ms2g_plan* plan, int32_t factor, int32_t kind, const float* x, const float* bsino, float* g,
                        const int32_t* subset, int32_t n_subset, void* stream);
 

@@ -652,3 +652,44 @@ def test_plan_lifecycle_releases_memory(P):
         cycle()
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 <= 8 << 20, (free0 - free1) / 2**20
+
+
+def test_full_size_sampled_c3_subset_and_c5_batch(P):
+    """C3 (512^2, 720 x 768, one interleaved 90-view subset) and C5 (batch of
+    8 images) at full size in the launch configurations the solves use:
+    sampled rays and pixels against the oracle, one by one."""
+    rng = np.random.default_rng(35)
+    pr = S.PRESETS[3]
+    n, V, B = pr.n, pr.n_views, pr.n_bins
+    g = O.Geometry(n, V, B)
+    sub = list(range(3, V, 8))
+    with P.plan_geometry(n, V, B, factors=(4, 2, 1)) as plan:
+        for s in (4, 1):
+            nc = n // s
+            x = S.random_image(nc, 90 + s)
+            got = host(P.forward_project(plan, s, dev(x)[None], subset=sub))[0]
+            kk, tt = rng.integers(0, len(sub), 100), rng.integers(0, B, 100)
+            ref = np.array([O.ray_sum(g, s, x, sub[int(k)], int(t)) for k, t in zip(kk, tt)])
+            assert rel(got[kk, tt], ref) <= TOL_OP, s
+            r = S.random_sinogram((len(sub), B), 95 + s)
+            img = host(P.back_project(plan, s, dev(r)[None], subset=sub))[0]
+            pix = [(0, 0), (nc - 1, nc - 1), (nc // 2, nc // 3), (nc // 5, nc - 2)]
+            refp = np.array([O.backward_pixel(g, s, r, i, j, views=sub) for i, j in pix])
+            gotp = np.array([img[i, j] for i, j in pix])
+            assert np.max(np.abs(gotp - refp)) <= TOL_OP * np.sqrt(np.mean(img ** 2)) * 3, s
+    pr = S.PRESETS[5]
+    nb = pr.batch
+    with P.plan_geometry(n, V, B, factors=(2, 1), batch=nb) as plan:
+        xs = np.stack([S.random_image(n, 200 + i) for i in range(nb)])
+        got = host(P.forward_project(plan, 1, dev(xs)))
+        for i in (0, nb - 1):
+            vv, tt = rng.integers(0, V, 60), rng.integers(0, B, 60)
+            ref = np.array([O.ray_sum(g, 1, xs[i], int(v), int(t)) for v, t in zip(vv, tt)])
+            assert rel(got[i][vv, tt], ref) <= TOL_OP, i
+        rs = np.stack([S.random_sinogram((V, B), 300 + i) for i in range(nb)])
+        img = host(P.back_project(plan, 2, dev(rs)))
+        for i in (0, nb - 1):
+            pix = [(0, 0), (255, 255), (100, 17)]
+            refp = np.array([O.backward_pixel(g, 2, rs[i], a, c) for a, c in pix])
+            gotp = np.array([img[i][a, c] for a, c in pix])
+            assert np.max(np.abs(gotp - refp)) <= TOL_OP * np.sqrt(np.mean(img[i] ** 2)) * 3, i

@@ -53,4 +53,5 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="-v" in sys.argv))
+    # --debug: device bounds checks (MS2G_DASSERT) into the default library path
+    print(build(force=True, verbose="-v" in sys.argv, defines=("MS2G_DEBUG=1",) if "--debug" in sys.argv else ()))

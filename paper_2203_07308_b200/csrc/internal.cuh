@@ -15,6 +15,21 @@
 
 namespace ms2g {
 
+// Device bounds checks for the debug build (-DMS2G_DEBUG=1, `build.py --debug`):
+// a violated index traps the kernel (the launch then fails with an error)
+// instead of reading or writing out of bounds.  compute-sanitizer is closed on
+// this GPU pool, so the GPU test suite is also run against this build.
+#if defined(MS2G_DEBUG) && MS2G_DEBUG
+#define MS2G_DASSERT(cond) \
+  do {                     \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define MS2G_DASSERT(cond) \
+  do {                     \
+  } while (0)
+#endif
+
 // Fixed-point minor coordinate: 32 fractional bits (1 unit = 2^-32 pixel).
 constexpr double kFix = 4294967296.0;
 

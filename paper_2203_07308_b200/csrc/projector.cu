@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
   int bxi = blockIdx.x, byi = blockIdx.y;
   if (order) {
     const int item = __ldg(order + blockIdx.y * gridDim.x + blockIdx.x);
+    MS2G_DASSERT(item >= 0 && item < (int)(gridDim.x * gridDim.y));
     bxi = item % gridDim.x;
     byi = item / gridDim.x;
   }
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
         asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
         const float mf = (float)min(elo, S);
         const unsigned e = offk + min(ehi, umax);
+        MS2G_DASSERT(e < (unsigned)(nc * L));
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           float pl, pu;
@@ -265,6 +267,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
       asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
       const float mf = (float)min(elo, S);
       const unsigned e = offk + min(ehi, umax);
+      MS2G_DASSERT(e < (unsigned)(nc * L));
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
         float pl, pu;
@@ -470,6 +473,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   const int bi = bx - fam * per * chx;
   const int ti = bi % per, chunk = bi / per;
   const int tile = fam * per + ti;                 // index into the range table
+  MS2G_DASSERT(bx >= 0 && bx < (int)gridDim.x && ti < per);
   const int vpc = fam ? vpcy : vpcx;
   const int plane = fam ? chx + chunk : chunk;
   const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * kBH;   // major / minor origin
@@ -529,6 +533,9 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     rn = __ldg(sb + (size_t)k * B + tn);
   }
   const unsigned tbase = (unsigned)__cvta_generic_to_shared(T) + 4u * (unsigned)lane;
+  const unsigned acc0 = (unsigned)__cvta_generic_to_shared(acc), acc1 = acc0 + 4u * kAccRows * kBT;
+  (void)acc0;
+  (void)acc1;
   while (have) {
     // commit the prefetched round to shared memory (tile-relative end coordinate, +1 row)
     const int cte = te, ctb = tb;
@@ -567,6 +574,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
       const float mu = (float)m, ml = (float)(S - m);
       const unsigned adu = sbase + min(u, (unsigned)(kBH + 2)) * sstride;
       const unsigned adl = adu - sstride;
+      MS2G_DASSERT(adu >= acc0 && adu < acc1 && adl >= acc0 && adl < acc1);
       asm volatile("{\n\t.reg .f32 c0, c1;\n\t"
                    "ld.shared.f32 c0, [%0];\n\t"
                    "ld.shared.f32 c1, [%1];\n\t"
@@ -593,6 +601,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   }
   const size_t np = (size_t)nc * nc;
   const int nplanes = chx + (int)((gridDim.x - per * chx) / per);   // X chunks + Y chunks
+  MS2G_DASSERT(plane < nplanes);
   float* dst = part + ((size_t)bz * nplanes + plane) * np;
   if (!fam) {       // X-tile: row l = y - m0, lane = x - c0 (coalesced)
 #pragma unroll

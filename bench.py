@@ -401,10 +401,29 @@ def run_ms2g(args, rank, nranks, local_rank):
         dist.all_reduce(tc, op=dist.ReduceOp.MAX)
     t_cached = float(tc.item())
 
+    # steady-state iterations/s of each stage alone (SURVEY 8(d) "iters/s per
+    # stage"): a one-stage schedule with the cached step, 50 iterations
+    stage_rate = {}
+    for fac in sorted({s_[0] for s_ in pr.stages}, reverse=True):
+        one = [(fac, 50, 0)]
+        P.pnp_ms2g_solve_async(plan, one, b, x0, xo, den=pr.den, alpha=pr.alpha, power_iters=0)
+        P.solve_status(plan)
+        c0.record(st)
+        for _ in range(args.steps):
+            P.pnp_ms2g_solve_async(plan, one, b, x0, xo, den=pr.den, alpha=pr.alpha, power_iters=0)
+        c1.record(st)
+        c1.synchronize()
+        try:
+            P.solve_status(plan)
+        except P.MS2GError:
+            pass    # 50 iterations of one stage alone may leave the safe range of the toy; timing only
+        stage_rate[f"s{fac}"] = 50 * args.steps / (c0.elapsed_time(c1) / 1000.0)
+
     # ---- per-kernel timing of the projector pair + operator throughputs ----
     nnz = nnz_counts()[f"C{pr.cfg}"]
     frac_views = (ve - vb) / pr.n_views
-    detail = {"solve_cached_step": {"iters_per_s": pr.n_steps * args.steps / t_cached,
+    detail = {"stage_iters_per_s": stage_rate,
+              "solve_cached_step": {"iters_per_s": pr.n_steps * args.steps / t_cached,
                                     "ms_per_solve": 1000.0 * t_cached / args.steps,
                                     "note": "power_iters=0: per-stage step 1/L reused from the plan's cache "
                                             "(computed by the headline solves); L2 not flushed"}}

@@ -52,7 +52,10 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_quality_study.md"))
     a = ap.parse_args()
     dev = torch.device("cuda")
-    import oracle as O
+    # segment counts from the oracle-written table (scripts/count_nnz.py --study-only):
+    # this script drives the product path only
+    with open(os.path.join(ROOT, "profiles", "nnz_counts.json")) as f:
+        nnz_all = json.load(f)
     n, B, N = a.n, a.bins, a.iters
     xt = S.phantom(n, 20, S.config_seed(2)).astype(np.float32)
     schedules = {
@@ -63,8 +66,9 @@ def main():
     rows = []
     for name, st in SETTINGS.items():
         V = st["n_views"]
-        g = O.Geometry(n, V, B, arc=st["arc"])
-        nnz = {s: O.count_nnz(g, s) for s in (4, 2, 1)}
+        ent = nnz_all[f"QS_{name}"]
+        assert ent["geometry"][:3] == [n, V, B], "run scripts/count_nnz.py --study-only for this geometry"
+        nnz = {s: ent[str(s)] for s in (4, 2, 1)}
         with P.plan_geometry(n, V, B, factors=(4, 2, 1), arc=st["arc"]) as plan:
             p = P.forward_project(plan, 1, torch.from_numpy(xt).to(dev)[None])[0].cpu().numpy()
             b = torch.from_numpy(S.poisson_data(p, st["i0"], S.config_seed(2))).to(dev)[None].contiguous()

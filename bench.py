@@ -477,6 +477,7 @@ def run_ms2g(args, rank, nranks, local_rank):
                 "launches_timed": n_l, "launch_ms": tk * 1e3,
                 "instrumented_ms_per_step": t_instr / args.steps,
                 "compulsory_frac": compulsory / tk / 1e9 / hbm,
+                "frac_vs_nominal_8tbs": achieved / 8000.0,   # also against the nominal HBM3e peak
                 # what actually bounds the kernel (ncu --set full, profiles/r01_ncu_full_projectors.md):
                 # L1/shared data-pipe wavefronts, fraction of the per-SM peak of one per clock
                 "l1_data_pipe_frac": l1frac,

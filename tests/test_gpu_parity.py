@@ -693,3 +693,28 @@ def test_full_size_sampled_c3_subset_and_c5_batch(P):
             refp = np.array([O.backward_pixel(g, 2, rs[i], a, c) for a, c in pix])
             gotp = np.array([img[i][a, c] for a, c in pix])
             assert np.max(np.abs(gotp - refp)) <= TOL_OP * np.sqrt(np.mean(img[i] ** 2)) * 3, i
+
+
+@pytest.mark.parametrize("kw", [
+    dict(arc=np.pi),                                   # limited angle
+    dict(fov=1.0, sod=1.3, sdd=3.1),                   # other FOV and distances
+    dict(bin_pitch=0.03),                              # wider detector pitch
+    dict(arc=np.pi / 3),                               # 60-degree arc
+])
+def test_geometry_variants(P, kw):
+    """Forward, adjoint and a short solve on non-default geometries (limited
+    angle, FOV / source distances, detector pitch) against the oracle."""
+    n, V, B = 96, 48, 144
+    g = O.Geometry(n, V, B, **{k: v for k, v in kw.items()})
+    with P.plan_geometry(n, V, B, factors=(2, 1), **kw) as plan:
+        for s in (2, 1):
+            x = S.random_image(n // s, 60 + s)
+            assert rel(host(P.forward_project(plan, s, dev(x)[None]))[0], O.forward(g, s, x)) <= TOL_OP, s
+            r = S.random_sinogram((V, B), 61 + s)
+            assert rel(host(P.back_project(plan, s, dev(r)[None]))[0], O.backward(g, s, r)) <= TOL_OP, s
+        xt = S.phantom(n, 8, 62)
+        b = O.forward(g, 1, xt).astype(np.float32)
+        stages = [(2, 4, 0), (1, 3, 0)]
+        xo = host(P.pnp_ms2g_solve(plan, stages, dev(b)[None], den=("tv", 0.02, 10), alpha=1.0))[0]
+    xr, _, _ = O.pnp_ms2g(g, stages, b, den=("tv", 0.02, 10), alpha=1.0)
+    assert rel(xo, xr) <= TOL_SOLVE

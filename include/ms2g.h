@@ -228,7 +228,6 @@ int ms2g_pnp_ms2g_solve_async(ms2g_plan* plan, const ms2g_solve_desc* desc, cons
 /* Synchronous: returns MS2G_OK or MS2G_ERR_DIVERGED for the last solve. */
 int ms2g_solve_status(ms2g_plan* plan, void* stream);
 
-/* Thread-local message of the last failing call ("" if none). */
 /* Per-kernel timing inside the solve graph (measurement support).
  * ms2g_set_kernel_timing(plan, 1): the next captured solve graph records an
  * external CUDA event before and after every projector launch (k_forward,
@@ -239,6 +238,7 @@ int ms2g_solve_status(ms2g_plan* plan, void* stream);
 int ms2g_set_kernel_timing(ms2g_plan* plan, int32_t enable);
 int ms2g_kernel_time(ms2g_plan* plan, int32_t kind, int32_t factor, double* total_ms, int32_t* launches);
 
+/* Thread-local message of the last failing call ("" if none). */
 const char* ms2g_last_error(void);
 
 /* Number of device kernels libms2g has launched in this process (graph

@@ -382,7 +382,10 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 // The X- and Y-families write separate partial planes (per view chunk too);
 // k_chunk_reduce sums them in fixed order.
 constexpr int kBT = 32;                          // major extent (lanes)
-constexpr int kBW = 4;                           // warps per block
+#ifndef MS2G_BW
+#define MS2G_BW 4
+#endif
+constexpr int kBW = MS2G_BW;                     // warps per block
 constexpr int kPadR = 2;
 // minor extent H of the tiles: 64 (6 blocks of 36 KB per SM) or, for n_c >=
 // 1024, 96 (4 blocks of 51 KB; lane utilisation 0.88, measured 10 % faster
@@ -396,7 +399,7 @@ struct BpShape {
   static constexpr int kWinR = H + kPadR;                // rows per warp window (+ shared pads)
   static constexpr int kAccRows = kPadR + kBW * kWinR;
   static constexpr size_t kSmem = sizeof(float) * kAccRows * kBT;
-  static constexpr int kMinBlocks = H <= 64 ? 6 : 4;
+  static constexpr int kMinBlocks = (H <= 64 ? 24 : 16) / kBW;   // resident warps: 24 (H = 64) / 16 (H = 96)
 };
 
 struct BpTiling {

@@ -147,6 +147,26 @@ struct ms2g_plan {
   int* w_peer_err = nullptr;
   int peer_rank = 0, peer_n = 0;       // peer_n > 0: attached
   std::vector<void*> peer_opened;      // IPC mappings to close
+  // Power-iteration branches of the solve graph: one per stage factor, each
+  // with its own workspaces (batch 1), so the geometry-only power chains of
+  // all stages run concurrently with each other and with the earlier stages'
+  // steps.  Single rank only (a communicator is not used from two branches).
+  struct PowerBranch {
+    int factor = 0;
+    float* w_v = nullptr;
+    float2* w_pair = nullptr;
+    size_t pair_stride = 0;
+    float* w_res = nullptr;
+    float* w_G = nullptr;
+    float* w_part = nullptr;
+    double* w_red = nullptr;
+    double* w_pw = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+  };
+  std::vector<PowerBranch> pbr;
+  cudaEvent_t ev_fork = nullptr;
+  ms2g_plan* root = nullptr;           // set on shadow copies that borrow a branch's workspaces
   // per-kernel timing inside the captured solve graph (ms2g_set_kernel_timing):
   // external event-record nodes around every k_forward / k_backward launch
   struct TimedLaunch { cudaEvent_t a, b; int kind, factor; };

@@ -30,6 +30,7 @@ const FactorTables* find_factor(const ms2g_plan* p, int factor) {
 }
 
 int timing_begin(ms2g_plan* p, int kind, int factor, cudaStream_t st) {
+  if (p->root) p = p->root;
   if (!p->timing || !t_capturing) return -1;
   ms2g_plan::TimedLaunch tl{nullptr, nullptr, kind, factor};
   if (cudaEventCreate(&tl.a) != cudaSuccess || cudaEventCreate(&tl.b) != cudaSuccess) return -1;
@@ -39,6 +40,7 @@ int timing_begin(ms2g_plan* p, int kind, int factor, cudaStream_t st) {
 }
 
 void timing_end(ms2g_plan* p, int slot, cudaStream_t st) {
+  if (p->root) p = p->root;
   if (slot < 0) return;
   cudaEventRecordWithFlags(p->tev[slot].b, st, cudaEventRecordExternal);
 }
@@ -278,6 +280,18 @@ static void free_plan(ms2g_plan* p) {
   if (p->sel_ev) cudaEventDestroy(p->sel_ev);
   if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
   if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
+  for (auto& br : p->pbr) {
+    cudaFree(br.w_v);
+    cudaFree(br.w_pair);
+    cudaFree(br.w_res);
+    cudaFree(br.w_G);
+    cudaFree(br.w_part);
+    cudaFree(br.w_red);
+    cudaFree(br.w_pw);
+    if (br.stream) cudaStreamDestroy(br.stream);
+    if (br.done) cudaEventDestroy(br.done);
+  }
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   for (void* q : p->peer_opened) cudaIpcCloseMemHandle(q);
   cudaFree(p->xch_buf);
   cudaFree(p->xch_pad);
@@ -520,6 +534,73 @@ static int prepare_subsets(ms2g_plan* p, int n_subsets) {
   return MS2G_OK;
 }
 
+// Branch workspaces for the power chains of the stage factors (allocated
+// once, outside any capture).  Returns false when branching is not used.
+static bool power_branching(const ms2g_plan* p) {
+  static const bool off = getenv("MS2G_SERIAL_POWER") != nullptr;   // experiment switch
+  return !off && p->nranks == 1 && !p->comm && p->peer_n == 0;
+}
+
+static int ensure_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd) {
+  for (int k = 0; k < sd->n_stages; ++k) {
+    const int fac = sd->stages[k].factor;
+    bool have = false;
+    for (const auto& br : p->pbr) have |= br.factor == fac;
+    if (have) continue;
+    const FactorTables* f = find_factor(p, fac);
+    ms2g_plan::PowerBranch br;
+    br.factor = fac;
+    const size_t nc = (size_t)f->nc, np = nc * nc;
+    br.pair_stride = nc * (nc + 3);
+    const size_t planes = (size_t)(f->bp_chunks[0] + f->bp_chunks[1]);
+    MS2G_CUDA(cudaMalloc(&br.w_v, sizeof(float) * np));
+    MS2G_CUDA(cudaMalloc(&br.w_pair, sizeof(float2) * 4 * br.pair_stride));
+    MS2G_CUDA(cudaMemset(br.w_pair, 0, sizeof(float2) * 4 * br.pair_stride));
+    MS2G_CUDA(cudaMalloc(&br.w_res, sizeof(float) * (size_t)p->V_r * p->B));
+    MS2G_CUDA(cudaMalloc(&br.w_G, sizeof(float) * np));
+    MS2G_CUDA(cudaMalloc(&br.w_part, sizeof(float) * planes * np));
+    MS2G_CUDA(cudaMalloc(&br.w_red, sizeof(double) * 2 * p->red_blocks));
+    MS2G_CUDA(cudaMalloc(&br.w_pw, sizeof(double) * 8));
+    MS2G_CUDA(cudaStreamCreateWithFlags(&br.stream, cudaStreamNonBlocking));
+    MS2G_CUDA(cudaEventCreateWithFlags(&br.done, cudaEventDisableTiming));
+    p->pbr.push_back(br);
+  }
+  if (!p->ev_fork) MS2G_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  return MS2G_OK;
+}
+
+// Fork every stage factor's power chain onto its branch (inside the capture):
+// the chain writes the factor's step cache and every stage slot of that
+// factor, then records the branch's `done` event for the stage to wait on.
+static int enqueue_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd, cudaStream_t st) {
+  MS2G_CUDA(cudaEventRecord(p->ev_fork, st));
+  for (auto& br : p->pbr) {
+    int first = -1;
+    for (int k = 0; k < sd->n_stages; ++k)
+      if (sd->stages[k].factor == br.factor && first < 0) first = k;
+    if (first < 0) continue;
+    MS2G_CUDA(cudaStreamWaitEvent(br.stream, p->ev_fork, 0));
+    ms2g_plan shadow = *p;                 // same tables, the branch's workspaces
+    shadow.root = p;
+    shadow.w_v = br.w_v;
+    shadow.w_pair = br.w_pair;
+    shadow.pair_stride = br.pair_stride;
+    shadow.w_res = br.w_res;
+    shadow.w_G = br.w_G;
+    shadow.w_part = br.w_part;
+    shadow.w_red = br.w_red;
+    shadow.w_pw = br.w_pw;
+    const FactorTables* f = find_factor(p, br.factor);
+    MS2G_TRY(enqueue_power(&shadow, *f, sd->power_iters, p->w_scal + first, p->w_scal + 64 + first,
+                           p->w_etaf + first, br.stream));
+    for (int k = first + 1; k < sd->n_stages; ++k)
+      if (sd->stages[k].factor == br.factor)
+        MS2G_TRY(launch_cached_step(f->d_Lcache, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, br.stream));
+    MS2G_CUDA(cudaEventRecord(br.done, br.stream));
+  }
+  return MS2G_OK;
+}
+
 // The whole solve as one stream-ordered sequence (captured into a graph).
 static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vector<ms2g_sched_entry>& sch,
                          const float* b, const float* x0, float* x_out, cudaStream_t st) {
@@ -531,13 +612,19 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
   MS2G_CUDA(cudaMemcpyAsync(p->w_y, x0, sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
   int cur = 0;
   size_t step = 0;
+  const bool branched = sd->power_iters > 0 && power_branching(p);
+  if (branched) MS2G_TRY(enqueue_power_branches(p, sd, st));
   for (int k = 0; k < sd->n_stages; ++k) {
     const ms2g_stage& stg = sd->stages[k];
     const FactorTables* f = find_factor(p, stg.factor);
-    if (sd->power_iters > 0)
+    if (branched) {           // this stage's step size comes from its factor's branch
+      for (const auto& br : p->pbr)
+        if (br.factor == stg.factor) MS2G_CUDA(cudaStreamWaitEvent(st, br.done, 0));
+    } else if (sd->power_iters > 0) {
       MS2G_TRY(enqueue_power(p, *f, sd->power_iters, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
-    else   // reuse the plan's cached step for this factor (geometry-only, S8(e))
+    } else {   // reuse the plan's cached step for this factor (geometry-only, S8(e))
       MS2G_TRY(launch_cached_step(f->d_Lcache, p->w_scal + k, p->w_scal + 64 + k, p->w_etaf + k, st));
+    }
     int step_in_stage = 0;
     if (sd->option == 5 && step < sch.size() && sch[step].stage == k) {
       // SAGA table at the stage start: phi_q = c_q A_{M_q}^T (A_{M_q} S y - b), avg = mean_q phi_q
@@ -667,6 +754,7 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
   }
   const std::string key = solve_key(sd, b, x0, x_out);
   if (sd->option == 4 && (key != p->sg.key || !p->sg.exec)) MS2G_TRY(prepare_minibatches(p, sd, (int)sch.size()));
+  if (sd->power_iters > 0 && power_branching(p)) MS2G_TRY(ensure_power_branches(p, sd));
   if (key != p->sg.key || !p->sg.exec) {
     if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
     if (p->sg.graph) cudaGraphDestroy(p->sg.graph);

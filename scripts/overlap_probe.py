@@ -1,6 +1,7 @@
-"""Does running two independent power iterations (factor 2 and factor 1 of the
-C4 geometry, separate plans = separate workspaces) concurrently on two streams
-beat running them back to back?  (dev aid; timings by CUDA events / wall)"""
+"""Does running independent power iterations (one per stage factor, separate
+plans = separate workspaces) concurrently on separate streams beat running
+them back to back?  (dev aid; wall-clock around synchronised regions)"""
+import argparse
 import os
 import sys
 import threading
@@ -13,29 +14,34 @@ import torch  # noqa: E402
 import ms2g_synth as S  # noqa: E402
 import paper_2203_07308_b200 as P  # noqa: E402
 
-pr = S.PRESETS[4]
-pa = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2,))
-pb = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(1,))
-sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+ap = argparse.ArgumentParser()
+ap.add_argument("--cfg", type=int, default=4)
+a = ap.parse_args()
+pr = S.PRESETS[a.cfg]
+facs = sorted({s[0] for s in pr.stages}, reverse=True)
+plans = [P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(f,)) for f in facs]
+streams = [torch.cuda.Stream() for _ in facs]
 
 
-def run(plan, f, st, out, k):
+def run(plan, f, st):
     with torch.cuda.stream(st):
-        out[k] = P.power_iteration(plan, f, 20)
+        P.power_iteration(plan, f, 20)
 
 
-res = [None, None]
 for rep in range(3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    run(pa, 2, sa, res, 0)
-    run(pb, 1, sb, res, 1)
+    for pl, f, st in zip(plans, facs, streams):
+        run(pl, f, st)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    ta = threading.Thread(target=run, args=(pa, 2, sa, res, 0))
-    tb = threading.Thread(target=run, args=(pb, 1, sb, res, 1))
+    th = [threading.Thread(target=run, args=(pl, f, st)) for pl, f, st in zip(plans, facs, streams)]
     t2 = time.perf_counter()
-    ta.start(); tb.start(); ta.join(); tb.join()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
     torch.cuda.synchronize()
     t3 = time.perf_counter()
-    print(f"sequential {1e3 * (t1 - t0):.1f} ms, concurrent {1e3 * (t3 - t2):.1f} ms", flush=True)
+    print(f"C{a.cfg} factors {facs}: sequential {1e3 * (t1 - t0):.2f} ms, concurrent {1e3 * (t3 - t2):.2f} ms",
+          flush=True)

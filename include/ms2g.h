@@ -232,6 +232,8 @@ int ms2g_solve_status(ms2g_plan* plan, void* stream);
  * ms2g_set_kernel_timing(plan, 1): the next captured solve graph records an
  * external CUDA event before and after every projector launch (k_forward,
  * k_backward); 0 removes them (the cached graph is re-captured either way).
+ * An instrumented solve runs its power iterations serially (no concurrent
+ * branches), so each timed interval holds one kernel alone on the GPU.
  * ms2g_kernel_time: for the LAST replayed solve, the summed device time (ms)
  * and count of the launches of one kind (0 forward, 1 backward) at one
  * factor.  Synchronizes on those events.  MS2G_ERR_INPUT on NULL. */

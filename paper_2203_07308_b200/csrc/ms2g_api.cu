@@ -538,7 +538,9 @@ static int prepare_subsets(ms2g_plan* p, int n_subsets) {
 // once, outside any capture).  Returns false when branching is not used.
 static bool power_branching(const ms2g_plan* p) {
   static const bool off = getenv("MS2G_SERIAL_POWER") != nullptr;   // experiment switch
-  return !off && p->nranks == 1 && !p->comm && p->peer_n == 0;
+  // kernel timing wants each launch's own duration: concurrent branches would
+  // share the GPU inside the timed intervals, so an instrumented solve is serial
+  return !off && !p->timing && p->nranks == 1 && !p->comm && p->peer_n == 0;
 }
 
 static int ensure_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd) {

@@ -77,6 +77,12 @@ struct FactorTables {
   int* d_bp_order = nullptr;      // full-view launches: block -> work item, longest first
   int* d_fwd_order = nullptr;     // same for the single-image forward (for fwd_order_vpb views per block)
   int fwd_order_vpb = 0;
+  // host cost tables behind the orders (also used for subset orders):
+  // rays meeting (tile, view) [2 tiles-per-family][V_r]; longest ray column
+  // range of (view, 32-bin block) [V_r][ceil(B/32)]
+  std::vector<uint16_t> h_bp_cost, h_fwd_cost;
+  // per interleaved subset of the current Option-2/3/5 partition: block orders
+  std::vector<int*> d_bp_order_sub, d_fwd_order_sub;
   // bicubic resampling tables (NEXT-1), [n_out][taps] clamped input index / weight
   int taps_down = 0, taps_up = 0;
   int* d_idx_down = nullptr;
@@ -225,14 +231,18 @@ void timing_end(ms2g_plan* p, int slot, cudaStream_t st);
 
 // ---- kernel launchers (projector.cu) ----
 int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s);
+// order_sel: longest-first block order for a subset launch (d_sel != NULL),
+// built for this view list (subset_orders in ms2g_api.cu); NULL = grid order
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
-                   int batch, cudaStream_t s);
+                   int batch, cudaStream_t s, const int* order_sel = nullptr);
 int bp_tile_count(int nc);   // adjoint tiles (both families) of an n_c grid
 int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch);
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
 // publish != 0: write scale * A_s^T sino into the peer exchange slot (not img)
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
-                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish = 0);
+                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish = 0,
+                    const int* order_sel = nullptr);
+void bp_launch_chunks(const ms2g_plan* p, const FactorTables& f, int n_sel, int* ch);
 
 // ---- peer-memory allreduce (peer_reduce.cu, NEXT-3) ----
 int launch_peer_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st);

@@ -61,6 +61,51 @@ static long long floor_div(long long a, long long b) {
 }
 static long long ceil_div(long long a, long long b) { return -floor_div(-a, b); }
 
+// Longest-first (LPT) block orders from the host cost tables, for a launch over
+// `views` (rank-local, in launch order).  Adjoint: block = (family, view chunk,
+// tile) with the chunking of bp_launch_chunks; forward: block = (view block of
+// vpb views, 32-bin block).  The result (a permutation of the block indices,
+// longest first) goes to a new device array.
+static int upload_order(const std::vector<long long>& cost, int** out) {
+  std::vector<int> order(cost.size());
+  for (size_t it = 0; it < order.size(); ++it) order[it] = (int)it;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  MS2G_CUDA(cudaMalloc(out, sizeof(int) * std::max<size_t>(order.size(), 1)));
+  MS2G_CUDA(cudaMemcpy(*out, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
+  return MS2G_OK;
+}
+
+static int upload_bp_order(const ms2g_plan* p, const FactorTables& f, const std::vector<int>& views, int** out) {
+  const int n_sel = (int)views.size(), V_r = p->V_r;
+  const int per_t = bp_tile_count(f.nc) / 2;
+  int ch[2];
+  bp_launch_chunks(p, f, n_sel, ch);
+  const int n_items = per_t * (ch[0] + ch[1]);
+  std::vector<long long> cost(n_items, 0);
+  for (int it = 0; it < n_items; ++it) {
+    const int fam = it >= per_t * ch[0];
+    const int bi = it - fam * per_t * ch[0];
+    const int ti = bi % per_t, c = bi / per_t;
+    const int vpc = (n_sel + ch[fam] - 1) / ch[fam];
+    const uint16_t* row = f.h_bp_cost.data() + (size_t)(fam * per_t + ti) * V_r;
+    long long sum = 0;
+    for (int k = c * vpc; k < std::min(n_sel, (c + 1) * vpc); ++k) sum += row[views[k]];
+    cost[it] = sum;
+  }
+  return upload_order(cost, out);
+}
+
+static int upload_fwd_order(const ms2g_plan* p, const FactorTables& f, const std::vector<int>& views, int vpb,
+                            int** out) {
+  const int n_sel = (int)views.size();
+  const int nbx = (p->B + 31) / 32, nby = (n_sel + vpb - 1) / vpb;
+  std::vector<long long> cost((size_t)nbx * nby, 0);
+  for (int by = 0; by < nby; ++by)
+    for (int k = by * vpb; k < std::min(n_sel, (by + 1) * vpb); ++k)
+      for (int bx = 0; bx < nbx; ++bx) cost[(size_t)by * nbx + bx] += f.h_fwd_cost[(size_t)views[k] * nbx + bx];
+  return upload_order(cost, out);
+}
+
 // Geometry plan: per-view and
 // per-ray constants computed in fp64 on the host, rounded once.
 static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
@@ -188,64 +233,45 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     if (ch < 1) ch = 1;
     f.bp_chunks[fam] = (int)ch;
   }
-  // Block order of full-view backprojections: longest (tile, view chunk)
-  // first (LPT).  Blocks start roughly in index order, so a launch of 2-3
-  // waves of uneven blocks (tiles outside the disk of the fan, families of a
-  // view shard) no longer ends on its longest blocks.  Cost = rays meeting the
-  // tile in the chunk, from the range table.
+  // Cost tables for the longest-first block orders (LPT): blocks start
+  // roughly in index order, so a launch of 2-3 waves of uneven blocks (tiles
+  // outside the disk of the fan, families of a view shard) no longer ends on
+  // its longest blocks.  Adjoint: rays meeting (tile, view), from the range
+  // table; forward: the longest ray column range of (view, 32-bin block).
   {
-    const int ntile = bp_tile_count(nc), per_t = ntile / 2;
+    const int ntile = bp_tile_count(nc);
     std::vector<int4> rt((size_t)ntile * V_r);
     MS2G_CUDA(cudaMemcpy(rt.data(), f.d_bpr, sizeof(int4) * rt.size(), cudaMemcpyDeviceToHost));
-    const int chx = f.bp_chunks[0], chy = f.bp_chunks[1];
-    const int n_items = per_t * (chx + chy);
-    std::vector<long long> cost(n_items, 0);
-    for (int it = 0; it < n_items; ++it) {
-      const int fam = it >= per_t * chx;
-      const int bi = it - fam * per_t * chx;
-      const int ti = bi % per_t, c = bi / per_t;
-      const int chf = fam ? chy : chx, vpc = (V_r + chf - 1) / chf;
-      const int4* row = rt.data() + (size_t)(fam * per_t + ti) * V_r;
-      long long sum = 0;
-      for (int v = c * vpc; v < std::min(V_r, (c + 1) * vpc); ++v) {
-        const int4 r = row[v];
-        const int nr = (r.z >> 16) & 0xff;
-        if (nr > 0) sum += (short)(r.x >> 16) - (r.x & 0xffff) + 1;
-        if (nr > 1) sum += (short)(r.y >> 16) - (r.y & 0xffff) + 1;
-      }
-      cost[it] = sum;
+    f.h_bp_cost.assign(rt.size(), 0);
+    for (size_t i = 0; i < rt.size(); ++i) {
+      const int4 r = rt[i];
+      const int nr = (r.z >> 16) & 0xff;
+      int sum = 0;
+      if (nr > 0) sum += (short)(r.x >> 16) - (r.x & 0xffff) + 1;
+      if (nr > 1) sum += (short)(r.y >> 16) - (r.y & 0xffff) + 1;
+      f.h_bp_cost[i] = (uint16_t)std::min(sum, 65535);
     }
-    std::vector<int> order(n_items);
-    for (int it = 0; it < n_items; ++it) order[it] = it;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-    MS2G_CUDA(cudaMalloc(&f.d_bp_order, sizeof(int) * n_items));
-    MS2G_CUDA(cudaMemcpy(f.d_bp_order, order.data(), sizeof(int) * n_items, cudaMemcpyHostToDevice));
-  }
-  // The same for the single-image forward: a block = 32 bins x vpb views,
-  // cost = sum over its warps of the longest ray's column range.
-  if (d.batch % 2 != 0) {
-    const int vpb = fwd_views_per_block(p, V_r, d.batch);
-    const int nbx = (B + 31) / 32, nby = (V_r + vpb - 1) / vpb;
-    std::vector<long long> cost((size_t)nbx * nby, 0);
-    for (int by = 0; by < nby; ++by)
-      for (int v = by * vpb; v < std::min(V_r, (by + 1) * vpb); ++v)
-        for (int bx = 0; bx < nbx; ++bx) {
-          int lo = INT_MAX, hi = INT_MIN;
-          for (int t = bx * 32; t < std::min(B, bx * 32 + 32); ++t) {
-            const RayEntry& R = rays[(size_t)v * B + t];
-            if (R.c_lo < R.c_hi) {
-              lo = std::min(lo, (int)R.c_lo);
-              hi = std::max(hi, (int)R.c_hi);
-            }
+    const int nbx = (B + 31) / 32;
+    f.h_fwd_cost.assign((size_t)V_r * nbx, 0);
+    for (int v = 0; v < V_r; ++v)
+      for (int bx = 0; bx < nbx; ++bx) {
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int t = bx * 32; t < std::min(B, bx * 32 + 32); ++t) {
+          const RayEntry& R = rays[(size_t)v * B + t];
+          if (R.c_lo < R.c_hi) {
+            lo = std::min(lo, (int)R.c_lo);
+            hi = std::max(hi, (int)R.c_hi);
           }
-          if (lo < hi) cost[(size_t)by * nbx + bx] += hi - lo;
         }
-    std::vector<int> order(cost.size());
-    for (size_t it = 0; it < order.size(); ++it) order[it] = (int)it;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-    MS2G_CUDA(cudaMalloc(&f.d_fwd_order, sizeof(int) * order.size()));
-    MS2G_CUDA(cudaMemcpy(f.d_fwd_order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
-    f.fwd_order_vpb = vpb;
+        f.h_fwd_cost[(size_t)v * nbx + bx] = (uint16_t)(lo < hi ? hi - lo : 0);
+      }
+  }
+  std::vector<int> all_views(V_r);
+  for (int v = 0; v < V_r; ++v) all_views[v] = v;
+  MS2G_TRY(upload_bp_order(p, f, all_views, &f.d_bp_order));
+  if (d.batch % 2 != 0) {
+    f.fwd_order_vpb = fwd_views_per_block(p, V_r, d.batch);
+    MS2G_TRY(upload_fwd_order(p, f, all_views, f.fwd_order_vpb, &f.d_fwd_order));
   }
   return MS2G_OK;
 }
@@ -258,6 +284,8 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(f.d_bpr);
     cudaFree(f.d_bp_order);
     cudaFree(f.d_fwd_order);
+    for (int* q : f.d_bp_order_sub) cudaFree(q);
+    for (int* q : f.d_fwd_order_sub) cudaFree(q);
     cudaFree(f.d_idx_down);
     cudaFree(f.d_w_down);
     cudaFree(f.d_idx_up);
@@ -344,13 +372,13 @@ static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
 // chunk reduction publishes straight into the exchange slot (fused, no
 // separate collective); otherwise backprojection then NCCL (or nothing).
 static int backward_sum(ms2g_plan* p, const FactorTables& f, const float* sino, float* G, float c, const int* d_sel,
-                        int n_sel, int batch, cudaStream_t st) {
+                        int n_sel, int batch, cudaStream_t st, const int* order_sel = nullptr) {
   const size_t count = (size_t)f.nc * f.nc * batch;
   if (p->peer_n > 0) {
-    MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st, 1));
+    MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st, 1, order_sel));
     return launch_peer_finish(p, G, count, st);
   }
-  MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st));
+  MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st, 0, order_sel));
   return allreduce(p, G, count, st);
 }
 
@@ -530,6 +558,21 @@ static int prepare_subsets(ms2g_plan* p, int n_subsets) {
   MS2G_CUDA(cudaMalloc(&p->w_subsets, sizeof(int) * (all.size() + 1)));
   if (!all.empty())
     MS2G_CUDA(cudaMemcpy(p->w_subsets, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice));
+  // longest-first block orders of every subset launch, per factor
+  for (auto& f : p->ft) {
+    for (int* q : f.d_bp_order_sub) cudaFree(q);
+    for (int* q : f.d_fwd_order_sub) cudaFree(q);
+    f.d_bp_order_sub.assign(n_subsets, nullptr);
+    f.d_fwd_order_sub.assign(n_subsets, nullptr);
+    for (int k = 0; k < n_subsets; ++k) {
+      if (p->subset_len[k] == 0) continue;
+      const std::vector<int> views(all.begin() + p->subset_off[k], all.begin() + p->subset_off[k] + p->subset_len[k]);
+      MS2G_TRY(upload_bp_order(p, f, views, &f.d_bp_order_sub[k]));
+      if (p->d.batch % 2 != 0)
+        MS2G_TRY(upload_fwd_order(p, f, views, fwd_views_per_block(p, (int)views.size(), p->d.batch),
+                                  &f.d_fwd_order_sub[k]));
+    }
+  }
   p->subsets_n = n_subsets;
   return MS2G_OK;
 }
@@ -642,14 +685,17 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
       for (int q = 0; q < sd->n_subsets; ++q) {
         float* ph = p->w_saga + (size_t)q * ncimg;
         const float cq = (float)((double)p->d.n_views / (double)p->subset_global_len[q]);
-        MS2G_TRY(launch_forward(p, *f, b, p->w_res, p->w_subsets + p->subset_off[q], p->subset_len[q], batch, st));
-        MS2G_TRY(backward_sum(p, *f, p->w_res, ph, cq, p->w_subsets + p->subset_off[q], p->subset_len[q], batch, st));
+        MS2G_TRY(launch_forward(p, *f, b, p->w_res, p->w_subsets + p->subset_off[q], p->subset_len[q], batch, st,
+                                f->d_fwd_order_sub[q]));
+        MS2G_TRY(backward_sum(p, *f, p->w_res, ph, cq, p->w_subsets + p->subset_off[q], p->subset_len[q], batch, st,
+                              f->d_bp_order_sub[q]));
         MS2G_TRY(launch_axpby(avg, avg, ph, 1.f, 1.f / (float)sd->n_subsets, ncimg, st));
       }
     }
     while (step < sch.size() && sch[step].stage == k) {
       const ms2g_sched_entry& e = sch[step];
       const int* d_sel = nullptr;
+      const int *ford = nullptr, *bord = nullptr;   // longest-first block orders of a subset launch
       int n_sel = p->V_r;
       float c = 1.f;
       if (sd->option == 4) {
@@ -660,6 +706,11 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
         d_sel = p->w_subsets + p->subset_off[e.subset];
         n_sel = p->subset_len[e.subset];
         c = (float)((double)p->d.n_views / (double)p->subset_global_len[e.subset]);
+        static const bool sub_off = getenv("MS2G_SUB_NO_ORDER") != nullptr;   // experiment switch
+        if ((int)f->d_bp_order_sub.size() == p->subsets_n && !sub_off) {
+          bord = f->d_bp_order_sub[e.subset];
+          ford = f->d_fwd_order_sub[e.subset];
+        }
       }
       // G-step: z = y - eta_k U (c A_s^T (A_s S y - b_M))       (Options 1, 2)
       //         z = y - eta_k U (c A_M^T A_M S (y - xs) + mu)  (Option 3, SVRG)
@@ -685,8 +736,8 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
           vd = p->w_v;
         }
         MS2G_TRY(launch_pair_prep(p, f->nc, batch, vd, st));
-        MS2G_TRY(launch_forward(p, *f, nullptr, p->w_res, d_sel, n_sel, batch, st));
-        MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st));
+        MS2G_TRY(launch_forward(p, *f, nullptr, p->w_res, d_sel, n_sel, batch, st, ford));
+        MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st, bord));
         MS2G_TRY(launch_axpby(p->w_G, p->w_G, p->w_mu, 1.f, 1.f, ncimg, st));  // + mu
       } else {
         const float* v = p->w_y;
@@ -695,8 +746,8 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
           v = p->w_v;
         }
         MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
-        MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st));
-        MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st));
+        MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st, ford));
+        MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st, bord));
         if (sd->option == 5)   // G = new - phi_j + avg; phi_j = new; avg += (new - phi_j)/K
           MS2G_TRY(launch_saga(p->w_G, p->w_saga + (size_t)e.subset * ncimg,
                                p->w_saga + (size_t)sd->n_subsets * ncimg, sd->n_subsets, ncimg, st));

@@ -311,11 +311,15 @@ static void fwd_launch_batch(int n_sel, int batch, cudaStream_t s, ms2g_plan* p,
 
 template <int NB, int SPLIT, int SEG>
 static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
-                        const int* d_sel, const float* b, float* out) {
+                        const int* d_sel, const float* b, float* out, const int* order_sel) {
   constexpr int VPB = kFwdWarps / SPLIT;
   dim3 grid((p->B + 31) / 32, (n_sel + VPB - 1) / VPB, batch / NB);
+  // longest-first block order: the plan's for full-view launches, the
+  // caller's (built for this view list with fwd_views_per_block) for subsets
   static const bool no_order = getenv("MS2G_FWD_NO_ORDER") != nullptr;   // experiment switch
-  const int* order = (!d_sel && n_sel == p->V_r && f.fwd_order_vpb == VPB && !no_order) ? f.d_fwd_order : nullptr;
+  const int* order = no_order ? nullptr
+                              : (d_sel ? order_sel
+                                       : ((n_sel == p->V_r && f.fwd_order_vpb == VPB) ? f.d_fwd_order : nullptr));
   k_forward<NB, SPLIT, SEG><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
                                                             p->pair_stride, f.nc, b, out, order);
 }
@@ -330,7 +334,7 @@ int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch) {
 }
 
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
-                   int batch, cudaStream_t s) {
+                   int batch, cudaStream_t s, const int* order_sel) {
   if (n_sel <= 0) return MS2G_OK;
   const int nb = (batch % 8 == 0) ? 8 : (batch % 4 == 0) ? 4 : (batch % 2 == 0) ? 2 : 1;
   const int slot = timing_begin(p, 0, f.factor, s);
@@ -344,8 +348,9 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
   if (nb == 8) fwd_launch_batch<8>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 4) fwd_launch_batch<4>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 2) fwd_launch_batch<2>(n_sel, batch, s, p, f, d_sel, b, out);
-  else if (fwd_views_per_block(p, n_sel, batch) != kFwdWarps) fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out);
-  else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out);
+  else if (fwd_views_per_block(p, n_sel, batch) != kFwdWarps)
+    fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+  else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
   const int rc = check_launch("k_forward");
   timing_end(p, slot, s);
   return rc;
@@ -668,27 +673,33 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
   return MS2G_OK;
 }
 
-int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
-                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish) {
-  const int H = bp_height(f.nc);
-  const BpTiling t = bp_tiling(f.nc, H);
-  int ch[2], vpc[2];
+// View chunks per tile family of a backprojection over n_sel views.  The
+// plan's chunking is for all V_r views; a view subset (Option 2, a minibatch)
+// keeps the views per chunk, not the chunk count: otherwise a 90-view subset
+// would be cut into 4-view chunks whose fixed cost (accumulator zeroing,
+// partial planes, their reduction) dominates.
+void bp_launch_chunks(const ms2g_plan* p, const FactorTables& f, int n_sel, int* ch) {
   for (int fam = 0; fam < 2; ++fam) {
-    // the plan's chunking is for all V_r views; a view subset (Option 2, a
-    // minibatch) keeps the views per chunk, not the chunk count: otherwise a
-    // 90-view subset would be cut into 4-view chunks whose fixed cost
-    // (accumulator zeroing, partial planes, their reduction) dominates
     ch[fam] = (int)(((long long)f.bp_chunks[fam] * n_sel + p->V_r - 1) / p->V_r);
     const int max_chunks = (n_sel + kBW - 1) / kBW;
     if (ch[fam] > max_chunks) ch[fam] = max_chunks;
     if (ch[fam] < 1) ch[fam] = 1;
-    vpc[fam] = (n_sel + ch[fam] - 1) / ch[fam];
   }
+}
+
+int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
+                    int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish,
+                    const int* order_sel) {
+  const int H = bp_height(f.nc);
+  const BpTiling t = bp_tiling(f.nc, H);
+  int ch[2], vpc[2];
+  bp_launch_chunks(p, f, n_sel, ch);
+  for (int fam = 0; fam < 2; ++fam) vpc[fam] = (n_sel + ch[fam] - 1) / ch[fam];
   dim3 grid(t.per * (ch[0] + ch[1]), 1, batch);
-  // the plan's longest-first block order holds for its own (full-view) chunking
+  // longest-first block order: the plan's for full-view launches, the
+  // caller's (built for this view list with bp_launch_chunks) for subsets
   static const bool no_order = getenv("MS2G_BP_NO_ORDER") != nullptr;    // experiment switch
-  const int* order = (!d_sel && n_sel == p->V_r && ch[0] == f.bp_chunks[0] && ch[1] == f.bp_chunks[1] && !no_order)
-                         ? f.d_bp_order : nullptr;
+  const int* order = no_order ? nullptr : (d_sel ? order_sel : (n_sel == p->V_r ? f.d_bp_order : nullptr));
   const int slot = timing_begin(p, 1, f.factor, s);
   if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
   else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));

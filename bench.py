@@ -213,10 +213,14 @@ def detail_512(P, dev):
                                          "subset_segments_per_s": 2 * nnz[f"{s_}_subset0"] / t_sub}
         x0 = torch.zeros_like(x); xo = torch.empty_like(x)
         kw = dict(option=2, n_subsets=8, seed=S.config_seed(3), den=pr3.den, alpha=pr3.alpha)
-        ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr3.stages, b, x0, xo, **kw), 3, warm=2)
+        ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr3.stages, b, x0, xo, **kw), 10, warm=3)
+        P.solve_status(plan)
+        tc = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr3.stages, b, x0, xo, power_iters=0, **kw), 10, warm=3)
         P.solve_status(plan)
         out["C3_512_solve"] = {"iters_per_s": pr3.n_steps / ts, "ms_per_solve": ts * 1e3,
-                               "schedule": "Option 2, 8 subsets, epochs [3,3,2] at s=4,2,1"}
+                               "cached_step_iters_per_s": pr3.n_steps / tc, "cached_step_ms_per_solve": tc * 1e3,
+                               "schedule": "Option 2, 8 subsets, epochs [3,3,2] at s=4,2,1 (3 x 20 power "
+                                           "iterations; cached_step: power_iters=0)"}
     nb = pr5.batch
     with P.plan_geometry(pr5.n, pr5.n_views, pr5.n_bins, factors=(2, 1), batch=nb) as plan:
         bs = []
@@ -228,7 +232,7 @@ def detail_512(P, dev):
         b = torch.from_numpy(np.stack(bs)).to(dev).contiguous()
         x0 = torch.zeros((nb, pr5.n, pr5.n), device=dev); xo = torch.empty_like(x0)
         kw = dict(den=pr5.den, alpha=pr5.alpha)
-        ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr5.stages, b, x0, xo, **kw), 3, warm=2)
+        ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr5.stages, b, x0, xo, **kw), 5, warm=2)
         P.solve_status(plan)
         out["C5_512_batch8_solve"] = {"image_iters_per_s": nb * pr5.n_steps / ts, "ms_per_solve": ts * 1e3,
                                       "images_per_solve": nb}

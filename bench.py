@@ -242,8 +242,9 @@ def detail_512(P, dev):
 def shard_estimate(P, dev, pr, b_full, t_solve_1):
     """Multi-GPU scaling ESTIMATE for view sharding (only one GPU
     here): the solve on rank 0's contiguous view shard [0, V/N) timed on this
-    GPU without a communicator (same kernels, 1/N of the views), plus a
-    modelled allreduce per gradient and per power iteration: 20 us latency +
+    GPU with a 1-rank NCCL communicator (same kernels and graph shape as an
+    N-rank run, 1/N of the views; the in-graph allreduce is an identity), plus
+    a modelled allreduce per gradient and per power iteration: 20 us latency +
     2 x bytes at 450 GB/s (NVLink 5 ring bus bandwidth, conservative vs NVLS).
     Not measured scaling: labelled estimated."""
     import torch
@@ -254,6 +255,9 @@ def shard_estimate(P, dev, pr, b_full, t_solve_1):
     for nr in (2, 4, 8):
         vb, ve = P.view_shard(pr.n_views, 0, nr)
         with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve) as plan:
+            # a 1-rank communicator: the graph then has the N-rank run's shape
+            # (in-graph allreduce nodes, power iterations serial on one stream)
+            P.attach_nccl(plan, 0, 1)
             b = torch.from_numpy(np.ascontiguousarray(b_full[vb:ve])).to(dev)[None].contiguous()
             x0 = torch.zeros((1, pr.n, pr.n), device=dev); xo = torch.empty_like(x0)
             kw = dict(den=pr.den, alpha=pr.alpha, power_iters=pr.power_iters)

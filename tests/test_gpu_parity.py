@@ -718,3 +718,24 @@ def test_geometry_variants(P, kw):
         xo = host(P.pnp_ms2g_solve(plan, stages, dev(b)[None], den=("tv", 0.02, 10), alpha=1.0))[0]
     xr, _, _ = O.pnp_ms2g(g, stages, b, den=("tv", 0.02, 10), alpha=1.0)
     assert rel(xo, xr) <= TOL_SOLVE
+
+
+def test_solve_repeated_factors_and_serial_equivalence(P):
+    """A schedule that returns to a factor (coarse -> full -> coarse): the
+    concurrent power-iteration branches serve every stage of a factor, and the
+    solve matches the oracle; a plan with a 1-rank communicator (serial power
+    iterations on one stream) gives the same iterate bit for bit."""
+    pr = S.PRESETS[1]
+    g, xt, b = _make_data(pr, 1)
+    stages = [(2, 3, 0), (1, 2, 0), (2, 2, 0), (1, 1, 0)]
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1)) as a, \
+            P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1)) as c:
+        P.attach_nccl(c, 0, 1)
+        xa, ta = P.pnp_ms2g_solve(a, stages, dev(b)[None], den=pr.den, alpha=pr.alpha, trace=True)
+        xc, tc = P.pnp_ms2g_solve(c, stages, dev(b)[None], den=pr.den, alpha=pr.alpha, trace=True)
+        assert torch.equal(xa, xc)
+        assert ta == tc
+    xr, trr, _ = O.pnp_ms2g(g, stages, b, den=pr.den, alpha=pr.alpha)
+    assert rel(host(xa)[0], xr) <= TOL_SOLVE
+    for e, er in zip(ta, trr):
+        assert e[:4] == er[:4] and abs(e[4] - er[4]) <= 1e-5 * er[4]

@@ -241,7 +241,8 @@ def detail_512(P, dev):
 
 def shard_estimate(P, dev, pr, b_full, t_solve_1):
     """Multi-GPU scaling ESTIMATE for view sharding (only one GPU
-    here): the solve on rank 0's contiguous view shard [0, V/N) timed on this
+    here): the solve on every rank's contiguous view shard, the slowest of
+    them (SURVEY: "max shard time") timed on this
     GPU with a 1-rank NCCL communicator (same kernels and graph shape as an
     N-rank run, 1/N of the views; the in-graph allreduce is an identity), plus
     a modelled allreduce per gradient and per power iteration: 20 us latency +
@@ -253,23 +254,28 @@ def shard_estimate(P, dev, pr, b_full, t_solve_1):
             1: pr.power_iters + sum(s_[1] for s_ in pr.stages if s_[0] == 1)}
     t_ar = sum(n * (20e-6 + 2 * 4 * (pr.n // f) ** 2 / 450e9) for f, n in n_ar.items())
     for nr in (2, 4, 8):
-        vb, ve = P.view_shard(pr.n_views, 0, nr)
-        with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve) as plan:
-            # a 1-rank communicator: the graph then has the N-rank run's shape
-            # (in-graph allreduce nodes, power iterations serial on one stream)
-            P.attach_nccl(plan, 0, 1)
-            b = torch.from_numpy(np.ascontiguousarray(b_full[vb:ve])).to(dev)[None].contiguous()
-            x0 = torch.zeros((1, pr.n, pr.n), device=dev); xo = torch.empty_like(x0)
-            kw = dict(den=pr.den, alpha=pr.alpha, power_iters=pr.power_iters)
-            ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr.stages, b, x0, xo, **kw), 3, warm=2)
-            try:
-                P.solve_status(plan)
-            except P.MS2GError:
-                pass      # a shard's partial operator alone may drive the toy iterate anywhere; timing only
+        shard_ms = []
+        for r in range(nr):          # every rank's shard; the slowest sets the pace
+            vb, ve = P.view_shard(pr.n_views, r, nr)
+            with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve) as plan:
+                # a 1-rank communicator: the graph then has the N-rank run's shape
+                # (in-graph allreduce nodes, power iterations serial on one stream)
+                P.attach_nccl(plan, 0, 1)
+                b = torch.from_numpy(np.ascontiguousarray(b_full[vb:ve])).to(dev)[None].contiguous()
+                x0 = torch.zeros((1, pr.n, pr.n), device=dev); xo = torch.empty_like(x0)
+                kw = dict(den=pr.den, alpha=pr.alpha, power_iters=pr.power_iters)
+                shard_ms.append(1e3 * time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr.stages, b, x0, xo, **kw),
+                                                 3, warm=2))
+                try:
+                    P.solve_status(plan)
+                except P.MS2GError:
+                    pass      # a shard's partial operator alone may drive the toy iterate anywhere; timing only
+        ts = max(shard_ms) / 1e3
         t = ts + t_ar
-        out[f"N{nr}"] = {"shard_solve_ms": ts * 1e3, "allreduce_model_ms": t_ar * 1e3,
-                         "est_iters_per_s": pr.n_steps / t, "est_speedup": t_solve_1 / t}
-    out["note"] = ("estimated: rank-0 shard timed on 1 GPU (L2 not flushed) + modelled allreduce; "
+        out[f"N{nr}"] = {"max_shard_solve_ms": ts * 1e3, "shard_solve_ms": [round(v, 3) for v in shard_ms],
+                         "allreduce_model_ms": t_ar * 1e3, "est_iters_per_s": pr.n_steps / t,
+                         "est_speedup": t_solve_1 / t}
+    out["note"] = ("estimated: slowest rank shard timed on 1 GPU (L2 not flushed) + modelled allreduce; "
                    "not measured scaling")
     return out
 

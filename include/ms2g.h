@@ -15,10 +15,12 @@
  *      compacted [batch][n_sel][B] (views selected by a subset, ascending order)
  *  - `stream` is a cudaStream_t passed as void*.  Every call is asynchronous
  *    and ordered on that stream, except where "synchronous" is stated.
- *  - A plan is used by one host thread at a time.  No call allocates device
- *    memory after ms2g_plan_geometry / ms2g_attach_nccl / ms2g_attach_peers
- *    (except a first Option-5 solve's SAGA table, allocated before capture),
- *    so sequences of calls are CUDA-graph capturable.
+ *  - A plan is used by one host thread at a time.  Device memory is
+ *    allocated by ms2g_plan_geometry / ms2g_attach_nccl / ms2g_attach_peers
+ *    and, on a solve description's first use, before its graph is captured
+ *    (Option-5 table, power-iteration branch workspaces, subset block
+ *    orders); the per-operator calls never allocate, so sequences of them
+ *    are CUDA-graph capturable.
  *  - Configuration errors are detected on the host before any launch.
  */
 #ifndef MS2G_H

@@ -272,10 +272,10 @@ __global__ void k_tv_iter(const float* __restrict__ f, const float* __restrict__
     float qx = 0.f, qy = 0.f;
     if (j < n - 1) qx = (tv_div(px, py, n, i, j + 1) - fb[p + 1] * inv_lambda) - wc;
     if (i < n - 1) qy = (tv_div(px, py, n, i + 1, j) - fb[p + n] * inv_lambda) - wc;
-    const float den = 1.f + tau * sqrtf(qx * qx + qy * qy);
+    const float rden = 1.f / (1.f + tau * sqrtf(qx * qx + qy * qy));   // one division for both components
     float* ox = pout + b * 2 * np;
-    ox[p] = (px[p] + tau * qx) / den;
-    ox[np + p] = (py[p] + tau * qy) / den;
+    ox[p] = (px[p] + tau * qx) * rden;
+    ox[np + p] = (py[p] + tau * qy) * rden;
   }
 }
 

@@ -66,3 +66,52 @@ def test_fuzz_operators():
                                  subset=sub).cpu().numpy()
             ref = O.sketched_grad(g, s, x[0], b[0], views=sub)
             assert rel(gg[0], ref) <= TOL, ("grad", c, n, V, B, factors, batch, s, rel(gg[0], ref))
+
+
+def _solve_case(rng):
+    n = int(rng.choice([16, 24, 32, 48, 64]))
+    facs = [f for f in (4, 3, 2) if n % f == 0]
+    V = int(rng.integers(8, 61))
+    B = 2 * int(rng.integers(n // 2, n + 8))
+    option = int(rng.choice([1, 2, 3, 4, 5]))
+    k = int(rng.integers(1, 4))
+    stage_f = sorted(rng.choice(facs + [1], size=k, replace=True).tolist(), reverse=True)
+    if option in (2, 3, 5):
+        n_sub = int(rng.integers(2, min(8, V) + 1))
+        stages = [(int(f), 0, int(rng.integers(1, 3))) for f in stage_f]
+    else:
+        n_sub = int(rng.integers(2, V + 1)) if option == 4 else 1
+        stages = [(int(f), int(rng.integers(1, 5)), 0) for f in stage_f]
+    den = [("identity",), ("gauss", 0.8), ("tv", 0.02, 5)][int(rng.integers(0, 3))]
+    alpha = 1.0 if den[0] != "gauss" else 0.5
+    batch = int(rng.choice([1, 1, 2, 3]))
+    return n, V, B, stages, option, n_sub, den, alpha, batch
+
+
+def test_fuzz_solves():
+    """Random schedules (1-3 stages, factors 1-4, repeated factors), all five
+    options, the three denoisers, batches: the solve against the oracle's
+    Algorithm 1 and the schedule bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2203_07308_b200 as P
+    P.load()
+    rng = np.random.default_rng(7)
+    cases = int(os.environ.get("MS2G_FUZZ_SOLVES", "6"))
+    for c in range(cases):
+        n, V, B, stages, option, n_sub, den, alpha, batch = _solve_case(rng)
+        g = O.Geometry(n, V, B)
+        factors = sorted({s[0] for s in stages} | {1}, reverse=True)
+        xt = [S.phantom(n, 5, 4000 * c + i) for i in range(batch)]
+        bs = np.stack([O.forward(g, 1, x) for x in xt]).astype(np.float32)
+        seed = int(rng.integers(0, 2 ** 31))
+        with P.plan_geometry(n, V, B, factors=tuple(factors), batch=batch) as plan:
+            xo, tr = P.pnp_ms2g_solve(plan, stages, torch.from_numpy(bs).cuda(), option=option, n_subsets=n_sub,
+                                      seed=seed, den=den, alpha=alpha, trace=True)
+            xo = xo.cpu().numpy()
+        for i in (0, batch - 1):
+            xr, trr, _ = O.pnp_ms2g(g, stages, bs[i], option=option, n_subsets=n_sub, seed=seed, den=den,
+                                    alpha=alpha)
+            assert [e[:4] for e in tr] == [e[:4] for e in trr], ("schedule", c)
+            assert rel(xo[i], xr) <= 1e-3, ("solve", c, n, V, B, stages, option, n_sub, den, batch,
+                                            rel(xo[i], xr))

@@ -2,7 +2,8 @@
 
 Every step of the PnP-MS2G hot path runs in the hand-written sm_100a kernels of
 libms2g; PyTorch supplies device memory, the current stream and (for the
-multi-GPU view sharding) the process group used to broadcast the NCCL id.
+multi-GPU view sharding) the process group used to broadcast the NCCL id or
+gather the NVLink peer handles (NEXT-3).
 There is no CPU fallback: without the built library or a CUDA device every
 call raises.
 """
@@ -16,8 +17,9 @@ import torch
 
 __all__ = [
     "MS2GError", "DivergedError", "Plan", "plan_geometry", "forward_project", "back_project", "sketch_down",
-    "sketch_up", "sketched_grad", "power_iteration", "denoise", "schedule", "pnp_ms2g_solve",
-    "pnp_ms2g_solve_async", "attach_nccl", "launch_count", "lib_path", "load",
+    "sketch_up", "sketched_grad", "power_iteration", "denoise", "schedule", "schedule_views", "pnp_ms2g_solve",
+    "pnp_ms2g_solve_async", "solve_status", "attach_nccl", "attach_peers", "view_shard", "set_kernel_timing",
+    "kernel_time", "launch_count", "lib_path", "load",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -216,7 +218,8 @@ def forward_project(plan: Plan, factor: int, x, b=None, subset=None, out=None):
 
 def back_project(plan: Plan, factor: int, sino, img=None, scale=1.0, accumulate=False, subset=None,
                  allreduce=False):
-    """img = scale A_s^T sino (+img if accumulate); allreduce over NCCL ranks."""
+    """img = scale A_s^T sino (+img if accumulate); allreduce: sum over the
+    ranks attached by attach_nccl / attach_peers."""
     sel, m = _subset(subset)
     nc = plan.nc(factor)
     if img is None:
@@ -262,6 +265,8 @@ def sketched_grad(plan: Plan, factor: int, x, b, g=None, subset=None, resampler=
 
 
 def power_iteration(plan: Plan, factor: int, iters: int = 20) -> float:
+    """L = <v, A_s^T A_s v> after `iters` normalised steps from 1/||1|| (P:156,
+    reading Z5/Z6); also refreshes the plan's cached step for the factor."""
     L = C.c_double(0.0)
     _check(load().ms2g_power_iteration(plan.handle, factor, iters, C.byref(L), _stream()))
     return L.value

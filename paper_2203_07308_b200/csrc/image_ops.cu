@@ -258,8 +258,9 @@ __device__ __forceinline__ float tv_div(const float* __restrict__ px, const floa
   return a + b;
 }
 
+// first != 0: p^0 = 0 (no warm start, no read of pin): div p = 0
 __global__ void k_tv_iter(const float* __restrict__ f, const float* __restrict__ pin, float* __restrict__ pout,
-                          int n, float inv_lambda, float tau, size_t total) {
+                          int n, float inv_lambda, float tau, size_t total, int first) {
   const size_t np = (size_t)n * n;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
        idx += (size_t)gridDim.x * blockDim.x) {
@@ -268,14 +269,14 @@ __global__ void k_tv_iter(const float* __restrict__ f, const float* __restrict__
     const float* fb = f + b * np;
     const float* px = pin + b * 2 * np;
     const float* py = px + np;
-    const float wc = tv_div(px, py, n, i, j) - fb[p] * inv_lambda;
+    const float wc = (first ? 0.f : tv_div(px, py, n, i, j)) - fb[p] * inv_lambda;
     float qx = 0.f, qy = 0.f;
-    if (j < n - 1) qx = (tv_div(px, py, n, i, j + 1) - fb[p + 1] * inv_lambda) - wc;
-    if (i < n - 1) qy = (tv_div(px, py, n, i + 1, j) - fb[p + n] * inv_lambda) - wc;
+    if (j < n - 1) qx = ((first ? 0.f : tv_div(px, py, n, i, j + 1)) - fb[p + 1] * inv_lambda) - wc;
+    if (i < n - 1) qy = ((first ? 0.f : tv_div(px, py, n, i + 1, j)) - fb[p + n] * inv_lambda) - wc;
     const float rden = 1.f / (1.f + tau * sqrtf(qx * qx + qy * qy));   // one division for both components
     float* ox = pout + b * 2 * np;
-    ox[p] = (px[p] + tau * qx) * rden;
-    ox[np + p] = (py[p] + tau * qy) * rden;
+    ox[p] = ((first ? 0.f : px[p]) + tau * qx) * rden;
+    ox[np + p] = ((first ? 0.f : py[p]) + tau * qy) * rden;
   }
 }
 
@@ -340,11 +341,12 @@ int launch_tv(int n, int batch, float lambda, float tau, int iters, const float*
   if (lambda == 0.f) {  // prox of the zero function: identity
     return launch_copy_mix_mom(n, batch, f, xprev, xout, yout, a, mode, flag, iter, st);
   }
-  MS2G_TRY(launch_fill(p0, 2 * total, 0.f, st));  // p^0 = 0 at every call (no warm start)
+  // p^0 = 0 at every call (no warm start): the first iteration does not read p
+  if (iters < 1) MS2G_TRY(launch_fill(p0, 2 * total, 0.f, st));
   float* pin = p0;
   float* pout = p1;
   for (int k = 0; k < iters; ++k) {
-    k_tv_iter<<<grid1d(total), 256, 0, st>>>(f, pin, pout, n, 1.f / lambda, tau, total);
+    k_tv_iter<<<grid1d(total), 256, 0, st>>>(f, pin, pout, n, 1.f / lambda, tau, total, k == 0);
     MS2G_TRY(check_launch("k_tv_iter"));
     float* tmp = pin;
     pin = pout;

@@ -12,6 +12,19 @@
 
 namespace ms2g {
 
+// Pixel kernels run on a (32 x 8)-thread block over a (columns, rows, batch)
+// grid: the pixel comes from the block/thread indices, no index division
+// (64-bit / and % of a flat index cost more than the pixel's arithmetic).
+static inline dim3 px_grid(int cols, int rows, int batch) {
+  return dim3((unsigned)((cols + 31) / 32), (unsigned)((rows + 7) / 8), (unsigned)batch);
+}
+static const dim3 kPxBlock(32, 8);
+#define PIXEL_IJB(rows, cols)                              \
+  const int j = blockIdx.x * 32 + threadIdx.x;             \
+  const int i = blockIdx.y * 8 + threadIdx.y;              \
+  const size_t b = blockIdx.z;                             \
+  if (i >= (rows) || j >= (cols)) return
+
 static inline int grid1d(size_t total, int block = 256, int cap = 148 * 32) {
   size_t g = (total + block - 1) / block;
   if (g > (size_t)cap) g = cap;
@@ -21,28 +34,21 @@ static inline int grid1d(size_t total, int block = 256, int cap = 148 * 32) {
 
 // -------------------------------------------------------------- sketch --
 // S_s: s x s average pool (north-star D; BASELINE configs "2x2 average pool").
-__global__ void k_sketch_down(const float* __restrict__ x, float* __restrict__ v, int n, int s, int nc,
-                              size_t total) {
+__global__ void k_sketch_down(const float* __restrict__ x, float* __restrict__ v, int n, int s, int nc) {
+  PIXEL_IJB(nc, nc);
   const float inv = 1.0f / (float)(s * s);
-  const size_t np = (size_t)nc * nc;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = idx / np, p = idx % np;
-    const int I = (int)(p / nc), J = (int)(p % nc);
-    const float* xb = x + b * n * n;
-    float acc = 0.f;
-    for (int a = 0; a < s; ++a) {
-      const float* row = xb + (size_t)(s * I + a) * n + (size_t)s * J;
-      for (int c = 0; c < s; ++c) acc += row[c];
-    }
-    v[idx] = (s == 1) ? acc : acc * inv;
+  const float* xb = x + b * n * n;
+  float acc = 0.f;
+  for (int a = 0; a < s; ++a) {
+    const float* row = xb + (size_t)(s * i + a) * n + (size_t)s * j;
+    for (int c = 0; c < s; ++c) acc += row[c];
   }
+  v[(b * nc + i) * nc + j] = (s == 1) ? acc : acc * inv;
 }
 
 int launch_sketch_down(int n, int s, int batch, const float* x, float* v, cudaStream_t st) {
   const int nc = n / s;
-  const size_t total = (size_t)nc * nc * batch;
-  k_sketch_down<<<grid1d(total), 256, 0, st>>>(x, v, n, s, nc, total);
+  k_sketch_down<<<px_grid(nc, nc, batch), kPxBlock, 0, st>>>(x, v, n, s, nc);
   return check_launch("k_sketch_down");
 }
 
@@ -50,22 +56,17 @@ int launch_sketch_down(int n, int s, int batch, const float* x, float* v, cudaSt
 // z = y - eta * U_s g, U_s = nearest replication (reading Z2).
 __global__ void k_up_step(const float* __restrict__ g, const float* __restrict__ y,
                           const float* __restrict__ eta_dev, float eta, float* __restrict__ z, int n, int s,
-                          int nc, size_t total) {
+                          int nc) {
+  PIXEL_IJB(n, n);
   const float e = eta_dev ? *eta_dev : eta;
-  const size_t np = (size_t)n * n;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = idx / np, p = idx % np;
-    const int i = (int)(p / n), j = (int)(p % n);
-    const float gv = g[b * nc * nc + (size_t)(i / s) * nc + (j / s)];
-    z[idx] = y ? (y[idx] - e * gv) : gv;
-  }
+  const size_t idx = (b * n + i) * n + j;
+  const float gv = g[(b * nc + i / s) * nc + (j / s)];
+  z[idx] = y ? (y[idx] - e * gv) : gv;
 }
 
 int launch_up_step(int n, int s, int batch, const float* g, const float* y, const float* eta_dev, float eta,
                    float* z, cudaStream_t st) {
-  const size_t total = (size_t)n * n * batch;
-  k_up_step<<<grid1d(total), 256, 0, st>>>(g, y, eta_dev, eta, z, n, s, n / s, total);
+  k_up_step<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(g, y, eta_dev, eta, z, n, s, n / s);
   return check_launch("k_up_step");
 }
 
@@ -124,45 +125,37 @@ int build_bicubic_tables(FactorTables& f, int n) {
 
 // rows pass: out[b][r][o] = sum_t w[o][t] in[b][r][idx[o][t]]   (rows x n_in -> rows x n_out)
 __global__ void k_rs_rows(const float* __restrict__ in, float* __restrict__ out, int rows, int n_in, int n_out,
-                          int taps, const int* __restrict__ idx, const float* __restrict__ w, size_t total) {
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-    const int o = (int)(e % n_out);
-    const size_t br = e / n_out;           // b * rows + r
-    const float* row = in + br * n_in;
-    float acc = 0.f;
-    for (int t = 0; t < taps; ++t) acc = fmaf(__ldg(w + o * taps + t), row[__ldg(idx + o * taps + t)], acc);
-    out[e] = acc;
-  }
+                          int taps, const int* __restrict__ idx, const float* __restrict__ w) {
+  PIXEL_IJB(rows, n_out);                      // i = input row r, j = output sample o
+  const float* row = in + (b * rows + i) * n_in;
+  float acc = 0.f;
+  for (int t = 0; t < taps; ++t) acc = fmaf(__ldg(w + j * taps + t), row[__ldg(idx + j * taps + t)], acc);
+  out[(b * rows + i) * n_out + j] = acc;
 }
 
 // columns pass: val = sum_t w[o][t] in[b][idx[o][t]][c]; z = y - eta val (y != NULL) or val
 __global__ void k_rs_cols(const float* __restrict__ in, float* __restrict__ out, int cols, int n_in, int n_out,
                           int taps, const int* __restrict__ idx, const float* __restrict__ w,
-                          const float* __restrict__ y, const float* __restrict__ eta_dev, float eta, size_t total) {
+                          const float* __restrict__ y, const float* __restrict__ eta_dev, float eta) {
+  PIXEL_IJB(n_out, cols);                      // i = output row o, j = column c
   const float e_ = eta_dev ? *eta_dev : eta;
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % cols);
-    const size_t bo = e / cols;
-    const int o = (int)(bo % n_out);
-    const size_t b = bo / n_out;
-    const float* base = in + b * (size_t)n_in * cols + c;
-    float acc = 0.f;
-    for (int t = 0; t < taps; ++t)
-      acc = fmaf(__ldg(w + o * taps + t), base[(size_t)__ldg(idx + o * taps + t) * cols], acc);
-    out[e] = y ? y[e] - e_ * acc : acc;
-  }
+  const float* base = in + b * (size_t)n_in * cols + j;
+  float acc = 0.f;
+  for (int t = 0; t < taps; ++t)
+    acc = fmaf(__ldg(w + i * taps + t), base[(size_t)__ldg(idx + i * taps + t) * cols], acc);
+  const size_t e = (b * n_out + i) * cols + j;
+  out[e] = y ? y[e] - e_ * acc : acc;
 }
 
 int launch_resample_down(ms2g_plan* p, const FactorTables& f, int kind, int batch, const float* x, float* v,
                          cudaStream_t st) {
   const int n = p->d.n;
   if (kind == 0 || f.factor == 1) return launch_sketch_down(n, f.factor, batch, x, v, st);
-  const size_t t1 = (size_t)batch * n * f.nc;
-  k_rs_rows<<<grid1d(t1), 256, 0, st>>>(x, p->w_rs, n, n, f.nc, f.taps_down, f.d_idx_down, f.d_w_down, t1);
+  k_rs_rows<<<px_grid(f.nc, n, batch), kPxBlock, 0, st>>>(x, p->w_rs, n, n, f.nc, f.taps_down, f.d_idx_down,
+                                                          f.d_w_down);
   MS2G_TRY(check_launch("k_rs_rows"));
-  const size_t t2 = (size_t)batch * f.nc * f.nc;
-  k_rs_cols<<<grid1d(t2), 256, 0, st>>>(p->w_rs, v, f.nc, n, f.nc, f.taps_down, f.d_idx_down, f.d_w_down,
-                                        nullptr, nullptr, 0.f, t2);
+  k_rs_cols<<<px_grid(f.nc, f.nc, batch), kPxBlock, 0, st>>>(p->w_rs, v, f.nc, n, f.nc, f.taps_down, f.d_idx_down,
+                                                             f.d_w_down, nullptr, nullptr, 0.f);
   return check_launch("k_rs_cols");
 }
 
@@ -170,12 +163,11 @@ int launch_resample_up_step(ms2g_plan* p, const FactorTables& f, int kind, int b
                             const float* y, const float* eta_dev, float eta, float* z, cudaStream_t st) {
   const int n = p->d.n;
   if (kind == 0 || f.factor == 1) return launch_up_step(n, f.factor, batch, g, y, eta_dev, eta, z, st);
-  const size_t t1 = (size_t)batch * f.nc * n;
-  k_rs_rows<<<grid1d(t1), 256, 0, st>>>(g, p->w_rs, f.nc, f.nc, n, f.taps_up, f.d_idx_up, f.d_w_up, t1);
+  k_rs_rows<<<px_grid(n, f.nc, batch), kPxBlock, 0, st>>>(g, p->w_rs, f.nc, f.nc, n, f.taps_up, f.d_idx_up,
+                                                          f.d_w_up);
   MS2G_TRY(check_launch("k_rs_rows"));
-  const size_t t2 = (size_t)batch * n * n;
-  k_rs_cols<<<grid1d(t2), 256, 0, st>>>(p->w_rs, z, n, f.nc, n, f.taps_up, f.d_idx_up, f.d_w_up, y, eta_dev, eta,
-                                        t2);
+  k_rs_cols<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(p->w_rs, z, n, f.nc, n, f.taps_up, f.d_idx_up, f.d_w_up, y,
+                                                       eta_dev, eta);
   return check_launch("k_rs_cols");
 }
 
@@ -200,32 +192,29 @@ __device__ __forceinline__ void mix_momentum(size_t idx, float zv, float dv, con
 // replicate boundary, rows then columns.
 __global__ void k_gauss_mm(const float* __restrict__ z, const float* __restrict__ xprev, float* __restrict__ xout,
                            float* __restrict__ yout, int n, float w0, float w1, float alpha, float a, int mode,
-                           int* flag, int iter, size_t total) {
+                           int* flag, int iter) {
+  PIXEL_IJB(n, n);
   const size_t np = (size_t)n * n;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = idx / np, p = idx % np;
-    const int i = (int)(p / n), j = (int)(p % n);
-    const float* zb = z + b * np;
-    const int jl = max(j - 1, 0), jr = min(j + 1, n - 1);
-    float t[3];
+  const float* zb = z + b * np;
+  const int jl = max(j - 1, 0), jr = min(j + 1, n - 1);
+  float t[3];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int r = min(max(i + q - 1, 0), n - 1);
-      const float* row = zb + (size_t)r * n;
-      t[q] = w1 * row[jl] + w0 * row[j] + w1 * row[jr];
-    }
-    const float dv = w1 * t[0] + w0 * t[1] + w1 * t[2];
-    mix_momentum(idx, zb[p], dv, xprev, xout, yout, alpha, a, mode, flag, iter);
+  for (int q = 0; q < 3; ++q) {
+    const int r = min(max(i + q - 1, 0), n - 1);
+    const float* row = zb + (size_t)r * n;
+    t[q] = w1 * row[jl] + w0 * row[j] + w1 * row[jr];
   }
+  const float dv = w1 * t[0] + w0 * t[1] + w1 * t[2];
+  const size_t p = (size_t)i * n + j;
+  mix_momentum(b * np + p, zb[p], dv, xprev, xout, yout, alpha, a, mode, flag, iter);
 }
 
 int launch_gauss_mix_mom(int n, int batch, float sigma, const float* z, const float* xprev, float* xout,
                          float* yout, float alpha, float a, int mode, int* flag, int iter, cudaStream_t st) {
   const double e = exp(-1.0 / (2.0 * (double)sigma * (double)sigma));
   const float w1 = (float)(e / (1.0 + 2.0 * e)), w0 = (float)(1.0 / (1.0 + 2.0 * e));
-  const size_t total = (size_t)n * n * batch;
-  k_gauss_mm<<<grid1d(total), 256, 0, st>>>(z, xprev, xout, yout, n, w0, w1, alpha, a, mode, flag, iter, total);
+  k_gauss_mm<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(z, xprev, xout, yout, n, w0, w1, alpha, a, mode, flag,
+                                                        iter);
   return check_launch("k_gauss_mm");
 }
 
@@ -260,39 +249,31 @@ __device__ __forceinline__ float tv_div(const float* __restrict__ px, const floa
 
 // first != 0: p^0 = 0 (no warm start, no read of pin): div p = 0
 __global__ void k_tv_iter(const float* __restrict__ f, const float* __restrict__ pin, float* __restrict__ pout,
-                          int n, float inv_lambda, float tau, size_t total, int first) {
-  const size_t np = (size_t)n * n;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = idx / np, p = idx % np;
-    const int i = (int)(p / n), j = (int)(p % n);
-    const float* fb = f + b * np;
-    const float* px = pin + b * 2 * np;
-    const float* py = px + np;
-    const float wc = (first ? 0.f : tv_div(px, py, n, i, j)) - fb[p] * inv_lambda;
-    float qx = 0.f, qy = 0.f;
-    if (j < n - 1) qx = ((first ? 0.f : tv_div(px, py, n, i, j + 1)) - fb[p + 1] * inv_lambda) - wc;
-    if (i < n - 1) qy = ((first ? 0.f : tv_div(px, py, n, i + 1, j)) - fb[p + n] * inv_lambda) - wc;
-    const float rden = 1.f / (1.f + tau * sqrtf(qx * qx + qy * qy));   // one division for both components
-    float* ox = pout + b * 2 * np;
-    ox[p] = ((first ? 0.f : px[p]) + tau * qx) * rden;
-    ox[np + p] = ((first ? 0.f : py[p]) + tau * qy) * rden;
-  }
+                          int n, float inv_lambda, float tau, int first) {
+  PIXEL_IJB(n, n);
+  const size_t np = (size_t)n * n, p = (size_t)i * n + j;
+  const float* fb = f + b * np;
+  const float* px = pin + b * 2 * np;
+  const float* py = px + np;
+  const float wc = (first ? 0.f : tv_div(px, py, n, i, j)) - fb[p] * inv_lambda;
+  float qx = 0.f, qy = 0.f;
+  if (j < n - 1) qx = ((first ? 0.f : tv_div(px, py, n, i, j + 1)) - fb[p + 1] * inv_lambda) - wc;
+  if (i < n - 1) qy = ((first ? 0.f : tv_div(px, py, n, i + 1, j)) - fb[p + n] * inv_lambda) - wc;
+  const float rden = 1.f / (1.f + tau * sqrtf(qx * qx + qy * qy));   // one division for both components
+  float* ox = pout + b * 2 * np;
+  ox[p] = ((first ? 0.f : px[p]) + tau * qx) * rden;
+  ox[np + p] = ((first ? 0.f : py[p]) + tau * qy) * rden;
 }
 
 __global__ void k_tv_final(const float* __restrict__ f, const float* __restrict__ pin,
                            const float* __restrict__ xprev, float* __restrict__ xout, float* __restrict__ yout,
-                           int n, float lambda, float alpha, float a, int mode, int* flag, int iter, size_t total) {
-  const size_t np = (size_t)n * n;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = idx / np, p = idx % np;
-    const int i = (int)(p / n), j = (int)(p % n);
-    const float* px = pin + b * 2 * np;
-    const float fv = f[idx];
-    const float u = fv - lambda * tv_div(px, px + np, n, i, j);
-    mix_momentum(idx, fv, u, xprev, xout, yout, alpha, a, mode, flag, iter);
-  }
+                           int n, float lambda, float alpha, float a, int mode, int* flag, int iter) {
+  PIXEL_IJB(n, n);
+  const size_t np = (size_t)n * n, idx = b * np + (size_t)i * n + j;
+  const float* px = pin + b * 2 * np;
+  const float fv = f[idx];
+  const float u = fv - lambda * tv_div(px, px + np, n, i, j);
+  mix_momentum(idx, fv, u, xprev, xout, yout, alpha, a, mode, flag, iter);
 }
 
 // out = a x + b y  (SVRG difference / correction, NEXT-4)
@@ -346,14 +327,14 @@ int launch_tv(int n, int batch, float lambda, float tau, int iters, const float*
   float* pin = p0;
   float* pout = p1;
   for (int k = 0; k < iters; ++k) {
-    k_tv_iter<<<grid1d(total), 256, 0, st>>>(f, pin, pout, n, 1.f / lambda, tau, total, k == 0);
+    k_tv_iter<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(f, pin, pout, n, 1.f / lambda, tau, k == 0);
     MS2G_TRY(check_launch("k_tv_iter"));
     float* tmp = pin;
     pin = pout;
     pout = tmp;
   }
-  k_tv_final<<<grid1d(total), 256, 0, st>>>(f, pin, xprev, xout, yout, n, lambda, alpha, a, mode, flag, iter,
-                                            total);
+  k_tv_final<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(f, pin, xprev, xout, yout, n, lambda, alpha, a, mode, flag,
+                                                        iter);
   return check_launch("k_tv_final");
 }
 

@@ -37,16 +37,18 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 
 // scale * (sum of nplanes partial planes) -> the local exchange slot of the
 // NEXT epoch (fused publish of the backprojection).
-__global__ void k_chunk_reduce_publish(const float* __restrict__ part, int nplanes, size_t np, size_t total,
+// grid.y = batch image (no index division)
+__global__ void k_chunk_reduce_publish(const float* __restrict__ part, int nplanes, size_t np,
                                        float* __restrict__ xbuf, size_t slot_elems, const unsigned* __restrict__ pad,
                                        float scale) {
-  float* dst = xbuf + (size_t)((pad[kEpoch] + 1u) & 1u) * slot_elems;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = i / np, p = i % np;
-    const float* src = part + b * nplanes * np + p;
+  const size_t b = blockIdx.y;
+  float* dst = xbuf + (size_t)((pad[kEpoch] + 1u) & 1u) * slot_elems + b * np;
+  const float* src0 = part + b * nplanes * np;
+  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
+    const float* src = src0 + p;
     float s = 0.f;
     for (int c = 0; c < nplanes; ++c) s += src[(size_t)c * np];
-    dst[i] = scale * s;
+    dst[p] = scale * s;
   }
 }
 
@@ -114,8 +116,8 @@ int launch_peer_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t s
 int launch_chunk_reduce_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
                                 cudaStream_t st) {
   if (total > p->xch_slot) return set_error(MS2G_ERR_CONFIG, "peer allreduce larger than the exchange slot");
-  k_chunk_reduce_publish<<<grid_for(total), 256, 0, st>>>(part, nplanes, np, total, p->xch_buf, p->xch_slot,
-                                                          p->xch_pad, scale);
+  k_chunk_reduce_publish<<<dim3(grid_for(np), (unsigned)(total / np)), 256, 0, st>>>(part, nplanes, np, p->xch_buf,
+                                                                                     p->xch_slot, p->xch_pad, scale);
   return check_launch("k_chunk_reduce_publish");
 }
 

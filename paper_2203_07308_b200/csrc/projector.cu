@@ -638,17 +638,20 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   }
 }
 
-// out = scale * sum of the nplanes partial planes (+ out if accumulate), fixed order.
-__global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size_t np, size_t total,
-                               float* __restrict__ out, float scale, int accumulate) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = i / np, p = i % np;
-    const float* src = part + b * nplanes * np + p;
+// out = scale * sum of the nplanes partial planes (+ out if accumulate), fixed
+// order.  grid.y = batch image (no index division).
+__global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size_t np, float* __restrict__ out,
+                               float scale, int accumulate) {
+  const size_t b = blockIdx.y;
+  const float* src0 = part + b * nplanes * np;
+  float* ob = out + b * np;
+  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
+    const float* src = src0 + p;
     float s = 0.f;
     for (int c = 0; c < nplanes; ++c) s += src[(size_t)c * np];
     float v = scale * s;
-    if (accumulate) v += out[i];
-    out[i] = v;
+    if (accumulate) v += ob[p];
+    ob[p] = v;
   }
 }
 
@@ -708,8 +711,8 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   const size_t np = (size_t)f.nc * f.nc, total = np * batch;
   if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)
     return launch_chunk_reduce_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);
-  const int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-  k_chunk_reduce<<<blocks, 256, 0, s>>>(p->w_part, ch[0] + ch[1], np, total, img, scale, accumulate);
+  const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);
+  k_chunk_reduce<<<dim3(blocks, batch), 256, 0, s>>>(p->w_part, ch[0] + ch[1], np, img, scale, accumulate);
   return check_launch("k_chunk_reduce");
 }
 

@@ -247,18 +247,37 @@ __device__ __forceinline__ float tv_div(const float* __restrict__ px, const floa
   return a + b;
 }
 
-// first != 0: p^0 = 0 (no warm start, no read of pin): div p = 0
-__global__ void k_tv_iter(const float* __restrict__ f, const float* __restrict__ pin, float* __restrict__ pout,
-                          int n, float inv_lambda, float tau, int first) {
-  PIXEL_IJB(n, n);
-  const size_t np = (size_t)n * n, p = (size_t)i * n + j;
+// One dual iteration.  The block's 32 x 8 pixels need w = div p - f / lambda
+// on themselves and one column / row beyond: w is formed once per point into
+// a (8+1) x (32+1) shared tile (instead of three times per pixel), then
+// q = grad w and the p update.  first != 0: p^0 = 0 (no warm start, pin not
+// read), so w = -f / lambda.
+__global__ void __launch_bounds__(256) k_tv_iter(const float* __restrict__ f, const float* __restrict__ pin,
+                                                 float* __restrict__ pout, int n, float inv_lambda, float tau,
+                                                 int first) {
+  __shared__ float sw[9][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 8;
+  const size_t b = blockIdx.z, np = (size_t)n * n;
   const float* fb = f + b * np;
   const float* px = pin + b * 2 * np;
   const float* py = px + np;
-  const float wc = (first ? 0.f : tv_div(px, py, n, i, j)) - fb[p] * inv_lambda;
-  float qx = 0.f, qy = 0.f;
-  if (j < n - 1) qx = ((first ? 0.f : tv_div(px, py, n, i, j + 1)) - fb[p + 1] * inv_lambda) - wc;
-  if (i < n - 1) qy = ((first ? 0.f : tv_div(px, py, n, i + 1, j)) - fb[p + n] * inv_lambda) - wc;
+  for (int e = ty * 32 + tx; e < 9 * 33; e += 256) {
+    const int li = e / 33, lj = e % 33, gi = i0 + li, gj = j0 + lj;
+    float w = 0.f;
+    if (gi < n && gj < n) {
+      const size_t q = (size_t)gi * n + gj;
+      w = (first ? 0.f : tv_div(px, py, n, gi, gj)) - fb[q] * inv_lambda;
+    }
+    sw[li][lj] = w;
+  }
+  __syncthreads();
+  const int i = i0 + ty, j = j0 + tx;
+  if (i >= n || j >= n) return;
+  const size_t p = (size_t)i * n + j;
+  const float wc = sw[ty][tx];
+  const float qx = (j < n - 1) ? sw[ty][tx + 1] - wc : 0.f;
+  const float qy = (i < n - 1) ? sw[ty + 1][tx] - wc : 0.f;
   const float rden = 1.f / (1.f + tau * sqrtf(qx * qx + qy * qy));   // one division for both components
   float* ox = pout + b * 2 * np;
   ox[p] = ((first ? 0.f : px[p]) + tau * qx) * rden;

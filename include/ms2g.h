@@ -64,7 +64,11 @@ typedef struct {
 
 /* Build the per-factor ray tables (host fp64, cast once) and every workspace.
  * factors: the sketch factors s (each divides n) the plan will be used with.
- * Synchronous.  Errors: MS2G_ERR_CONFIG (bad desc / factor), MS2G_ERR_CUDA. */
+ * Synchronous.  Errors: MS2G_ERR_CONFIG (bad desc / factor, or a ray lying
+ * exactly on a grid line of a planned grid -- reading Z14: such a ray meets
+ * two closed pixel rows and its row is undefined; it needs an odd bin count
+ * with views at multiples of 90 deg -- checked on the host before any device
+ * work), MS2G_ERR_CUDA. */
 int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32_t n_factors,
                        ms2g_plan** out);
 void ms2g_plan_destroy(ms2g_plan* plan);
@@ -139,6 +143,26 @@ int ms2g_sketch_up(ms2g_plan* plan, int32_t factor, int32_t kind, const float* g
  * partial A_s^T is summed over the ranks before U. */
 int ms2g_sketched_grad(ms2g_plan* plan, int32_t factor, int32_t kind, const float* x, const float* bsino, float* g,
                        const int32_t* subset, int32_t n_subset, void* stream);
+
+/* Registered view subsets (P:72, P:95-97 minibatches M_i reused every
+ * epoch).  ms2g_register_subset validates the ascending GLOBAL view list
+ * (MS2G_ERR_INPUT as above), uploads this rank's part once, builds the
+ * longest-first block orders of its projector launches for every planned
+ * factor and returns an id (synchronous; allocates).  The *_registered calls
+ * are the calls above with the list given by id: no host->device copy, no
+ * host synchronisation, so a loop of them is launch-bound only (and graph
+ * capturable).  ms2g_release_subset frees it (synchronises the device).
+ * MS2G_ERR_INPUT on an unknown or released id.  Ad-hoc `subset` arguments of
+ * the calls above use a ring of 8 staged lists per plan, each reused only
+ * after the kernels of its previous call (on whatever stream) completed. */
+int ms2g_register_subset(ms2g_plan* plan, const int32_t* subset, int32_t n_subset, int32_t* id);
+int ms2g_release_subset(ms2g_plan* plan, int32_t id);
+int ms2g_forward_project_registered(ms2g_plan* plan, int32_t factor, const float* x, const float* bsino,
+                                    float* out, int32_t subset_id, void* stream);
+int ms2g_back_project_registered(ms2g_plan* plan, int32_t factor, const float* sino, float* img, float scale,
+                                 int32_t accumulate, int32_t subset_id, int32_t allreduce, void* stream);
+int ms2g_sketched_grad_registered(ms2g_plan* plan, int32_t factor, int32_t kind, const float* x,
+                                  const float* bsino, float* g, int32_t subset_id, void* stream);
 
 /* Lipschitz constant of the factor-s fidelity ("eta = O(1/L)"; reading
  * Z5/Z6): v0 = 1/||1||, w = A_s^T A_s v, L = <v,w>, v = w/||w||, `iters`

@@ -19,7 +19,7 @@ __all__ = [
     "MS2GError", "DivergedError", "Plan", "plan_geometry", "forward_project", "back_project", "sketch_down",
     "sketch_up", "sketched_grad", "power_iteration", "denoise", "schedule", "schedule_views", "pnp_ms2g_solve",
     "pnp_ms2g_solve_async", "solve_status", "attach_nccl", "attach_peers", "view_shard", "set_kernel_timing",
-    "kernel_time", "launch_count", "lib_path", "load",
+    "kernel_time", "launch_count", "lib_path", "load", "register_subset", "release_subset", "RegisteredSubset",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -107,6 +107,11 @@ def load():
     L.ms2g_last_error.restype = C.c_char_p
     L.ms2g_launch_count.restype = C.c_uint64
     L.ms2g_plan_info.argtypes = [p, i, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(i)]
+    L.ms2g_register_subset.argtypes = [p, C.POINTER(C.c_int32), i, C.POINTER(i)]
+    L.ms2g_release_subset.argtypes = [p, i]
+    L.ms2g_forward_project_registered.argtypes = [p, i, p, p, p, i, p]
+    L.ms2g_back_project_registered.argtypes = [p, i, p, p, f, i, i, i, p]
+    L.ms2g_sketched_grad_registered.argtypes = [p, i, i, p, p, p, i, p]
     _lib = L
     return L
 
@@ -200,17 +205,59 @@ def plan_geometry(n, n_views, n_bins, factors=(1,), fov=2.0, arc=2 * math.pi, so
     return plan
 
 
+class RegisteredSubset:
+    """A view subset uploaded once (ms2g_register_subset); pass it as `subset`."""
+
+    def __init__(self, plan: Plan, sid: int, views):
+        self.plan, self.id = plan, sid
+        self.views = tuple(views)
+        self.n_sel = sum(1 for v in self.views if plan.view_begin <= v < plan.view_end)
+
+    def release(self):
+        if self.id is not None and self.plan._h is not None:
+            _check(load().ms2g_release_subset(self.plan.handle, self.id))
+        self.id = None
+
+
+def register_subset(plan: Plan, subset) -> RegisteredSubset:
+    """Upload an ascending global view list once (+ its block orders); the
+    projector / gradient calls then take it without a per-call copy."""
+    sel, m = _subset(subset)
+    sid = C.c_int32(-1)
+    _check(load().ms2g_register_subset(plan.handle, sel, m, C.byref(sid)))
+    return RegisteredSubset(plan, sid.value, [sel[k] for k in range(m)])
+
+
+def release_subset(rs: RegisteredSubset):
+    rs.release()
+
+
+def _reg(subset):
+    if isinstance(subset, RegisteredSubset):
+        if subset.id is None:
+            raise MS2GError(MS2G_ERR_INPUT, "subset was released")
+        return subset.id
+    return None
+
+
 def _n_sel(plan: Plan, subset) -> int:
     if subset is None:
         return plan.n_local_views
+    if isinstance(subset, RegisteredSubset):
+        return subset.n_sel
     return sum(1 for v in subset if plan.view_begin <= int(v) < plan.view_end)
 
 
 def forward_project(plan: Plan, factor: int, x, b=None, subset=None, out=None):
     """r = A_s x - b on the selected views, compacted [batch][n_sel][B]."""
-    sel, m = _subset(subset)
     if out is None:
         out = torch.empty((plan.batch, _n_sel(plan, subset), plan.n_bins), device=x.device, dtype=torch.float32)
+    rid = _reg(subset)
+    if rid is not None:
+        _check(load().ms2g_forward_project_registered(plan.handle, factor, _dev(x, "x"), _dev(b, "b"),
+                                                      _dev(out, "out"), rid, _stream()))
+        return out
+    sel, m = _subset(subset)
     _check(load().ms2g_forward_project(plan.handle, factor, _dev(x, "x"), _dev(b, "b"), _dev(out, "out"), sel, m,
                                        _stream()))
     return out
@@ -220,10 +267,16 @@ def back_project(plan: Plan, factor: int, sino, img=None, scale=1.0, accumulate=
                  allreduce=False):
     """img = scale A_s^T sino (+img if accumulate); allreduce: sum over the
     ranks attached by attach_nccl / attach_peers."""
-    sel, m = _subset(subset)
     nc = plan.nc(factor)
     if img is None:
         img = torch.empty((plan.batch, nc, nc), device=sino.device, dtype=torch.float32)
+    rid = _reg(subset)
+    if rid is not None:
+        _check(load().ms2g_back_project_registered(plan.handle, factor, _dev(sino, "sino"), _dev(img, "img"),
+                                                   float(scale), int(bool(accumulate)), rid, int(bool(allreduce)),
+                                                   _stream()))
+        return img
+    sel, m = _subset(subset)
     _check(load().ms2g_back_project(plan.handle, factor, _dev(sino, "sino"), _dev(img, "img"), float(scale),
                                     int(bool(accumulate)), sel, m, int(bool(allreduce)), _stream()))
     return img
@@ -256,9 +309,14 @@ def sketch_up(plan: Plan, factor: int, g, y=None, eta=0.0, z=None, resampler="me
 
 def sketched_grad(plan: Plan, factor: int, x, b, g=None, subset=None, resampler="mean"):
     """g = (V/|M|) U A_s^T (A_s S x - b_M)."""
-    sel, m = _subset(subset)
     if g is None:
         g = torch.empty((plan.batch, plan.n, plan.n), device=x.device, dtype=torch.float32)
+    rid = _reg(subset)
+    if rid is not None:
+        _check(load().ms2g_sketched_grad_registered(plan.handle, factor, _kind(resampler), _dev(x, "x"), _dev(b, "b"),
+                                                    _dev(g, "g"), rid, _stream()))
+        return g
+    sel, m = _subset(subset)
     _check(load().ms2g_sketched_grad(plan.handle, factor, _kind(resampler), _dev(x, "x"), _dev(b, "b"), _dev(g, "g"),
                                      sel, m, _stream()))
     return g
@@ -343,8 +401,12 @@ def pnp_ms2g_solve(plan: Plan, stages, b, x0=None, option=1, n_subsets=1, seed=0
     _check(load().ms2g_pnp_ms2g_solve(plan.handle, C.byref(desc), _dev(b_d, "b"), _dev(x0_d, "x0"),
                                       _dev(out_d, "x_out"), tr, _stream()))
     result = out_d
-    if host:
-        result = x_out if x_out is not None else torch.empty(out_d.shape, dtype=torch.float32).pin_memory()
+    if x_out is not None and not x_out.is_cuda:      # a host x_out is always written (either branch)
+        x_out.copy_(out_d, non_blocking=x_out.is_pinned())
+        torch.cuda.current_stream().synchronize()
+        result = x_out
+    elif host:
+        result = torch.empty(out_d.shape, dtype=torch.float32).pin_memory()
         result.copy_(out_d, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     if trace:

@@ -129,9 +129,23 @@ struct ms2g_plan {
   float* w_etaf = nullptr;             // fp32 eta per stage [64]
   double* w_pw = nullptr;              // power-iteration scalars (dot, inv_norm)
   int* w_flag = nullptr;               // first non-finite global iteration (INT_MAX = none)
-  int* w_sel = nullptr;                // selected-view scratch [V_r]
-  int* h_sel = nullptr;                // pinned host staging for subsets
-  cudaEvent_t sel_ev = nullptr;
+  // ad-hoc host subsets: a ring of kSelRing (pinned host, device) list slots;
+  // slot k is reused only after the event recorded behind its last consumer
+  // (on that consumer's stream) has completed, so calls on different streams
+  // never overwrite a list a kernel still reads
+  static constexpr int kSelRing = 8;
+  int* w_sel = nullptr;                // device lists [kSelRing][V_r]
+  int* h_sel = nullptr;                // pinned host staging [kSelRing][V_r]
+  cudaEvent_t sel_ev[kSelRing] = {};
+  int sel_next = 0;
+  // registered subsets (ms2g_register_subset): device list + longest-first
+  // block orders per factor, built once; id = index (nullptr d_sel: released)
+  struct RegSubset {
+    int* d_sel = nullptr;
+    int n_sel = 0, n_global = 0;
+    std::vector<int*> bp_order, fwd_order;   // per plan factor (index into ft)
+  };
+  std::vector<RegSubset> reg;
   int* w_subsets = nullptr;            // precomputed Option-2 subset lists
   int* w_mb = nullptr;                 // precomputed Option-4 minibatch lists
   float* w_saga = nullptr;             // Option-5 table: K coarse gradients + their mean
@@ -152,6 +166,7 @@ struct ms2g_plan {
   unsigned** d_peer_pads = nullptr;
   int* w_peer_err = nullptr;
   int peer_rank = 0, peer_n = 0;       // peer_n > 0: attached
+  bool peer_failed = false;            // a barrier timed out: exchanges refused until re-attached
   std::vector<void*> peer_opened;      // IPC mappings to close
   // Power-iteration branches of the solve graph: one per stage factor, each
   // with its own workspaces (batch 1), so the geometry-only power chains of

@@ -106,6 +106,47 @@ static int upload_fwd_order(const ms2g_plan* p, const FactorTables& f, const std
   return upload_order(cost, out);
 }
 
+// Reading Z14 at the boundary: a ray lying ON a grid line of a planned grid
+// (exactly axis-parallel, its constant coordinate a grid line) belongs to two
+// closed pixel rows at once; the paper and the configs leave that undefined
+// (it needs an odd bin count with an even grid side, or a shifted detector).
+// The oracle's fp64 crossings then split the ray by rounding noise while the
+// fixed-point traversal picks one row, so such geometries are rejected before
+// any device work (MS2G_ERR_CONFIG).  Tolerances: |slope| < 1e-9 and within
+// 1e-6 pixel of a grid line (the fixed point resolves 2^-32 pixel, and its
+// slope floor 2^-32 moves a ray by < 1e-6 pixel across 32767 columns).
+static int check_grid_ties(const ms2g_geom_desc& d, double pitch, const int32_t* factors, int n_factors) {
+  const double org = -0.5 * d.fov;
+  for (int v = d.view_begin; v < d.view_end; ++v) {
+    const double th = d.arc_rad * (double)v / (double)d.n_views;
+    const double c = std::cos(th), s = std::sin(th);
+    const double sx = d.sod * c, sy = d.sod * s;
+    for (int t = 0; t < d.n_bins; ++t) {
+      const double u = ((double)t - 0.5 * (double)(d.n_bins - 1)) * pitch;
+      const double px = -(d.sdd - d.sod) * c - u * s, py = -(d.sdd - d.sod) * s + u * c;
+      const double dx = px - sx, dy = py - sy;
+      double coord;   // the constant coordinate of an axis-parallel ray
+      if (std::fabs(dy) < 1e-9 * std::fabs(dx)) coord = sy + (org - sx) * dy / dx;
+      else if (std::fabs(dx) < 1e-9 * std::fabs(dy)) coord = sx + (org - sy) * dx / dy;
+      else continue;
+      for (int k = 0; k < n_factors; ++k) {
+        const int fac = factors[k];
+        if (fac < 1 || d.n % fac) continue;       // reported by the caller
+        const double hc = d.fov * fac / d.n;
+        const double q = (coord - org) / hc;      // grid-line units of this grid
+        const double r = std::nearbyint(q);
+        if (r >= 0 && r <= d.n / fac && std::fabs(q - r) < 1e-6) {
+          std::ostringstream os;
+          os << "ray (view " << v << ", bin " << t << ") lies on grid line " << (long long)r << " of the factor-"
+             << fac << " grid (reading Z14: ambiguous pixel row); use an even bin count or move the detector";
+          return set_error(MS2G_ERR_CONFIG, os.str());
+        }
+      }
+    }
+  }
+  return MS2G_OK;
+}
+
 // Geometry plan: per-view and
 // per-ray constants computed in fp64 on the host, rounded once.
 static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
@@ -305,7 +346,13 @@ static void free_plan(ms2g_plan* p) {
   cudaFree(p->w_mb);
   cudaFree(p->w_saga);
   if (p->h_sel) cudaFreeHost(p->h_sel);
-  if (p->sel_ev) cudaEventDestroy(p->sel_ev);
+  for (cudaEvent_t ev : p->sel_ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& r : p->reg) {
+    cudaFree(r.d_sel);
+    for (int* q : r.bp_order) cudaFree(q);
+    for (int* q : r.fwd_order) cudaFree(q);
+  }
   if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
   if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
   for (auto& br : p->pbr) {
@@ -333,36 +380,71 @@ static void free_plan(ms2g_plan* p) {
 
 // Resolve a host subset of GLOBAL view indices into this rank's compacted
 // list on the device (stream ordered).  subset == NULL -> all views.
+// Host subsets use a slot of the plan's list ring (*slot, -1 if none); the
+// caller releases it with release_subset after enqueueing every consumer.
+static int check_subset(const ms2g_plan* p, const int32_t* subset, int n_subset, int* m_local) {
+  if (n_subset < 1) return set_error(MS2G_ERR_INPUT, "empty view subset (S:285)");
+  int prev = -1, m = 0;
+  for (int k = 0; k < n_subset; ++k) {
+    const int v = subset[k];
+    if (v < 0 || v >= p->d.n_views || v <= prev)
+      return set_error(MS2G_ERR_INPUT, "subset must hold ascending view indices in [0, n_views)");
+    prev = v;
+    m += (v >= p->d.view_begin && v < p->d.view_end);
+  }
+  *m_local = m;
+  return MS2G_OK;
+}
+
 static int resolve_subset(ms2g_plan* p, const int32_t* subset, int n_subset, cudaStream_t st, const int** d_sel,
-                          int* n_sel, int* n_global) {
+                          int* n_sel, int* n_global, int* slot) {
+  *slot = -1;
   if (!subset) {
     *d_sel = nullptr;
     *n_sel = p->V_r;
     *n_global = p->d.n_views;
     return MS2G_OK;
   }
-  if (n_subset < 1) return set_error(MS2G_ERR_INPUT, "empty view subset (S:285)");
-  int prev = -1, m = 0;
-  MS2G_CUDA(cudaEventSynchronize(p->sel_ev));  // staging buffer free again
-  for (int k = 0; k < n_subset; ++k) {
-    const int v = subset[k];
-    if (v < 0 || v >= p->d.n_views || v <= prev)
-      return set_error(MS2G_ERR_INPUT, "subset must hold ascending view indices in [0, n_views)");
-    prev = v;
-    if (v >= p->d.view_begin && v < p->d.view_end) p->h_sel[m++] = v - p->d.view_begin;
-  }
+  int m = 0;
+  MS2G_TRY(check_subset(p, subset, n_subset, &m));
+  const int k = p->sel_next;
+  int* h = p->h_sel + (size_t)k * p->V_r;
+  int* dv = p->w_sel + (size_t)k * p->V_r;
   if (m > 0) {
-    MS2G_CUDA(cudaMemcpyAsync(p->w_sel, p->h_sel, sizeof(int) * m, cudaMemcpyHostToDevice, st));
-    MS2G_CUDA(cudaEventRecord(p->sel_ev, st));
+    // the slot's previous consumers (any stream) are done: ring depth 8, so
+    // this waits only when 8 calls are in flight
+    MS2G_CUDA(cudaEventSynchronize(p->sel_ev[k]));
+    int q = 0;
+    for (int i = 0; i < n_subset; ++i) {
+      const int v = subset[i];
+      if (v >= p->d.view_begin && v < p->d.view_end) h[q++] = v - p->d.view_begin;
+    }
+    MS2G_CUDA(cudaMemcpyAsync(dv, h, sizeof(int) * m, cudaMemcpyHostToDevice, st));
+    p->sel_next = (k + 1) % ms2g_plan::kSelRing;
+    *slot = k;
   }
-  *d_sel = p->w_sel;
+  *d_sel = dv;
   *n_sel = m;
   *n_global = n_subset;
   return MS2G_OK;
 }
 
+static int release_subset(ms2g_plan* p, int slot, cudaStream_t st) {
+  if (slot >= 0) MS2G_CUDA(cudaEventRecord(p->sel_ev[slot], st));
+  return MS2G_OK;
+}
+
+static int peer_ok(const ms2g_plan* p) {
+  if (p->peer_failed)
+    return set_error(MS2G_ERR_NCCL, "peer exchange failed earlier (barrier time-out): call ms2g_attach_peers again");
+  return MS2G_OK;
+}
+
 static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
-  if (p->peer_n > 0) return launch_peer_allreduce(p, buf, count, st);   // NEXT-3 peer path wins
+  if (p->peer_n > 0) {                      // NEXT-3 peer path wins
+    MS2G_TRY(peer_ok(p));
+    return launch_peer_allreduce(p, buf, count, st);
+  }
   if (!p->comm) return MS2G_OK;   // attached communicators are always used (1 rank: NCCL identity)
   MS2G_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, p->comm, st));
   return MS2G_OK;
@@ -375,6 +457,7 @@ static int backward_sum(ms2g_plan* p, const FactorTables& f, const float* sino, 
                         int n_sel, int batch, cudaStream_t st, const int* order_sel = nullptr) {
   const size_t count = (size_t)f.nc * f.nc * batch;
   if (p->peer_n > 0) {
+    MS2G_TRY(peer_ok(p));
     MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st, 1, order_sel));
     return launch_peer_finish(p, G, count, st);
   }
@@ -384,7 +467,8 @@ static int backward_sum(ms2g_plan* p, const FactorTables& f, const float* sino, 
 
 // g = c U_s A_s^T (A_s S_s x - b), into a full-resolution image.
 static int enqueue_grad(ms2g_plan* p, const FactorTables& f, int kind, const float* x, const float* b, float* g,
-                        const int* d_sel, int n_sel, float c, int batch, cudaStream_t st) {
+                        const int* d_sel, int n_sel, float c, int batch, cudaStream_t st,
+                        const int* ford = nullptr, const int* bord = nullptr) {
   const int s = f.factor;
   const float* v = x;
   if (s > 1) {
@@ -392,9 +476,9 @@ static int enqueue_grad(ms2g_plan* p, const FactorTables& f, int kind, const flo
     v = p->w_v;
   }
   MS2G_TRY(launch_pair_prep(p, f.nc, batch, v, st));
-  MS2G_TRY(launch_forward(p, f, b, p->w_res, d_sel, n_sel, batch, st));  // r = A_s v - b
+  MS2G_TRY(launch_forward(p, f, b, p->w_res, d_sel, n_sel, batch, st, ford));  // r = A_s v - b
   float* G = (s > 1) ? p->w_G : g;
-  MS2G_TRY(backward_sum(p, f, p->w_res, G, c, d_sel, n_sel, batch, st));      // G = c A_s^T r (+ ranks)
+  MS2G_TRY(backward_sum(p, f, p->w_res, G, c, d_sel, n_sel, batch, st, bord));  // G = c A_s^T r (+ ranks)
   if (s > 1) MS2G_TRY(launch_resample_up_step(p, f, kind, batch, G, nullptr, nullptr, 0.f, g, st));  // U G
   return MS2G_OK;
 }
@@ -765,12 +849,20 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
   return MS2G_OK;
 }
 
+// Key of a captured solve graph.  Every parameter baked into the graph's
+// kernel arguments enters with its exact bits (floats as their 32-bit
+// patterns): two descriptors that differ anywhere never share a graph.
 static std::string solve_key(const ms2g_solve_desc* sd, const float* b, const float* x0, const float* x_out) {
+  auto bits = [](float f) {
+    uint32_t u;
+    memcpy(&u, &f, sizeof(u));
+    return u;
+  };
   std::ostringstream os;
-  os << sd->n_stages << ':' << sd->option << ':' << sd->n_subsets << ':' << sd->seed << ':' << sd->den.kind << ':'
-     << sd->den.sigma << ':' << sd->den.lambda << ':' << sd->den.tau << ':' << sd->den.inner_iters << ':'
-     << sd->alpha << ':' << sd->power_iters << ':' << sd->resampler << ':' << (const void*)b << ':' << (const void*)x0 << ':'
-     << (const void*)x_out;
+  os << std::hex << sd->n_stages << ':' << sd->option << ':' << sd->n_subsets << ':' << sd->seed << ':'
+     << sd->den.kind << ':' << bits(sd->den.sigma) << ':' << bits(sd->den.lambda) << ':' << bits(sd->den.tau) << ':'
+     << sd->den.inner_iters << ':' << bits(sd->alpha) << ':' << sd->power_iters << ':' << sd->resampler << ':'
+     << (const void*)b << ':' << (const void*)x0 << ':' << (const void*)x_out;
   for (int k = 0; k < sd->n_stages; ++k)
     os << '|' << sd->stages[k].factor << ',' << sd->stages[k].n_iters << ',' << sd->stages[k].n_epochs;
   return os.str();
@@ -779,6 +871,7 @@ static std::string solve_key(const ms2g_solve_desc* sd, const float* b, const fl
 static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b, const float* x0, float* x_out,
                         cudaStream_t st) {
   if (!b || !x0 || !x_out) return set_error(MS2G_ERR_INPUT, "NULL b/x0/x_out");
+  if (p->peer_n > 0) MS2G_TRY(peer_ok(p));   // a cached graph would replay the failed exchange
   if (!(sd->alpha > 0.f && sd->alpha <= 1.f)) return set_error(MS2G_ERR_CONFIG, "alpha must be in (0, 1] (S:197)");
   if (sd->power_iters < 0) return set_error(MS2G_ERR_CONFIG, "power_iters must be >= 0");
   if (sd->resampler != 0 && sd->resampler != 1) return set_error(MS2G_ERR_CONFIG, "resampler must be 0 or 1");
@@ -854,7 +947,11 @@ static int solve_status(ms2g_plan* p, cudaStream_t st) {
   MS2G_CUDA(cudaMemcpyAsync(&flag, p->w_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (p->w_peer_err) MS2G_CUDA(cudaMemcpyAsync(&perr, p->w_peer_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   MS2G_CUDA(cudaStreamSynchronize(st));
-  if (perr) return set_error(MS2G_ERR_NCCL, "peer allreduce: barrier timed out (a rank never arrived)");
+  if (perr) {
+    p->peer_failed = true;     // epochs are out of step: refuse exchanges until every rank re-attaches
+    return set_error(MS2G_ERR_NCCL, "peer allreduce: barrier timed out (a rank never arrived); "
+                                    "call ms2g_attach_peers again on every rank");
+  }
   if (flag != INT_MAX) {
     int stage = -1;
     for (const auto& e : p->last_sched)
@@ -891,6 +988,11 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     return set_error(MS2G_ERR_CONFIG, "view shard [view_begin, view_end) out of range");
   if (d.batch < 1) d.batch = 1;
   if (!factors || n_factors < 1) return set_error(MS2G_ERR_CONFIG, "need at least one factor");
+  for (int k = 0; k < n_factors; ++k)
+    if (factors[k] < 1 || d.n % factors[k] != 0)
+      return set_error(MS2G_ERR_CONFIG, "every factor must be >= 1 and divide n (S:127, S:145)");
+  // host-only geometry checks first: they need no device (testable on CPU)
+  MS2G_TRY(check_grid_ties(d, d.bin_pitch > 0 ? d.bin_pitch : (d.sdd / d.sod) * d.fov / d.n, factors, n_factors));
   ms2g_plan* p = new ms2g_plan();
   p->d = d;
   p->V_r = d.view_end - d.view_begin;
@@ -958,9 +1060,10 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
   if (e == cudaSuccess) e = cudaMalloc(&p->w_scal, sizeof(double) * 128);
   if (e == cudaSuccess) e = cudaMalloc(&p->w_pw, sizeof(double) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&p->w_flag, sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&p->w_sel, sizeof(int) * p->V_r);
-  if (e == cudaSuccess) e = cudaMallocHost(&p->h_sel, sizeof(int) * p->V_r);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->sel_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_sel, sizeof(int) * p->V_r * ms2g_plan::kSelRing);
+  if (e == cudaSuccess) e = cudaMallocHost(&p->h_sel, sizeof(int) * p->V_r * ms2g_plan::kSelRing);
+  for (int k = 0; k < ms2g_plan::kSelRing && e == cudaSuccess; ++k)
+    e = cudaEventCreateWithFlags(&p->sel_ev[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMemset(p->w_flag, 0x7f, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(p->w_scal, 0, sizeof(double) * 128);
   if (e != cudaSuccess) {
@@ -1085,7 +1188,20 @@ int ms2g_peer_export(ms2g_plan* p, void* blob) {
 int ms2g_attach_peers(ms2g_plan* p, const void* blobs, int32_t rank, int32_t nranks) {
   if (!p || !blobs) return set_error(MS2G_ERR_INPUT, "NULL plan/blobs");
   if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) return set_error(MS2G_ERR_CONFIG, "bad rank/nranks");
-  if (p->peer_n > 0) return set_error(MS2G_ERR_CONFIG, "peers already attached");
+  if (p->peer_n > 0 && !p->peer_failed) return set_error(MS2G_ERR_CONFIG, "peers already attached");
+  if (p->peer_n > 0) {        // re-attach after a time-out: fresh mappings, epochs and error flag
+    MS2G_CUDA(cudaDeviceSynchronize());
+    for (void* q : p->peer_opened) cudaIpcCloseMemHandle(q);
+    p->peer_opened.clear();
+    cudaFree(p->d_peer_bufs);
+    cudaFree(p->d_peer_pads);
+    p->d_peer_bufs = nullptr;
+    p->d_peer_pads = nullptr;
+    p->peer_n = 0;
+    MS2G_CUDA(cudaMemset(p->xch_pad, 0, sizeof(unsigned) * kPadWords));
+    MS2G_CUDA(cudaMemset(p->w_peer_err, 0, sizeof(int)));
+    p->peer_failed = false;
+  }
   MS2G_TRY(ensure_exchange(p));
   std::vector<float*> bufs(nranks);
   std::vector<unsigned*> pads(nranks);
@@ -1123,33 +1239,178 @@ int ms2g_attach_peers(ms2g_plan* p, const void* blobs, int32_t rank, int32_t nra
   return MS2G_OK;
 }
 
+// A resolved view selection: an ad-hoc host subset in a ring slot, a
+// registered subset (with its longest-first block orders), or all views.
+struct Sel {
+  const int* d_sel = nullptr;
+  int n_sel = 0, n_glob = 0, slot = -1;
+  const int* ford = nullptr;
+  const int* bord = nullptr;
+};
+
+static int sel_host(ms2g_plan* p, const int32_t* subset, int32_t n_subset, cudaStream_t st, Sel* s) {
+  return resolve_subset(p, subset, n_subset, st, &s->d_sel, &s->n_sel, &s->n_glob, &s->slot);
+}
+
+static int sel_registered(ms2g_plan* p, int32_t id, const FactorTables* f, Sel* s) {
+  if (id < 0 || id >= (int)p->reg.size() || !p->reg[id].d_sel)
+    return set_error(MS2G_ERR_INPUT, "unknown or released subset id");
+  const auto& r = p->reg[id];
+  const int fi = (int)(f - p->ft.data());
+  s->d_sel = r.d_sel;
+  s->n_sel = r.n_sel;
+  s->n_glob = r.n_global;
+  s->ford = r.fwd_order.empty() ? nullptr : r.fwd_order[fi];
+  s->bord = r.bp_order.empty() ? nullptr : r.bp_order[fi];
+  return MS2G_OK;
+}
+
+static int do_forward(ms2g_plan* p, const FactorTables* f, const float* x, const float* b, float* out,
+                      const Sel& s, cudaStream_t st) {
+  MS2G_TRY(launch_pair_prep(p, f->nc, p->d.batch, x, st));
+  return launch_forward(p, *f, b, out, s.d_sel, s.n_sel, p->d.batch, st, s.ford);
+}
+
+static int do_backward(ms2g_plan* p, const FactorTables* f, const float* sino, float* img, float scale,
+                       int accumulate, int do_allreduce, const Sel& s, cudaStream_t st) {
+  MS2G_TRY(launch_backward(p, *f, sino, img, scale, accumulate, s.d_sel, s.n_sel, p->d.batch, st, 0, s.bord));
+  if (do_allreduce) MS2G_TRY(allreduce(p, img, (size_t)f->nc * f->nc * p->d.batch, st));
+  return MS2G_OK;
+}
+
+static int do_grad(ms2g_plan* p, const FactorTables* f, int kind, const float* x, const float* b, float* g,
+                   const Sel& s, cudaStream_t st) {
+  const float c = (float)((double)p->d.n_views / (double)s.n_glob);
+  return enqueue_grad(p, *f, kind, x, b, g, s.d_sel, s.n_sel, c, p->d.batch, st, s.ford, s.bord);
+}
+
+static int check_fwd(ms2g_plan* p, int32_t factor, const float* x, const float* out, const FactorTables** f) {
+  if (!p || !x || !out) return set_error(MS2G_ERR_INPUT, "NULL plan/x/out");
+  *f = find_factor(p, factor);
+  if (!*f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  return MS2G_OK;
+}
+
+static int check_bwd(ms2g_plan* p, int32_t factor, const float* sino, const float* img, int do_allreduce,
+                     const FactorTables** f) {
+  if (!p || !sino || !img) return set_error(MS2G_ERR_INPUT, "NULL plan/sino/img");
+  *f = find_factor(p, factor);
+  if (!*f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  if (do_allreduce && !p->comm && !p->peer_n && p->nranks > 1)
+    return set_error(MS2G_ERR_CONFIG, "allreduce needs attach_nccl or attach_peers");
+  return MS2G_OK;
+}
+
+static int check_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, const float* b, const float* g,
+                      const FactorTables** f) {
+  if (kind != 0 && kind != 1) return set_error(MS2G_ERR_CONFIG, "kind must be 0 or 1");
+  if (!p || !x || !b || !g) return set_error(MS2G_ERR_INPUT, "NULL plan/x/b/g");
+  *f = find_factor(p, factor);
+  if (!*f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  if (factor != 1 && p->nmax_c < (*f)->nc) return set_error(MS2G_ERR_CONFIG, "workspace too small");
+  return MS2G_OK;
+}
+
 int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* out,
                          const int32_t* subset, int32_t n_subset, void* stream) {
-  if (!p || !x || !out) return set_error(MS2G_ERR_INPUT, "NULL plan/x/out");
-  const FactorTables* f = find_factor(p, factor);
-  if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
+  const FactorTables* f;
+  MS2G_TRY(check_fwd(p, factor, x, out, &f));
   cudaStream_t st = (cudaStream_t)stream;
-  const int* d_sel;
-  int n_sel, n_glob;
-  MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
-  MS2G_TRY(launch_pair_prep(p, f->nc, p->d.batch, x, st));
-  return launch_forward(p, *f, b, out, d_sel, n_sel, p->d.batch, st);
+  Sel s;
+  MS2G_TRY(sel_host(p, subset, n_subset, st, &s));
+  const int rc = do_forward(p, f, x, b, out, s, st);
+  MS2G_TRY(release_subset(p, s.slot, st));
+  return rc;
 }
 
 int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* img, float scale, int32_t accumulate,
                       const int32_t* subset, int32_t n_subset, int32_t do_allreduce, void* stream) {
-  if (!p || !sino || !img) return set_error(MS2G_ERR_INPUT, "NULL plan/sino/img");
-  const FactorTables* f = find_factor(p, factor);
-  if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
-  if (do_allreduce && !p->comm && !p->peer_n && p->nranks > 1)
-    return set_error(MS2G_ERR_CONFIG, "allreduce needs attach_nccl or attach_peers");
+  const FactorTables* f;
+  MS2G_TRY(check_bwd(p, factor, sino, img, do_allreduce, &f));
   cudaStream_t st = (cudaStream_t)stream;
-  const int* d_sel;
-  int n_sel, n_glob;
-  MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
-  MS2G_TRY(launch_backward(p, *f, sino, img, scale, accumulate, d_sel, n_sel, p->d.batch, st));
-  if (do_allreduce) MS2G_TRY(allreduce(p, img, (size_t)f->nc * f->nc * p->d.batch, st));
+  Sel s;
+  MS2G_TRY(sel_host(p, subset, n_subset, st, &s));
+  const int rc = do_backward(p, f, sino, img, scale, accumulate, do_allreduce, s, st);
+  MS2G_TRY(release_subset(p, s.slot, st));
+  return rc;
+}
+
+int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, const float* b, float* g,
+                       const int32_t* subset, int32_t n_subset, void* stream) {
+  const FactorTables* f;
+  MS2G_TRY(check_grad(p, factor, kind, x, b, g, &f));
+  cudaStream_t st = (cudaStream_t)stream;
+  Sel s;
+  MS2G_TRY(sel_host(p, subset, n_subset, st, &s));
+  const int rc = do_grad(p, f, kind, x, b, g, s, st);
+  MS2G_TRY(release_subset(p, s.slot, st));
+  return rc;
+}
+
+int ms2g_register_subset(ms2g_plan* p, const int32_t* subset, int32_t n_subset, int32_t* id) {
+  if (!p || !subset || !id) return set_error(MS2G_ERR_INPUT, "NULL plan/subset/id");
+  int m = 0;
+  MS2G_TRY(check_subset(p, subset, n_subset, &m));
+  ms2g_plan::RegSubset r;
+  std::vector<int> local;
+  for (int i = 0; i < n_subset; ++i)
+    if (subset[i] >= p->d.view_begin && subset[i] < p->d.view_end) local.push_back(subset[i] - p->d.view_begin);
+  r.n_sel = m;
+  r.n_global = n_subset;
+  MS2G_CUDA(cudaMalloc(&r.d_sel, sizeof(int) * std::max(m, 1)));
+  if (m > 0) MS2G_CUDA(cudaMemcpy(r.d_sel, local.data(), sizeof(int) * m, cudaMemcpyHostToDevice));
+  if (m > 0) {
+    for (const auto& f : p->ft) {
+      int* o = nullptr;
+      MS2G_TRY(upload_bp_order(p, f, local, &o));
+      r.bp_order.push_back(o);
+      o = nullptr;
+      if (p->d.batch % 2 != 0) MS2G_TRY(upload_fwd_order(p, f, local, fwd_views_per_block(p, m, p->d.batch), &o));
+      r.fwd_order.push_back(o);
+    }
+  }
+  p->reg.push_back(r);
+  *id = (int32_t)p->reg.size() - 1;
   return MS2G_OK;
+}
+
+int ms2g_release_subset(ms2g_plan* p, int32_t id) {
+  if (!p || id < 0 || id >= (int)p->reg.size() || !p->reg[id].d_sel)
+    return set_error(MS2G_ERR_INPUT, "unknown or released subset id");
+  MS2G_CUDA(cudaDeviceSynchronize());   // no kernel of any stream may still read it
+  auto& r = p->reg[id];
+  cudaFree(r.d_sel);
+  for (int* q : r.bp_order) cudaFree(q);
+  for (int* q : r.fwd_order) cudaFree(q);
+  r = ms2g_plan::RegSubset{};
+  return MS2G_OK;
+}
+
+int ms2g_forward_project_registered(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* out,
+                                    int32_t subset_id, void* stream) {
+  const FactorTables* f;
+  MS2G_TRY(check_fwd(p, factor, x, out, &f));
+  Sel s;
+  MS2G_TRY(sel_registered(p, subset_id, f, &s));
+  return do_forward(p, f, x, b, out, s, (cudaStream_t)stream);
+}
+
+int ms2g_back_project_registered(ms2g_plan* p, int32_t factor, const float* sino, float* img, float scale,
+                                 int32_t accumulate, int32_t subset_id, int32_t do_allreduce, void* stream) {
+  const FactorTables* f;
+  MS2G_TRY(check_bwd(p, factor, sino, img, do_allreduce, &f));
+  Sel s;
+  MS2G_TRY(sel_registered(p, subset_id, f, &s));
+  return do_backward(p, f, sino, img, scale, accumulate, do_allreduce, s, (cudaStream_t)stream);
+}
+
+int ms2g_sketched_grad_registered(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, const float* b,
+                                  float* g, int32_t subset_id, void* stream) {
+  const FactorTables* f;
+  MS2G_TRY(check_grad(p, factor, kind, x, b, g, &f));
+  Sel s;
+  MS2G_TRY(sel_registered(p, subset_id, f, &s));
+  return do_grad(p, f, kind, x, b, g, s, (cudaStream_t)stream);
 }
 
 int ms2g_sketch_down(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, float* v, void* stream) {
@@ -1171,21 +1432,6 @@ int ms2g_sketch_up(ms2g_plan* p, int32_t factor, int32_t kind, const float* g, c
   const FactorTables* f = find_factor(p, factor);
   if (!f) return set_error(MS2G_ERR_CONFIG, "bicubic resampling needs the factor in the plan");
   return launch_resample_up_step(p, *f, kind, p->d.batch, g, y, nullptr, y ? eta : 0.f, z, (cudaStream_t)stream);
-}
-
-int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, const float* b, float* g,
-                       const int32_t* subset, int32_t n_subset, void* stream) {
-  if (kind != 0 && kind != 1) return set_error(MS2G_ERR_CONFIG, "kind must be 0 or 1");
-  if (!p || !x || !b || !g) return set_error(MS2G_ERR_INPUT, "NULL plan/x/b/g");
-  const FactorTables* f = find_factor(p, factor);
-  if (!f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
-  if (factor == 1 ? false : p->nmax_c < f->nc) return set_error(MS2G_ERR_CONFIG, "workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int* d_sel;
-  int n_sel, n_glob;
-  MS2G_TRY(resolve_subset(p, subset, n_subset, st, &d_sel, &n_sel, &n_glob));
-  const float c = (float)((double)p->d.n_views / (double)n_glob);
-  return enqueue_grad(p, *f, kind, x, b, g, d_sel, n_sel, c, p->d.batch, st);
 }
 
 int ms2g_power_iteration(ms2g_plan* p, int32_t factor, int32_t iters, double* L, void* stream) {

@@ -17,8 +17,11 @@
 // Two slots alternate: a rank reuses a slot two allreduces later only after
 // the barrier in between, which every peer passes only after finishing its
 // sum of that slot (stream order), so no extra barrier is needed.
-// The spin in the barrier is bounded (about 20 s); on time-out it raises the
-// plan's error flag instead of hanging the device.
+// The wait in the barrier is bounded by 20 s of wall time (%globaltimer); on a
+// time-out it raises the plan's error flag instead of hanging the device, and
+// every later barrier / sum of the plan returns at once.  The host then sees
+// MS2G_ERR_NCCL and the plan refuses further exchanges until every rank calls
+// ms2g_attach_peers again (epochs restart from 0).
 #include "internal.cuh"
 
 namespace ms2g {
@@ -59,6 +62,31 @@ __global__ void k_publish_copy(const float* __restrict__ buf, size_t count, floa
     dst[i] = buf[i];
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Wait until *slot has reached epoch e.  Bounded by WALL time (%globaltimer,
+// kPeerTimeoutNs), not by a spin count; returns false on a time-out (after
+// raising the plan's error flag) or at once when the flag is already up, so
+// a failed exchange costs one time-out, not one per later barrier.
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+__device__ bool wait_epoch(const unsigned* slot, unsigned e, int* err_flag, unsigned* timeout_word) {
+  if (*(volatile int*)err_flag) return false;
+  const unsigned long long t0 = globaltimer_ns();
+  while ((int)(ld_acquire_sys(slot) - e) < 0) {
+    if (globaltimer_ns() - t0 > kPeerTimeoutNs || *(volatile int*)err_flag) {
+      atomicExch(err_flag, 1);
+      *timeout_word = 1u;
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
 // one warp: lane q signals peer q and waits for peer q's signal
 __global__ void k_peer_barrier(unsigned* const* __restrict__ pads, int rank, int nranks, int* err_flag) {
   unsigned* mine = pads[rank];
@@ -70,22 +98,14 @@ __global__ void k_peer_barrier(unsigned* const* __restrict__ pads, int rank, int
   __syncthreads();
   __threadfence_system();            // this rank's published slot before the signal
   for (int q = threadIdx.x; q < nranks; q += blockDim.x) st_release_sys(pads[q] + rank, e);
-  for (int q = threadIdx.x; q < nranks; q += blockDim.x) {
-    long long spins = 0;
-    while ((int)(ld_acquire_sys(mine + q) - e) < 0) {
-      if (++spins > (1LL << 31)) {   // ~20 s: a peer never arrived
-        atomicExch(err_flag, 1);
-        mine[kTimeout] = 1u;
-        break;
-      }
-      __nanosleep(8);
-    }
-  }
+  for (int q = threadIdx.x; q < nranks; q += blockDim.x) wait_epoch(mine + q, e, err_flag, mine + kTimeout);
 }
 
 // out = sum over ranks (fixed order) of the current epoch's slots
 __global__ void k_peer_sum(const float* const* __restrict__ bufs, int nranks, size_t slot_elems,
-                           const unsigned* __restrict__ pad, float* __restrict__ out, size_t count) {
+                           const unsigned* __restrict__ pad, float* __restrict__ out, size_t count,
+                           const int* __restrict__ err_flag) {
+  if (*(volatile const int*)err_flag) return;   // a peer never arrived: its slot holds stale data
   const size_t off = (size_t)(pad[kEpoch] & 1u) * slot_elems;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -102,7 +122,8 @@ static int grid_for(size_t n) {
 int launch_peer_finish(ms2g_plan* p, float* out, size_t count, cudaStream_t st) {
   k_peer_barrier<<<1, 32, 0, st>>>(p->d_peer_pads, p->peer_rank, p->peer_n, p->w_peer_err);
   MS2G_TRY(check_launch("k_peer_barrier"));
-  k_peer_sum<<<grid_for(count), 256, 0, st>>>(p->d_peer_bufs, p->peer_n, p->xch_slot, p->xch_pad, out, count);
+  k_peer_sum<<<grid_for(count), 256, 0, st>>>(p->d_peer_bufs, p->peer_n, p->xch_slot, p->xch_pad, out, count,
+                                               p->w_peer_err);
   return check_launch("k_peer_sum");
 }
 

@@ -81,3 +81,35 @@ def test_view_shards_partition(P):
             shards = [P.view_shard(V, r, nr) for r in range(nr)]
             assert shards[0][0] == 0 and shards[-1][1] == V
             assert all(shards[k][1] == shards[k + 1][0] for k in range(nr - 1))
+
+
+def _raw_plan(P, n, V, B, factors, **kw):
+    """ms2g_plan_geometry through the C ABI directly (no Python device check)."""
+    import math
+    L = P.load()
+    d = P.GeomDesc(n, 2.0, V, kw.get("arc", 2 * math.pi), B, 4.0, 8.0, kw.get("pitch", 0.0), 0, 0, 1)
+    fs = (ctypes.c_int32 * len(factors))(*factors)
+    h = ctypes.c_void_p()
+    rc = L.ms2g_plan_geometry(ctypes.byref(d), fs, len(factors), ctypes.byref(h))
+    if rc == 0:
+        L.ms2g_plan_destroy(h)
+    return rc, L.ms2g_last_error().decode()
+
+
+def test_grid_line_rays_rejected_on_host(P):
+    """Reading Z14 at the boundary: an odd bin count with views at multiples
+    of 90 deg puts the central ray on the central grid line of an even grid;
+    the plan is refused with MS2G_ERR_CONFIG before any device work (so this
+    runs without a GPU).  Even B, or an odd grid side, has no such ray."""
+    rc, msg = _raw_plan(P, 64, 8, 97, (2, 1))
+    assert rc == 2 and "grid line" in msg and "view 0, bin 48" in msg
+    rc, msg = _raw_plan(P, 63, 8, 97, (1,))      # odd side: the centre is a pixel centre, not a line
+    assert rc != 2, msg
+    rc, msg = _raw_plan(P, 64, 8, 96, (2, 1))    # even B: no bin at u = 0
+    assert rc != 2, msg
+    rc, msg = _raw_plan(P, 64, 6, 97, (1,))      # views at 60 deg steps: 0 and 180 still align
+    assert rc == 2
+    rc, msg = _raw_plan(P, 64, 7, 97, (1,))      # only view 0 is axis-aligned, and it is
+    assert rc == 2
+    rc, msg = _raw_plan(P, 64, 7, 96, (1,))
+    assert rc != 2, msg

@@ -1,15 +1,23 @@
 #!/usr/bin/env python
 """PnP-MS2G hot-path benchmark (BASELINE.json metric) on B200.
 
-One step = one whole PnP-MS2G solve of the C4 workload (1024^2 image, 1440
-views x 1536 bins, stages 2x:30 then full:20, Gaussian denoiser, per-stage
-20-step power iteration) = every row of SURVEY §8(a), replayed as one CUDA
-graph with b resident in HBM.  value = PnP-MS2G iterations/s (50 per solve)
-over all ranks; views are sharded across ranks (torchrun --nproc-per-node N)
-with an NCCL allreduce of the partial backprojection: strong scaling.
+--cfg 4 (default; the metric's 1024^2 configuration): one step = one whole
+PnP-MS2G solve of C4 (1024^2 image, 1440 views x 1536 bins, stages 2x:30 then
+full:20, Gaussian denoiser, per-stage 20-step power iteration) = every row of
+SURVEY §8(a), replayed as one CUDA graph with b resident in HBM.  value =
+PnP-MS2G iterations/s (50 per solve).  With N ranks the views are sharded
+(rank r owns [rV/N, (r+1)V/N)) and the partial backprojections are summed by
+an NCCL allreduce inside the graph: strong scaling.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ms2g|reference]
+--cfg 5: C5 data parallelism, 8 images per rank (images 8r .. 8r+7 of the
+64), one batch-8 solve per step (stages 2x:20 then full:20, Poisson data, TV,
+20 power iterations per stage), no collective in the data path; value =
+image-iterations/s over all ranks: weak scaling.
 
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg 4|5] [--impl ms2g|reference]
+
+--gpus N > 1 without torchrun re-launches itself under
+`torch.distributed.run --nproc-per-node N` (one process per GPU).
 --impl reference times the fp64 CPU oracle (the only reference this paper
 has) on a bounded sample of the same workload, same metric and unit.
 """
@@ -30,9 +38,10 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 import ms2g_synth as S  # noqa: E402
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+from src_hash import src_hash  # noqa: E402
 
 METRIC = "sketched-gradient evals/s and PnP-MS2G iters/s at 512²/1024², frac. of HBM roofline"
-CFG = 4
 
 
 def peaks():
@@ -50,15 +59,29 @@ def nnz_counts():
 
 
 def workload_config(pr, nranks, l2_note, allreduce="nccl"):
-    return {"workload": f"C{pr.cfg}: {pr.n}x{pr.n} fp32 phantom ({pr.n_ellipses} seeded ellipses), fan-beam "
-                        f"{pr.n_views} views x {pr.n_bins} bins, stages "
-                        + " -> ".join(f"{s[0]}x:{s[1]}" for s in pr.stages)
-                        + f", Gaussian 3x3 denoiser alpha={pr.alpha}, 20 power iterations per stage",
-            "image": pr.n, "views": pr.n_views, "bins": pr.n_bins, "iters_per_solve": pr.n_steps,
-            "parallelism": (f"views sharded x{nranks} + " + ("NCCL allreduce" if allreduce == "nccl" else
-                                                              "NVLink peer-memory sum (NEXT-3)"))
-            if nranks > 1 else "1 GPU",
-            "l2": l2_note}
+    den = ("Gaussian 3x3 denoiser" if pr.den[0] == "gauss"
+           else f"TV-prox denoiser (lambda {pr.den[1]}, {pr.den[2]} Chambolle iterations)")
+    data = "Gaussian noise" if pr.noise[0] == "gauss" else f"Poisson transmission data (I0 {pr.noise[1]:g})"
+    cfg = {"workload": f"C{pr.cfg}: {pr.n}x{pr.n} fp32 phantom ({pr.n_ellipses} seeded ellipses), fan-beam "
+                       f"{pr.n_views} views x {pr.n_bins} bins, {data}, stages "
+                       + " -> ".join(f"{s[0]}x:{s[1]}" for s in pr.stages)
+                       + f", {den} alpha={pr.alpha}, {pr.power_iters} power iterations per stage",
+           "image": pr.n, "views": pr.n_views, "bins": pr.n_bins, "iters_per_solve": pr.n_steps,
+           "l2": l2_note}
+    if pr.batch > 1:
+        cfg["images_per_rank"] = pr.batch
+        cfg["images_total"] = pr.batch * nranks
+        cfg["parallelism"] = f"images data-parallel x{nranks} (no collective in the data path)" if nranks > 1 \
+            else "1 GPU"
+    else:
+        cfg["parallelism"] = (f"views sharded x{nranks} + " + ("NCCL allreduce" if allreduce == "nccl" else
+                                                               "NVLink peer-memory sum (NEXT-3)")) \
+            if nranks > 1 else "1 GPU"
+    return cfg
+
+
+def unit_of(pr):
+    return "image-iters/s" if pr.batch > 1 else "iters/s"
 
 
 # ----------------------------------------------------------------- clocks --
@@ -105,11 +128,22 @@ class ClockSampler:
 _last_s2 = [None]   # seconds of the last all-core factor-2 oracle gradient (for the 1-core ratio)
 
 
-def oracle_sample(pr, b_full, nthreads):
-    """Time the fp64 oracle on a bounded sample of the C4 solve: one factor-2
-    gradient, one full gradient and one Gaussian denoise; compose the solve
-    (20 + 30 factor-2 and 20 + 20 full gradient-equivalents, 50 denoises).
-    Returns (iters/s, seconds of CPU work, description)."""
+def oracle_data(pr, image=0):
+    """The workload's data for the oracle (seeded phantom, oracle projector)."""
+    import oracle as O
+    g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+    xt = S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg, image), texture=pr.texture)
+    p = O.forward(g, 1, xt)
+    if pr.noise[0] == "gauss":
+        return S.gaussian_data(p, pr.noise[1], S.config_seed(pr.cfg, image))
+    return S.poisson_data(p, pr.noise[1], S.config_seed(pr.cfg, image))
+
+
+def oracle_composed(pr, b_full, nthreads):
+    """Bounded sample of one solve of the workload (one image): one factor-2
+    gradient, one full gradient and one denoise, timed, composed into the
+    solve's counts (power iterations + steps per factor, one denoise per
+    step).  Returns (iters/s of one image, seconds of CPU work, description)."""
     import oracle as O
     g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
     x = S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg, 9)).astype(np.float64)
@@ -120,56 +154,59 @@ def oracle_sample(pr, b_full, nthreads):
         O.sketched_grad(g, s, x, b_full, nthreads=nthreads)
         t[s] = time.perf_counter() - a
     a = time.perf_counter()
-    O.gauss3(x, 0.8)
+    if pr.den[0] == "gauss":
+        O.gauss3(x, pr.den[1])
+    else:
+        O.tv_chambolle(x, pr.den[1], pr.den[2])
     t["den"] = time.perf_counter() - a
     total = time.perf_counter() - t0
     n2 = sum(st[1] for st in pr.stages if st[0] == 2)
     n1 = sum(st[1] for st in pr.stages if st[0] == 1)
     solve = (pr.power_iters + n2) * t[2] + (pr.power_iters + n1) * t[1] + pr.n_steps * t["den"]
     _last_s2[0] = t[2]
-    desc = (f"C{pr.cfg} oracle, {nthreads} threads: 1 factor-2 gradient ({t[2]:.2f} s) + 1 full gradient "
-            f"({t[1]:.2f} s) + 1 Gaussian denoise ({t['den']:.3f} s), composed into one solve "
+    desc = (f"C{pr.cfg} oracle, one image, {nthreads} threads: 1 factor-2 gradient ({t[2]:.2f} s) + 1 full "
+            f"gradient ({t[1]:.2f} s) + 1 denoise ({t['den']:.3f} s), composed into one solve "
             f"({pr.power_iters}+{n2} factor-2 and {pr.power_iters}+{n1} full gradient-equivalents, "
             f"{pr.n_steps} denoises) = {solve:.1f} s")
     return pr.n_steps / solve, total, desc
 
 
-def make_data(pr):
-    """Seeded phantom, exact projection by the GPU projector, Gaussian noise."""
-    import torch
-
-    import paper_2203_07308_b200 as P
-    xt = S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg), texture=pr.texture)
-    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(1,)) as full:
-        p = P.forward_project(full, 1, torch.from_numpy(xt).cuda()[None])[0].cpu().numpy()
-    if pr.noise[0] == "gauss":
-        return S.gaussian_data(p, pr.noise[1], S.config_seed(pr.cfg))
-    return S.poisson_data(p, pr.noise[1], S.config_seed(pr.cfg))
+def oracle_solve(pr, b_full, nthreads):
+    """One whole oracle solve of the workload (one image; Algorithm 1 with
+    the configuration's schedule, denoiser and power iterations), timed.
+    Returns (iters/s of one image, seconds)."""
+    import oracle as O
+    g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+    a = time.perf_counter()
+    O.pnp_ms2g(g, pr.stages, b_full, den=pr.den, alpha=pr.alpha, power_iters=pr.power_iters, nthreads=nthreads)
+    secs = time.perf_counter() - a
+    return pr.n_steps / secs, secs
 
 
 def run_reference(args, rank, nranks):
     if rank != 0:
         return
-    pr = S.PRESETS[CFG]
+    pr = S.PRESETS[args.cfg]
     import oracle as O
     nthreads = O.default_threads()
-    g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
-    xt = S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg))
-    b = S.gaussian_data(O.forward(g, 1, xt, nthreads=nthreads), pr.noise[1], S.config_seed(pr.cfg))
+    b = oracle_data(pr).astype(np.float64)
     vals, secs_l, desc = [], [], ""
     for k in range(args.warmup + args.steps):
-        v, secs, desc = oracle_sample(pr, b.astype(np.float64), nthreads)
+        v, secs, desc = oracle_composed(pr, b, nthreads)
         if k >= args.warmup:
             vals.append(v)
             secs_l.append(secs)
     value = statistics.median(vals)
-    line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
+    unit = unit_of(pr)
+    line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(secs_l),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
+            "higher_is_better": True, "scaling": "weak" if pr.batch > 1 else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": workload_config(pr, 1, "n/a (CPU)"),
-            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": nthreads, "kind": "oracle", "sample": desc},
-            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": value, "unit": unit, "cores": nthreads, "kind": "oracle",
+                             "sample": desc + "; each timed step is one such bounded sample (a whole oracle solve "
+                                              "is timed by the GPU arm's cpu_baseline)"},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -205,12 +242,16 @@ def detail_512(P, dev):
         b = torch.from_numpy(S.gaussian_data(p, pr3.noise[1], S.config_seed(3))).to(dev)[None].contiguous()
         g = torch.empty_like(x)
         sub = list(range(0, pr3.n_views, 8))
+        rs = P.register_subset(plan, sub)         # uploaded once (the solve's own subset lists are too)
         for s_ in (4, 2, 1):
-            t_all = time_calls(lambda: P.sketched_grad(plan, s_, x, b, g=g), 10)
-            t_sub = time_calls(lambda: P.sketched_grad(plan, s_, x, b, g=g, subset=sub), 10)
+            t_all = time_calls(lambda: P.sketched_grad(plan, s_, x, b, g=g), 20)
+            t_sub = time_calls(lambda: P.sketched_grad(plan, s_, x, b, g=g, subset=rs), 50)
+            t_adhoc = time_calls(lambda: P.sketched_grad(plan, s_, x, b, g=g, subset=sub), 20)
             out[f"C3_512_grad_s{s_}"] = {"evals_per_s": 1.0 / t_all, "subset_evals_per_s": 1.0 / t_sub,
+                                         "subset_adhoc_list_evals_per_s": 1.0 / t_adhoc,
                                          "segments_per_s": 2 * nnz[str(s_)] / t_all,
                                          "subset_segments_per_s": 2 * nnz[f"{s_}_subset0"] / t_sub}
+        rs.release()
         x0 = torch.zeros_like(x); xo = torch.empty_like(x)
         kw = dict(option=2, n_subsets=8, seed=S.config_seed(3), den=pr3.den, alpha=pr3.alpha)
         ts = time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr3.stages, b, x0, xo, **kw), 10, warm=3)
@@ -280,6 +321,76 @@ def shard_estimate(P, dev, pr, b_full, t_solve_1):
     return out
 
 
+def make_data_images(P, pr, images, dev):
+    """Seeded phantoms, exact projection by the GPU projector, noise (the
+    bench times the solver; it is not a parity check)."""
+    import torch
+    bs = []
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(1,)) as full:
+        for im in images:
+            xt = S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg, im), texture=pr.texture)
+            p = P.forward_project(full, 1, torch.from_numpy(xt).to(dev)[None])[0].cpu().numpy()
+            bs.append(S.gaussian_data(p, pr.noise[1], S.config_seed(pr.cfg, im)) if pr.noise[0] == "gauss"
+                      else S.poisson_data(p, pr.noise[1], S.config_seed(pr.cfg, im)))
+    return np.stack(bs)
+
+
+def roofline_entry(pr, ktime, steps, n_rays, hbm, hbm_src, nnz_seg):
+    """Roofline of the dominant projector kernel (largest device time per
+    solve), from the CUDA events around its launches inside the timed solves.
+
+    bound "hbm": achieved = ALGORITHMIC (compulsory) bytes per launch / the
+    average launch time -- adjoint: read the residual sinogram (4 B per ray)
+    and write the image (4 B per pixel); forward: read the image and b, write
+    the residual.  This is the honest HBM fraction of the method: it computes
+    its matrix, so it is tiny.  Beside it:
+      binding     -- the resource that actually bounds the kernel (ncu: the
+                     L1/shared data pipe), stamped with the source hash of the
+                     capture and marked stale if the kernels changed since;
+      spmv_equivalent -- the north star's reading (8 B per ray-pixel segment
+                     that an explicitly stored sparse A would stream), a
+                     throughput figure in byte units, NOT a roofline fraction.
+    """
+    share = {k: sum(ktime[(k, f_)][0] for f_ in (2, 1)) / steps for k in ("forward", "backward")}
+    dom = max(share, key=share.get)
+    s_dom = 1
+    tot_ms, n_l = ktime[(dom, s_dom)]
+    tk = tot_ms / max(n_l, 1) / 1e3
+    npix = pr.n * pr.n * pr.batch
+    compulsory = (4 * n_rays + 4 * npix) if dom == "backward" else (4 * npix + 8 * n_rays)
+    achieved = compulsory / tk / 1e9
+    seg = nnz_seg * pr.batch
+    spmv = (8.0 * seg + compulsory) / tk / 1e9
+    traffic, binding = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tj = json.load(f)
+        stamp = tj.get("source_hash")
+        stale = stamp != src_hash()
+        if pr.batch == 1:
+            traffic = tj.get(f"k_{dom}", {}).get(str(s_dom))
+        binding = {"resource": "L1/shared data pipe (l1tex__data_pipe_lsu_wavefronts, fraction of one wavefront "
+                               "per SM clock)",
+                   "frac": tj.get(f"k_{dom}:l1_pipe_frac", {}).get(str(s_dom)),
+                   "source": "profiles/ncu_traffic.json (ncu --set full, C4 single image)",
+                   "source_hash": stamp, "stale": stale}
+        if stale:
+            traffic = None
+    except Exception:
+        pass
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": traffic, "kernel": f"k_{dom}", "factor": s_dom,
+            "reading": "algorithmic = compulsory bytes per launch (residual sinogram read + image write for the "
+                       "adjoint) / average launch time, CUDA events around each launch inside the timed solve "
+                       f"graphs; peak = {hbm_src} copy bandwidth (MEASURED_PEAKS.json)",
+            "launches_timed": n_l, "launch_ms": tk * 1e3, "share_ms_per_solve": share,
+            "binding": binding,
+            "spmv_equivalent": {"gbs": spmv, "segments_per_launch": seg, "segments_per_s": seg / tk,
+                                "note": "north-star reading: 8 B per ray-pixel segment + compulsory bytes; a "
+                                        "throughput in byte units (the matrix is computed, never streamed), "
+                                        "not a fraction of HBM"}}
+
+
 def run_ms2g(args, rank, nranks, local_rank):
     import torch
     import torch.distributed as dist
@@ -287,21 +398,31 @@ def run_ms2g(args, rank, nranks, local_rank):
     import paper_2203_07308_b200 as P
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    pr = S.PRESETS[CFG]
+    pr = S.PRESETS[args.cfg]
     P.load()
-    b_full = make_data(pr)
-    vb, ve = P.view_shard(pr.n_views, rank, nranks)
-    plan = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve)
-    if nranks > 1:
+    batched = pr.batch > 1
+    if batched:          # C5: images 8r .. 8r+7 of this rank, every view
+        images = list(range(rank * pr.batch, (rank + 1) * pr.batch))
+        b_np = make_data_images(P, pr, images, dev)
+        vb, ve = 0, pr.n_views
+    else:                # C4: the rank's contiguous view shard of image 0
+        b_full = make_data_images(P, pr, [0], dev)[0]
+        vb, ve = P.view_shard(pr.n_views, rank, nranks)
+        b_np = b_full[None, vb:ve]
+    plan = P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve,
+                           batch=pr.batch)
+    if nranks > 1 and not batched:
         if args.allreduce == "peer":     # NEXT-3: fused NVLink peer-memory sum (fixed rank order)
             P.attach_peers(plan, rank, nranks)
         else:
             P.attach_nccl(plan, rank, nranks)
-    b = torch.from_numpy(np.ascontiguousarray(b_full[vb:ve])).to(dev)[None].contiguous()
-    x0 = torch.zeros((1, pr.n, pr.n), device=dev)
+    b = torch.from_numpy(np.ascontiguousarray(b_np)).to(dev).contiguous()
+    x0 = torch.zeros((pr.batch, pr.n, pr.n), device=dev)
     xo = torch.empty_like(x0)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     kw = dict(den=pr.den, alpha=pr.alpha, power_iters=pr.power_iters)
+    unit = unit_of(pr)
+    per_step_units = pr.n_steps * pr.batch          # iterations (x images) per solve and rank
 
     def step():
         P.pnp_ms2g_solve_async(plan, pr.stages, b, x0, xo, **kw)
@@ -338,7 +459,9 @@ def run_ms2g(args, rank, nranks, local_rank):
     if nranks > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_total = float(t.item())
-    value = pr.n_steps * args.steps / t_total
+    # whole job: every rank's units (C4: the N ranks together do one solve per
+    # step; C5: each rank solves its own 8 images per step)
+    value = per_step_units * (nranks if batched else 1) * args.steps / t_total
     clocks = clk.summary()
 
     # ---- the same K steps again with CUDA events around every projector
@@ -369,7 +492,7 @@ def run_ms2g(args, rank, nranks, local_rank):
 
     # ---- e2e: public API with host buffers (pinned H2D of b, D2H of x) ----
     b_host = b.cpu().pin_memory()
-    x_host = torch.empty((1, pr.n, pr.n), dtype=torch.float32).pin_memory()
+    x_host = torch.empty(tuple(x0.shape), dtype=torch.float32).pin_memory()
     b_dev2 = torch.empty_like(b)
     x_dev2 = torch.empty_like(x0)
 
@@ -391,7 +514,7 @@ def run_ms2g(args, rank, nranks, local_rank):
     te = torch.tensor([e0.elapsed_time(e1) / 1000.0], dtype=torch.float64, device=dev)
     if nranks > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = pr.n_steps * args.steps / float(te.item())
+    e2e_val = per_step_units * (nranks if batched else 1) * args.steps / float(te.item())
 
     # ---- the same solve reusing the plan's cached step (power_iters = 0): L
     # depends on the geometry only, so repeated reconstructions on one scanner
@@ -431,73 +554,39 @@ def run_ms2g(args, rank, nranks, local_rank):
             P.solve_status(plan)
         except P.MS2GError:
             pass    # 50 iterations of one stage alone may leave the safe range of the toy; timing only
-        stage_rate[f"s{fac}"] = 50 * args.steps / (c0.elapsed_time(c1) / 1000.0)
+        stage_rate[f"s{fac}"] = 50 * pr.batch * args.steps / (c0.elapsed_time(c1) / 1000.0)
 
     # ---- per-kernel timing of the projector pair + operator throughputs ----
-    nnz = nnz_counts()[f"C{pr.cfg}"]
+    nnz = nnz_counts()[f"C{3 if batched else pr.cfg}"]      # C5 has C3's geometry
     frac_views = (ve - vb) / pr.n_views
     detail = {"stage_iters_per_s": stage_rate,
-              "solve_cached_step": {"iters_per_s": pr.n_steps * args.steps / t_cached,
+              "solve_cached_step": {unit.replace("/s", "_per_s").replace("-", "_"):
+                                    per_step_units * (nranks if batched else 1) * args.steps / t_cached,
                                     "ms_per_solve": 1000.0 * t_cached / args.steps,
                                     "note": "power_iters=0: per-stage step 1/L reused from the plan's cache "
                                             "(computed by the headline solves); L2 not flushed"}}
-    x1 = torch.from_numpy(S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg, 9))).to(dev)[None].contiguous()
+    x1 = torch.from_numpy(np.stack([S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg, 9))] * pr.batch)).to(dev)
     g = torch.empty_like(x1)
     for s in (2, 1):
         nc = pr.n // s
         tg = time_calls(lambda: P.sketched_grad(plan, s, x1, b, g=g), 10)
         xs = x1 if s == 1 else P.sketch_down(plan, 2, x1)
-        res = torch.empty((1, ve - vb, pr.n_bins), device=dev)
-        img = torch.empty((1, nc, nc), device=dev)
+        res = torch.empty((pr.batch, ve - vb, pr.n_bins), device=dev)
+        img = torch.empty((pr.batch, nc, nc), device=dev)
         tf = time_calls(lambda: P.forward_project(plan, s, xs, b=b, out=res), 10)
         tb = time_calls(lambda: P.back_project(plan, s, res, img=img), 10)
-        seg = nnz[str(s)] * frac_views
-        detail[f"grad_s{s}"] = {"evals_per_s": 1.0 / tg, "ms": tg * 1e3,
+        seg = nnz[str(s)] * frac_views * pr.batch
+        detail[f"grad_s{s}"] = {"evals_per_s": pr.batch / tg, "ms": tg * 1e3,
                                 "forward_ms": tf * 1e3, "backward_ms": tb * 1e3,
                                 "segments_per_launch": seg,
                                 "forward_nnz_per_s": seg / tf, "backward_nnz_per_s": seg / tb}
     del flush
     hbm, hbm_src = peaks()
-    # dominant kernel: the one with the larger share of the solve (launch counts
-    # per solve: power iterations + iterations, per factor)
-    calls = {2: pr.power_iters + sum(s_[1] for s_ in pr.stages if s_[0] == 2),
-             1: pr.power_iters + sum(s_[1] for s_ in pr.stages if s_[0] == 1)}
-    share = {}       # device ms per solve of each kernel, from the instrumented timed steps
-    for kern in ("forward", "backward"):
-        share[kern] = sum(ktime[(kern, f_)][0] for f_ in (2, 1)) / args.steps
-    dom = max(share, key=share.get)
-    s_dom = 1
-    d = detail[f"grad_s{s_dom}"]
-    tot_ms, n_l = ktime[(dom, s_dom)]
-    tk = tot_ms / max(n_l, 1) / 1e3       # average launch duration inside the timed solves
-    seg = d["segments_per_launch"]
-    n_rays = (ve - vb) * pr.n_bins
-    compulsory = 4 * n_rays * (2 if dom == "forward" else 1) + 4 * pr.n * pr.n * (1 if dom == "backward" else 2)
-    algo_bytes = 8.0 * seg + compulsory
-    achieved = algo_bytes / tk / 1e9
-    traffic, l1frac = None, None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tj = json.load(f)
-        traffic = tj.get(f"k_{dom}", {}).get(str(s_dom))
-        l1frac = tj.get(f"k_{dom}:l1_pipe_frac", {}).get(str(s_dom))
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": f"k_{dom}", "factor": s_dom,
-                "reading": "SpMV-equivalent bytes: 8 B per ray-pixel segment (oracle-counted) + compulsory "
-                           "bytes, per launch / average launch time measured by CUDA events around each launch "
-                           f"inside the timed solve graphs; peak = {hbm_src} copy bandwidth",
-                "launches_timed": n_l, "launch_ms": tk * 1e3,
-                "instrumented_ms_per_step": t_instr / args.steps,
-                "compulsory_frac": compulsory / tk / 1e9 / hbm,
-                "frac_vs_nominal_8tbs": achieved / 8000.0,   # also against the nominal HBM3e peak
-                # what actually bounds the kernel (ncu --set full, profiles/r01_ncu_full_projectors.md):
-                # L1/shared data-pipe wavefronts, fraction of the per-SM peak of one per clock
-                "l1_data_pipe_frac": l1frac,
-                "share_ms_per_solve": share}
+    roofline = roofline_entry(pr, ktime, args.steps, (ve - vb) * pr.n_bins * pr.batch, hbm, hbm_src,
+                              nnz["1"] * frac_views)
+    roofline["instrumented_ms_per_step"] = t_instr / args.steps
 
-    if nranks == 1 and not args.no_detail:
+    if nranks == 1 and not args.no_detail and not batched:
         detail.update(detail_512(P, dev))
         detail["C4_view_shard_estimate"] = shard_estimate(P, dev, pr, b_full, t_total / args.steps)
 
@@ -505,24 +594,35 @@ def run_ms2g(args, rank, nranks, local_rank):
     if rank == 0 and nranks == 1 and not args.no_cpu:
         import oracle as O
         nth = O.default_threads()
-        v, secs, desc = oracle_sample(pr, b_full.astype(np.float64), nth)
-        cpu = {"value": v, "unit": "iters/s", "cores": nth, "kind": "oracle", "sample": desc}
-        # one core: a factor-2 gradient on every 16th view, scaled to the solve
+        b0 = b_np[0].astype(np.float64)
+        vc, secs_c, desc_c = oracle_composed(pr, b0, nth)
+        if args.cpu_sample == "solve":
+            v, secs = oracle_solve(pr, b0, nth)
+            cpu = {"value": v, "unit": "iters/s (one image)" if batched else "iters/s", "cores": nth,
+                   "kind": "oracle",
+                   "sample": f"one whole C{pr.cfg} oracle solve of image 0 (Algorithm 1, {pr.n_steps} steps, "
+                             f"{pr.power_iters} power iterations per stage, fp64, {nth} threads): {secs:.1f} s",
+                   "composed_estimate": {"value": vc, "sample": desc_c}}
+        else:
+            cpu = {"value": vc, "unit": "iters/s (one image)" if batched else "iters/s", "cores": nth,
+                   "kind": "oracle", "sample": desc_c}
+        # one core: a factor-2 gradient on every 16th view, scaled to all views
         g_ = O.Geometry(pr.n, pr.n_views, pr.n_bins)
         xs_ = S.phantom(pr.n, pr.n_ellipses, S.config_seed(pr.cfg, 9)).astype(np.float64)
         views_ = np.arange(0, pr.n_views, 16)
         a_ = time.perf_counter()
-        O.sketched_grad(g_, 2, xs_, b_full.astype(np.float64), views=views_, nthreads=1)
-        t1_ = (time.perf_counter() - a_) * 16          # all views, factor 2, one core
-        cpu["one_core"] = {"s2_gradient_s": t1_, "sample": "1 factor-2 gradient on 90 of 1440 views x 16",
+        O.sketched_grad(g_, 2, xs_, b0, views=views_, nthreads=1)
+        t1_ = (time.perf_counter() - a_) * 16
+        cpu["one_core"] = {"s2_gradient_s": t1_, "sample": f"1 factor-2 gradient on every 16th view x 16",
                            "speedup_all_cores": t1_ / secs_s2 if (secs_s2 := _last_s2[0]) else None}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": nranks, "steps": args.steps,
+        line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": nranks, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1000.0 * t_total / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "scaling": "weak" if batched else "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
                 "config": workload_config(pr, nranks, "flushed between timed steps (256 MiB write)", args.allreduce),
-                "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": int(b.numel() * 4),
+                "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": int(b.numel() * 4),
                         "d2h_bytes_per_step": int(x0.numel() * 4)},
                 "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline,
                 "cpu_baseline": cpu, "detail": detail}
@@ -530,30 +630,80 @@ def run_ms2g(args, rank, nranks, local_rank):
     plan.destroy()
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def dry_run(args, rank, nranks):
+    """--dry-run: the launcher and sharding plumbing without a GPU (gloo):
+    every rank reports its shard; rank 0 prints them as one JSON line."""
+    import torch.distributed as dist
+    pr = S.PRESETS[args.cfg]
+    if pr.batch > 1:
+        mine = {"rank": rank, "images": list(range(rank * pr.batch, (rank + 1) * pr.batch))}
+    else:
+        import paper_2203_07308_b200 as P
+        vb, ve = P.view_shard(pr.n_views, rank, nranks)
+        mine = {"rank": rank, "views": [vb, ve]}
+    out = [None] * nranks
+    if nranks > 1:
+        dist.all_gather_object(out, mine)
+    else:
+        out = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": nranks, "cfg": args.cfg, "shards": out}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--cfg", type=int, default=4, choices=[4, 5],
+                    help="4: C4 1024^2 view-sharded solve (the metric's configuration); 5: C5 8 images per rank")
     ap.add_argument("--impl", default="ms2g", choices=["ms2g", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle run")
+    ap.add_argument("--cpu-sample", default="solve", choices=["solve", "composed"],
+                    help="cpu_baseline: one whole timed oracle solve (default; ~200 s at C4 on 16 cores) or the "
+                         "composed bounded sample")
     ap.add_argument("--allreduce", default="nccl", choices=["nccl", "peer"],
                     help="cross-rank sum of the partial backprojections (N > 1): NCCL, or the NEXT-3 "
                          "peer-memory path (untested at N > 1 on this 1-GPU pool)")
     ap.add_argument("--no-detail", action="store_true", help="skip the 512^2 detail numbers")
     ap.add_argument("--profile-once", action="store_true",
                     help="run one warm-up solve and one solve, print nothing (for ncu launch lists)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher/sharding plumbing only (gloo, no GPU): print every rank's shard")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rendezvous on 127.0.0.1)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     nranks = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, nranks)
         return
+    if args.dry_run:
+        import torch.distributed as dist
+        if nranks > 1:
+            dist.init_process_group("gloo")
+        dry_run(args, rank, nranks)
+        if nranks > 1:
+            dist.destroy_process_group()
+        return
     if nranks > 1:
         import torch
         import torch.distributed as dist
+        if torch.cuda.device_count() < nranks:
+            raise SystemExit(f"bench.py: {nranks} ranks need {nranks} GPUs, found {torch.cuda.device_count()}")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ms2g(args, rank, nranks, local_rank)

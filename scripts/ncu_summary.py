@@ -73,7 +73,13 @@ def full(rep, out, traffic_json=None):
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic_json:   # launches of each kernel in capture order: factor 2, then factor 1 (profile_run.py)
-        out_t = {"source": f"{rep} (scripts/profile_run.py --mode kernels; C4); dram read+write bytes per launch"}
+        import os
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from src_hash import src_hash
+        hfile = os.path.join(os.path.dirname(os.path.abspath(rep)), "prof_hash.txt")
+        stamp = open(hfile).read().strip() if os.path.exists(hfile) else src_hash()
+        out_t = {"source": f"{rep} (scripts/profile_run.py --mode kernels; C4); dram read+write bytes per launch",
+                 "source_hash": stamp}
         for k, v in traffic.items():
             out_t[k] = {str(f): b for f, (b, _) in zip((2, 1), v)}
             out_t[k + ":l1_pipe_frac"] = {str(f): q for f, (_, q) in zip((2, 1), v)}

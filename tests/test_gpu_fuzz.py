@@ -18,8 +18,17 @@ TOL = 1e-5
 
 
 def rel(a, b):
+    """Error measure of every parity assertion: the larger of the relative L2
+    error and one tenth of the largest element error over the reference's
+    RMS.  `rel(...) <= tol` thus gates both ||d|| <= tol ||ref|| and
+    max|d| <= 10 tol rms(ref) (a bad tile that the L2 norm dilutes fails)."""
     a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
-    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+    d = a - b
+    l2 = float(np.linalg.norm(d) / max(np.linalg.norm(b), 1e-300))
+    if d.size == 0:
+        return l2
+    rms = float(np.sqrt(np.mean(b ** 2)))
+    return max(l2, float(np.max(np.abs(d))) / max(rms, 1e-300) / 10.0)
 
 
 def _case(rng):

@@ -44,13 +44,26 @@ def _worker(rank, world, port, q):
         sch = P.schedule(None, pr.stages, pr.option, pr.n_subsets, S.config_seed(3))
         allsch = [None] * world
         dist.all_gather_object(allsch, sch)
-        uid = bytes(range(128)) if rank == 0 else None
+        # the NCCL unique id as attach_nccl makes it: rank 0 asks libms2g
+        # (ncclGetUniqueId, no GPU needed), the process group broadcasts it
+        import ctypes
+        L = P.load()
+        uid = None
+        if rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            assert L.ms2g_nccl_unique_id(buf) == 0
+            uid = bytes(buf)
         got = P.broadcast_unique_id(uid, rank, world)
+        ids = [None] * world
+        dist.all_gather_object(ids, got)
+        id_ok = all(i == ids[0] for i in ids) and len(got) == 128 and any(got)
+        # the attach entry point validates before touching NCCL or a device
+        id_ok &= L.ms2g_attach_nccl(None, (ctypes.c_uint8 * 128).from_buffer_copy(got), rank, world) == 7
         # NEXT-3 peer blob exchange: rank-ordered concatenation of equal-size blobs
         blob = bytes([rank + 1]) * 40
         allb = P.gather_blobs(blob, rank, world)
         blobs_ok = allb == b"".join(bytes([q_ + 1]) * 40 for q_ in range(world))
-        q.put((rank, err, all(s == allsch[0] for s in allsch), got == bytes(range(128)) and blobs_ok, (vb, ve)))
+        q.put((rank, err, all(s == allsch[0] for s in allsch), id_ok and blobs_ok, (vb, ve)))
     finally:
         dist.destroy_process_group()
 
@@ -77,3 +90,28 @@ def test_view_sharded_allreduce_gloo(world):
     for rank, err, same_sched, uid_ok, _ in res:
         assert err <= 1e-13, err
         assert same_sched and uid_ok
+
+
+@pytest.mark.parametrize("cfg,gpus", [(4, 2), (4, 8), (5, 8)])
+def test_bench_launcher_dry_run(cfg, gpus):
+    """`bench.py --gpus N` without torchrun re-launches itself as N ranks
+    (torch.distributed.run, 127.0.0.1); --dry-run stops after every rank has
+    derived its shard (C4: contiguous views covering all 1440; C5: images
+    8r..8r+7 covering all 64) and rank 0 printed them."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", "--gpus", str(gpus),
+                          "--cfg", str(cfg)], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == gpus and len(line["shards"]) == gpus
+    sh = sorted(line["shards"], key=lambda r: r["rank"])
+    if cfg == 4:
+        assert sh[0]["views"][0] == 0 and sh[-1]["views"][1] == 1440
+        assert all(sh[k]["views"][1] == sh[k + 1]["views"][0] for k in range(gpus - 1))
+    else:
+        assert sorted(i for r in sh for i in r["images"]) == list(range(8 * gpus))

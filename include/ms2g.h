@@ -82,20 +82,24 @@ int ms2g_attach_nccl(ms2g_plan* plan, const void* unique_id_128_bytes, int32_t r
 
 /* NEXT-3: the same cross-rank sum over NVLink peer memory,
  * fused into the backprojection (no separate collective).  The plan owns an
- * IPC-shareable exchange buffer (2 x n_cmax^2 x batch fp32) and a signal pad;
- * ms2g_peer_export writes this rank's ms2g_peer_blob_size() bytes (CUDA IPC
- * handles + slot size), the caller all-gathers the blobs in rank order
- * (nranks x size bytes, host memory) and every rank calls ms2g_attach_peers
- * (one process per GPU of one node, nranks <= 64).  From then on every
- * allreduce of the plan (back_project(..., allreduce=1), sketched_grad,
- * power_iteration, the solve) is: publish this rank's partial image into the
- * exchange slot (fused into the backprojector's chunk reduction), a barrier
- * on the signal pads, then a sum of every rank's slot by peer loads in FIXED
- * rank order -- all ranks get bitwise identical images.  Peers take
- * precedence over an attached NCCL communicator.  Synchronous; MS2G_ERR_CUDA
- * (IPC), MS2G_ERR_CONFIG (blob mismatch: plans of different shapes).  A
- * barrier that waits ~20 s for a rank that never arrives gives up and makes
- * the next ms2g_solve_status / synchronous solve return MS2G_ERR_NCCL. */
+ * IPC-shareable exchange buffer (2 x n_cmax^2 x batch fp32: this rank's
+ * partial, and its chunk of the sum) and a signal pad; ms2g_peer_export
+ * writes this rank's ms2g_peer_blob_size() bytes (CUDA IPC handles + region
+ * size), the caller all-gathers the blobs in rank order (nranks x size
+ * bytes, host memory) and every rank calls ms2g_attach_peers (one process per
+ * GPU of one node, nranks <= 64).  From then on every allreduce of the plan
+ * (back_project(..., allreduce=1), sketched_grad, power_iteration, the solve)
+ * is a reduce-scatter + all-gather over peer loads in three launches with
+ * the barrier folded in: publish (fused into the backprojector's chunk
+ * reduction; its last block signals the peers), reduce-scatter (each rank
+ * sums its 1/P chunk over the ranks in FIXED rank order, then signals),
+ * all-gather (fused with the step z = y - eta U_s G in the solve) -- all
+ * ranks get bitwise identical images.  Peers take precedence over an
+ * attached NCCL communicator.  Synchronous; MS2G_ERR_CUDA (IPC),
+ * MS2G_ERR_CONFIG (blob mismatch: plans of different shapes).  A wait that
+ * lasts 20 s of wall time (a rank never arrived) gives up: the next
+ * ms2g_solve_status / synchronous solve returns MS2G_ERR_NCCL and the plan
+ * refuses exchanges until every rank calls ms2g_attach_peers again. */
 int ms2g_peer_blob_size(void);
 int ms2g_peer_export(ms2g_plan* plan, void* blob_out);
 int ms2g_attach_peers(ms2g_plan* plan, const void* blobs_all_ranks, int32_t rank, int32_t nranks);

@@ -4,8 +4,11 @@
 //   momentum, and the fp64 reductions of the power iteration.
 // These are HBM/L2-streaming kernels; one thread per
 // output pixel, coalesced along rows, 32x32 shared tiles for transposes.
+#include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.cuh"
@@ -61,7 +64,7 @@ __global__ void k_up_step(const float* __restrict__ g, const float* __restrict__
   const float e = eta_dev ? *eta_dev : eta;
   const size_t idx = (b * n + i) * n + j;
   const float gv = g[(b * nc + i / s) * nc + (j / s)];
-  z[idx] = y ? (y[idx] - e * gv) : gv;
+  z[idx] = y ? fmaf(-e, gv, y[idx]) : gv;   // y - eta G with one rounding (as k_reduce_up_step)
 }
 
 int launch_up_step(int n, int s, int batch, const float* g, const float* y, const float* eta_dev, float eta,
@@ -338,12 +341,283 @@ int launch_fill(float* x, size_t count, float value, cudaStream_t st) {
   return check_launch("k_fill");
 }
 
+// ---------------------------------------------- TV-prox, persistent form --
+// All K dual iterations and the output step in ONE cooperative launch,
+// temporally blocked in row strips.  The batch's image rows form one list;
+// CTA c owns rows [R0, R1) = [c R, (c+1) R) and keeps p = (px, py), w =
+// div p - f / lambda (and f when it fits) for rows [R0 - k - 1, R1 + k) in
+// shared memory: p_new at a row needs p of the rows above and below only, so
+// k iterations computed on that halo'd strip, the valid region shrinking by
+// one row per side per iteration, leave p^{+k} exact on [R0 - 1, R1) without
+// any exchange.  The K iterations run in rounds of k; since p^0 = 0 (no warm
+// start) the first round needs no neighbour data at all, and when K fits one
+// round (k = K: 512^2 batch 1 and smaller) the kernel never synchronises with
+// another CTA.  Between rounds each CTA stores its own rows of p to global
+// memory (the plan's dual buffers, double-buffered by round parity), raises
+// its 64-bit flag (launch generation << 32 | round, st.release.gpu after one
+// fence by thread 0) and loads its halo rows after the flags of the CTAs
+// owning them (and of every CTA that reads its rows) reached the round
+// (ld.acquire.gpu).  A buffer is rewritten two rounds later, after every CTA
+// reading it has published the round in between.  The generation (one device
+// word, bumped by the last CTA to finish) keeps flags monotonic across
+// launches and graph replays.  Halo rows are computed redundantly with the
+// same arithmetic as their owner, term by term as k_tv_iter / k_tv_final
+// (same order, MUFU sqrt / rcp): results are bitwise equal to the K + 1-launch
+// form.  Waits are bounded by 2 s of %globaltimer (then *err is raised and
+// the kernel finishes instead of hanging the device).
+struct TvSync {
+  unsigned long long* flags;   // [CTAs]
+  unsigned* gen_ticket;        // {generation, finished-CTA ticket}
+  int* err;
+  float* pg[2];                // global p by round parity, layout [batch][2][n][n]
+};
+
+__device__ __forceinline__ unsigned long long tv_ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void tv_st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long tv_clock_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// global px / py of row R (global row index b n + i) in a [batch][2][n][n] buffer
+__device__ __forceinline__ float* tv_row(float* base, int R, int n, int comp) {
+  const int b = R / n, i = R - b * n;
+  return base + ((size_t)b * 2 + comp) * n * n + (size_t)i * n;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_tv_persist(const float* __restrict__ f, int n, int total_rows,
+                                                        int rows_per, int kround, int f_in_smem, float lambda,
+                                                        float inv_lambda, float tau, int iters, TvSync sy,
+                                                        const float* __restrict__ xprev, float* __restrict__ xout,
+                                                        float* __restrict__ yout, float alpha, float a, int mode,
+                                                        int* flag, int iter) {
+  extern __shared__ float sm[];
+  const int c = blockIdx.x, C = gridDim.x;
+  const int R0 = c * rows_per, R1 = min(total_rows, R0 + rows_per);
+  const int A = max(0, R0 - kround - 1), E = min(total_rows, R1 + kround);   // strip with halos [A, E)
+  const int W = rows_per + 2 * kround + 1;          // allocated rows per array
+  float* px = sm;                                    // local row r <-> global row A + r
+  float* py = px + (size_t)W * n;
+  float* w = py + (size_t)W * n;
+  float* fs = w + (size_t)W * n;                     // f (only when f_in_smem)
+  const int tx = threadIdx.x, ty = threadIdx.y, TX = blockDim.x, TY = blockDim.y;
+  const unsigned long long gen = (unsigned long long)*(volatile unsigned*)sy.gen_ticket << 32;
+  // f rows of the strip: shared memory (loaded once) or global (L2)
+  if (f_in_smem) {
+    for (int r = ty; r < E - A; r += TY)
+      for (int j = tx; j < n; j += TX) fs[(size_t)r * n + j] = f[(size_t)(A + r) * n + j];
+    __syncthreads();
+  }
+  const float* frow_base = f_in_smem ? fs : f + (size_t)A * n;
+  // CTAs whose rows this one reads or whose readers include it (symmetric range)
+  const int c_lo = max(0, (R0 - kround - 1) / rows_per), c_hi = min(C - 1, (R1 + kround) / rows_per);
+
+  int it = 0, round = 0;
+  while (it < iters) {
+    const int kr = min(kround, iters - it);
+    if (round > 0) {   // halo rows of p^it from the owners' published rows
+      if (tx == 0 && ty == 0) {
+        const unsigned long long target = gen | (unsigned long long)round;
+        const unsigned long long t0 = tv_clock_ns();
+        for (int q = c_lo; q <= c_hi; ++q) {
+          if (q == c) continue;
+          while (tv_ld_acquire(sy.flags + q) < target) {
+            if (*(volatile int*)sy.err || tv_clock_ns() - t0 > 2000000000ull) {
+              atomicExch(sy.err, 1);
+              break;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      float* pg = (round & 1) ? sy.pg[1] : sy.pg[0];
+      for (int r = ty; r < E - A; r += TY) {
+        const int R = A + r;
+        if (R >= R0 && R < R1) continue;            // own rows: already in shared memory
+        const float* gx = tv_row(pg, R, n, 0);
+        const float* gy = tv_row(pg, R, n, 1);
+        for (int j = tx; j < n; j += TX) {
+          px[(size_t)r * n + j] = __ldcg(gx + j);
+          py[(size_t)r * n + j] = __ldcg(gy + j);
+        }
+      }
+      __syncthreads();
+    }
+    for (int jj = 0; jj < kr; ++jj, ++it) {
+      const bool first = it == 0;
+      // p_new on [lo, hi): the valid region shrinks by one row per side per
+      // iteration, except at the ends of the row list (no rows beyond)
+      const int lo = (A == 0) ? 0 : A + jj + 1;
+      const int hi = (E == total_rows) ? total_rows : E - jj - 1;
+      const int whi = min(hi + 1, total_rows);       // w on [lo, whi)
+      for (int r = lo - A + ty; r < whi - A; r += TY) {
+        const int R = A + r, i = R % n;
+        const float* fr = frow_base + (size_t)r * n;
+        const float* pxr = px + (size_t)r * n;
+        const float* pyr = py + (size_t)r * n;
+        for (int j = tx; j < n; j += TX) {
+          float d = 0.f;
+          if (!first) {
+            const float ax = (j < n - 1 ? pxr[j] : 0.f) - (j > 0 ? pxr[j - 1] : 0.f);
+            const float by = (i < n - 1 ? pyr[j] : 0.f) - (i > 0 ? pyr[j - n] : 0.f);
+            d = ax + by;
+          }
+          w[(size_t)r * n + j] = d - fr[j] * inv_lambda;
+        }
+      }
+      __syncthreads();
+      for (int r = lo - A + ty; r < hi - A; r += TY) {
+        const int i = (A + r) % n;
+        const float* wr = w + (size_t)r * n;
+        float* pxr = px + (size_t)r * n;
+        float* pyr = py + (size_t)r * n;
+        for (int j = tx; j < n; j += TX) {
+          const float wc = wr[j];
+          const float qx = (j < n - 1) ? wr[j + 1] - wc : 0.f;
+          const float qy = (i < n - 1) ? wr[j + n] - wc : 0.f;
+          float sq, rden;
+          asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(qx * qx + qy * qy));
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rden) : "f"(fmaf(tau, sq, 1.f)));
+          pxr[j] = ((first ? 0.f : pxr[j]) + tau * qx) * rden;
+          pyr[j] = ((first ? 0.f : pyr[j]) + tau * qy) * rden;
+        }
+      }
+      __syncthreads();
+    }
+    ++round;
+    if (it < iters) {   // publish own rows of p^it for the next round's halos
+      float* pg = (round & 1) ? sy.pg[1] : sy.pg[0];
+      for (int r = R0 - A + ty; r < R1 - A; r += TY) {
+        float* gx = tv_row(pg, A + r, n, 0);
+        float* gy = tv_row(pg, A + r, n, 1);
+        for (int j = tx; j < n; j += TX) {
+          __stcg(gx + j, px[(size_t)r * n + j]);
+          __stcg(gy + j, py[(size_t)r * n + j]);
+        }
+      }
+      // one thread releases for the block: bar.sync orders the block's stores
+      // before thread 0's gpu-scope fence + release (cumulativity)
+      __syncthreads();
+      if (tx == 0 && ty == 0) {
+        __threadfence();
+        tv_st_release(sy.flags + c, gen | (unsigned long long)round);
+      }
+    }
+  }
+  // u = f - lambda div p^K on the own rows (row R0 - 1 of p is valid in the
+  // strip), then the mix + momentum epilogue
+  for (int r = R0 - A + ty; r < R1 - A; r += TY) {
+    const int R = A + r, i = R % n;
+    const float* pxr = px + (size_t)r * n;
+    const float* pyr = py + (size_t)r * n;
+    for (int j = tx; j < n; j += TX) {
+      float dv = 0.f;
+      if (iters > 0) {
+        const float ax = (j < n - 1 ? pxr[j] : 0.f) - (j > 0 ? pxr[j - 1] : 0.f);
+        const float by = (i < n - 1 ? pyr[j] : 0.f) - (i > 0 ? pyr[j - n] : 0.f);
+        dv = ax + by;
+      }
+      const size_t idx = (size_t)R * n + j;
+      const float fv = f[idx];
+      mix_momentum(idx, fv, fv - lambda * dv, xprev, xout, yout, alpha, a, mode, flag, iter);
+    }
+  }
+  // the last CTA to finish advances the generation for the next launch
+  __syncthreads();
+  if (tx == 0 && ty == 0) {
+    __threadfence();
+    if (atomicAdd(sy.gen_ticket + 1, 1u) == (unsigned)C - 1) {
+      sy.gen_ticket[1] = 0u;
+      atomicAdd(sy.gen_ticket, 1u);
+    }
+  }
+}
+
+// shared memory of a strip with k-row halos: px, py, w (+ f)
+static size_t tv_persist_smem(int n, int rows_per, int k, bool with_f) {
+  return sizeof(float) * (size_t)(rows_per + 2 * k + 1) * n * (with_f ? 4 : 3);
+}
+
+// Persistent TV workspace (TvWs in internal.cuh): usable when a strip with a
+// halo of at least one row fits one CTA's shared memory; the round length k
+// is the largest that fits (k = K: no exchange at all).
+int launch_tv_persist(const TvWs& ws, int n, int batch, float lambda, float tau, int iters, const float* f,
+                      float* p0, float* p1, const float* xprev, float* xout, float* yout, float alpha, float a,
+                      int mode, int* flag, int iter, cudaStream_t st, bool* used) {
+  *used = false;
+  static const bool off = getenv("MS2G_TV_PERSIST") && atoi(getenv("MS2G_TV_PERSIST")) == 0;   // experiment switch
+  static const int kmax_env = getenv("MS2G_TV_KROUND") ? atoi(getenv("MS2G_TV_KROUND")) : 0;    // experiment switch
+  if (off || !ws.flags || iters < 1) return MS2G_OK;
+  // Measured on B200 (scripts/tv_probe.py, K = 10): batch 8 at 512^2 126.7 vs
+  // 167.1 us, 1024^2 81.7 vs 106.5 us for the K + 1 launches; a single image
+  // at <= 512^2 is latency-bound either way (47-61 vs 50 us), so it keeps the
+  // per-iteration kernels (MS2G_TV_PERSIST=1 forces this form).
+  static const bool force = getenv("MS2G_TV_PERSIST") && atoi(getenv("MS2G_TV_PERSIST")) == 1;
+  if (!force && batch == 1 && n <= 512) return MS2G_OK;
+  const int total_rows = n * batch;
+  int C = std::min(ws.max_ctas, total_rows);
+  const int rows_per = (total_rows + C - 1) / C;
+  C = (total_rows + rows_per - 1) / rows_per;
+  if (C > ws.max_ctas) return MS2G_OK;
+  // the longest round that fits, with f in shared memory or (if that allows
+  // fewer rounds) read from L2
+  const int kcap = kmax_env > 0 ? std::min(iters, kmax_env) : iters;
+  auto kfit = [&](bool wf) {
+    int kk = kcap;
+    while (kk >= 1 && tv_persist_smem(n, rows_per, kk, wf) > (size_t)ws.smem_optin) --kk;
+    return kk;
+  };
+  const int k1 = kfit(true), k0 = kfit(false);
+  if (k0 < 1) return MS2G_OK;                      // not even a one-row halo fits
+  auto rounds = [&](int kk) { return (iters + kk - 1) / kk; };
+  const bool with_f = k1 >= 1 && rounds(k1) <= rounds(k0);
+  const int k = with_f ? k1 : k0;
+  const size_t smem = tv_persist_smem(n, rows_per, k, with_f);
+  static std::atomic<uint64_t> attr_devices{0};
+  int dev = 0;
+  MS2G_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_devices.load() & bit)) {
+    MS2G_CUDA(cudaFuncSetAttribute(k_tv_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, ws.smem_optin));
+    attr_devices.fetch_or(bit);
+  }
+  TvSync sy{ws.flags, ws.gen_ticket, ws.err, {p0, p1}};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(256, 4);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident: the round waits cannot deadlock
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MS2G_CUDA(cudaLaunchKernelEx(&cfg, k_tv_persist, f, n, total_rows, rows_per, k, with_f ? 1 : 0, lambda,
+                               1.f / lambda, tau, iters, sy, xprev, xout, yout, alpha, a, mode, flag, iter));
+  MS2G_TRY(check_launch("k_tv_persist"));
+  *used = true;
+  return MS2G_OK;
+}
+
 int launch_tv(int n, int batch, float lambda, float tau, int iters, const float* f, float* p0, float* p1,
               const float* xprev, float* xout, float* yout, float alpha, float a, int mode, int* flag, int iter,
-              cudaStream_t st) {
+              cudaStream_t st, const TvWs* ws) {
   const size_t total = (size_t)n * n * batch;
   if (lambda == 0.f) {  // prox of the zero function: identity
     return launch_copy_mix_mom(n, batch, f, xprev, xout, yout, a, mode, flag, iter, st);
+  }
+  if (ws) {
+    bool used = false;
+    MS2G_TRY(launch_tv_persist(*ws, n, batch, lambda, tau, iters, f, p0, p1, xprev, xout, yout, alpha, a, mode,
+                               flag, iter, st, &used));
+    if (used) return MS2G_OK;
   }
   // p^0 = 0 at every call (no warm start): the first iteration does not read p
   if (iters < 1) MS2G_TRY(launch_fill(p0, 2 * total, 0.f, st));
@@ -362,84 +636,8 @@ int launch_tv(int n, int batch, float lambda, float tau, int iters, const float*
 }
 
 // ------------------------------------------------------ power iteration --
-// O8 / Z6: L = <v, w>, v <- w / ||w||, fp64 partial sums with a fixed
-// per-thread order and a fixed tree: deterministic.
-__global__ void k_dot_norm(const float* __restrict__ v, const float* __restrict__ w, size_t np,
-                           double* __restrict__ red) {
-  __shared__ double sd[256], sn[256];
-  double d = 0.0, q = 0.0;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
-    const double wi = w[i];
-    d += (double)v[i] * wi;
-    q += wi * wi;
-  }
-  sd[threadIdx.x] = d;
-  sn[threadIdx.x] = q;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      sd[threadIdx.x] += sd[threadIdx.x + o];
-      sn[threadIdx.x] += sn[threadIdx.x + o];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    red[2 * blockIdx.x] = sd[0];
-    red[2 * blockIdx.x + 1] = sn[0];
-  }
-}
-
-__global__ void k_power_finalize(const double* __restrict__ red, int nblocks, double* __restrict__ pw,
-                                 double* L_out, double* eta_out, float* etaf_out) {
-  // fixed-order tree over the block partials (deterministic)
-  __shared__ double sd[256], sn[256];
-  double d = 0.0, q = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) {
-    d += red[2 * b];
-    q += red[2 * b + 1];
-  }
-  sd[threadIdx.x] = d;
-  sn[threadIdx.x] = q;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      sd[threadIdx.x] += sd[threadIdx.x + o];
-      sn[threadIdx.x] += sn[threadIdx.x + o];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x != 0) return;
-  d = sd[0];
-  q = sn[0];
-  pw[0] = d;
-  pw[1] = q > 0.0 ? 1.0 / sqrt(q) : 0.0;
-  if (L_out) *L_out = d;
-  if (eta_out) *eta_out = 1.0 / d;
-  if (etaf_out) *etaf_out = (float)(1.0 / d);
-}
-
-__global__ void k_scale(const float* __restrict__ w, const double* __restrict__ pw, float* __restrict__ v,
-                        size_t np) {
-  const float inv = (float)pw[1];
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x)
-    v[i] = w[i] * inv;
-}
-
-int launch_power_step(int nc, int /*batch*/, const float* v, const float* w, double* red, int red_blocks,
-                      double* pw, double* L_out, float* vnext, double* eta_out, float* etaf_out,
-                      cudaStream_t st) {
-  const size_t np = (size_t)nc * nc;
-  k_dot_norm<<<red_blocks, 256, 0, st>>>(v, w, np, red);
-  MS2G_TRY(check_launch("k_dot_norm"));
-  k_power_finalize<<<1, 256, 0, st>>>(red, red_blocks, pw, L_out, eta_out, etaf_out);
-  MS2G_TRY(check_launch("k_power_finalize"));
-  if (vnext) {
-    k_scale<<<grid1d(np), 256, 0, st>>>(w, pw, vnext, np);
-    MS2G_TRY(check_launch("k_scale"));
-  }
-  return MS2G_OK;
-}
-
+// (the step itself, O8 / Z6, is k_reduce_power in projector.cu: fused with
+// the backprojection's chunk sum, last-block fp64 finalisation)
 // {L, eta, (float) eta} from a factor's cache into a stage's slots (each may be NULL)
 __global__ void k_cached_step(const double* __restrict__ cache, double* L_out, double* eta_out, float* etaf_out) {
   if (L_out) *L_out = cache[0];

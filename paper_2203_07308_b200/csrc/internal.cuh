@@ -91,6 +91,14 @@ struct FactorTables {
   float* d_w_up = nullptr;
 };
 
+// workspace of the persistent TV-prox kernel (plan-owned, zero-initialised)
+struct TvWs {
+  unsigned long long* flags = nullptr;   // [max_ctas]
+  unsigned* gen_ticket = nullptr;        // {generation, ticket}
+  int* err = nullptr;
+  int max_ctas = 0, smem_optin = 0;      // (the round halos go through the plan's dual buffers w_p)
+};
+
 struct SolveGraph {
   std::string key;
   cudaGraph_t graph = nullptr;
@@ -123,11 +131,13 @@ struct ms2g_plan {
   float* w_snap = nullptr;             // SVRG snapshot (full res)
   float* w_mu = nullptr;               // SVRG snapshot gradient (coarse)
   float* w_p[2] = {nullptr, nullptr};  // TV dual double buffer [batch][2][n][n]
+  ms2g::TvWs tvws;                     // persistent TV-prox kernel workspace
   double* w_red = nullptr;             // reduction partials
   int red_blocks = 0;
   double* w_scal = nullptr;            // device scalars: [0..63] L per stage, [64..127] eta
   float* w_etaf = nullptr;             // fp32 eta per stage [64]
   double* w_pw = nullptr;              // power-iteration scalars (dot, inv_norm)
+  unsigned* w_ticket = nullptr;        // last-block ticket of k_reduce_power (0 between launches)
   int* w_flag = nullptr;               // first non-finite global iteration (INT_MAX = none)
   // ad-hoc host subsets: a ring of kSelRing (pinned host, device) list slots;
   // slot k is reused only after the event recorded behind its last consumer
@@ -156,9 +166,10 @@ struct ms2g_plan {
   // NCCL
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
-  // peer-memory allreduce (NEXT-3): exchange buffer of two slots, signal pad
-  // (words 0..63: per-rank epochs written by the peers, 64: local epoch,
-  // 65: time-out), device tables of every rank's buffer / pad
+  // peer-memory allreduce (NEXT-3, peer_reduce.cu): exchange buffer of two
+  // regions (PUB: this rank's partial, RED: its chunk of the sum), signal pad
+  // (PUB / RED epochs by rank, local epoch, time-out, ticket), device tables
+  // of every rank's buffer / pad
   float* xch_buf = nullptr;
   size_t xch_slot = 0;                 // floats per slot
   unsigned* xch_pad = nullptr;
@@ -182,6 +193,7 @@ struct ms2g_plan {
     float* w_part = nullptr;
     double* w_red = nullptr;
     double* w_pw = nullptr;
+    unsigned* w_ticket = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
   };
@@ -195,6 +207,11 @@ struct ms2g_plan {
   std::vector<TimedLaunch> tev;
   // graph cache
   ms2g::SolveGraph sg;
+  // per-call graphs of the standalone gradient (all views or a registered
+  // subset: no host-side staging), most recent first, at most kGradGraphs
+  static constexpr int kGradGraphs = 16;
+  std::vector<ms2g::SolveGraph> grad_graphs;
+  uint64_t topo_version = 0;           // bumped when a communicator / peers attach (graphs re-captured)
   int last_total_steps = 0;
   std::vector<ms2g_sched_entry> last_sched;
   std::vector<int> last_stage_of_step;
@@ -245,7 +262,11 @@ int timing_begin(ms2g_plan* p, int kind, int factor, cudaStream_t st);
 void timing_end(ms2g_plan* p, int slot, cudaStream_t st);
 
 // ---- kernel launchers (projector.cu) ----
-int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s);
+// pair images of v for the forward; v = x (factor 1), the factor x factor mean
+// of the full-resolution x (fused S_s), times *scale_dev if given; v_out
+// (optional) receives v
+int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s, int factor = 1,
+                     const double* scale_dev = nullptr, float* v_out = nullptr);
 // order_sel: longest-first block order for a subset launch (d_sel != NULL),
 // built for this view list (subset_orders in ms2g_api.cu); NULL = grid order
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
@@ -253,15 +274,26 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 int bp_tile_count(int nc);   // adjoint tiles (both families) of an n_c grid
 int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch);
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
-// publish != 0: write scale * A_s^T sino into the peer exchange slot (not img)
+// publish: 0 = img = scale A_s^T sino (+ img), 1 = write scale * A_s^T sino
+// into the peer exchange slot (not img), 2 = leave the partial planes in
+// p->w_part for a fused epilogue; *nplanes_out = their count
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish = 0,
-                    const int* order_sel = nullptr);
+                    const int* order_sel = nullptr, int* nplanes_out = nullptr);
+// fused epilogues of the backprojection (projector.cu)
+int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, float c, const float* y,
+                          const float* eta_dev, float* z, int s, cudaStream_t st);
+int launch_reduce_power(ms2g_plan* p, const float* part, int nplanes, size_t np, float* w_out, const float* v,
+                        double* red, int red_blocks, unsigned* ticket, double* pw, double* L_out, double* eta_out,
+                        float* etaf_out, cudaStream_t st);
 void bp_launch_chunks(const ms2g_plan* p, const FactorTables& f, int n_sel, int* ch);
 
 // ---- peer-memory allreduce (peer_reduce.cu, NEXT-3) ----
 int launch_peer_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st);
 int launch_peer_finish(ms2g_plan* p, float* out, size_t count, cudaStream_t st);
+// reduce-scatter + all-gather fused with z = y - eta U_s G (y == NULL: z = U_s G)
+int launch_peer_finish_step(ms2g_plan* p, size_t count, int nc, int s, const float* y, const float* eta_dev,
+                            float* z, cudaStream_t st);
 int launch_chunk_reduce_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
                                 cudaStream_t st);
 
@@ -277,17 +309,15 @@ int launch_resample_up_step(ms2g_plan* p, const FactorTables& f, int kind, int b
 int build_bicubic_tables(FactorTables& f, int n);
 int launch_gauss_mix_mom(int n, int batch, float sigma, const float* z, const float* xprev, float* xout,
                          float* yout, float alpha, float a, int mode, int* flag, int iter, cudaStream_t st);
+// ws != NULL: the persistent single-launch form when it fits, else K + 1 launches
 int launch_tv(int n, int batch, float lambda, float tau, int iters, const float* f, float* p0, float* p1,
               const float* xprev, float* xout, float* yout, float alpha, float a, int mode, int* flag,
-              int iter, cudaStream_t st);
+              int iter, cudaStream_t st, const TvWs* ws = nullptr);
 int launch_copy_mix_mom(int n, int batch, const float* z, const float* xprev, float* xout, float* yout,
                         float a, int mode, int* flag, int iter, cudaStream_t st);
 int launch_fill(float* x, size_t count, float value, cudaStream_t st);
 int launch_axpby(float* out, const float* x, const float* y, float a, float b, size_t count, cudaStream_t st);
 int launch_saga(float* nw, float* phi, float* avg, int K, size_t count, cudaStream_t st);
-int launch_power_step(int nc, int batch, const float* v, const float* w, double* red, int red_blocks,
-                      double* pw, double* L_out, float* vnext, double* eta_out,
-                      float* etaf_out, cudaStream_t st);
 int launch_init_flag(int* flag, cudaStream_t st);
 int launch_cached_step(const double* cache, double* L_out, double* eta_out, float* etaf_out, cudaStream_t st);
 

@@ -340,6 +340,10 @@ static void free_plan(ms2g_plan* p) {
   cudaFree(p->w_red);
   cudaFree(p->w_scal);
   cudaFree(p->w_pw);
+  cudaFree(p->w_ticket);
+  cudaFree(p->tvws.flags);
+  cudaFree(p->tvws.gen_ticket);
+  cudaFree(p->tvws.err);
   cudaFree(p->w_flag);
   cudaFree(p->w_sel);
   cudaFree(p->w_subsets);
@@ -355,6 +359,12 @@ static void free_plan(ms2g_plan* p) {
   }
   if (p->sg.exec) cudaGraphExecDestroy(p->sg.exec);
   if (p->sg.graph) cudaGraphDestroy(p->sg.graph);
+  for (auto& gg : p->grad_graphs) {   // per-call gradient graphs captured without it
+    if (gg.exec) cudaGraphExecDestroy(gg.exec);
+    if (gg.graph) cudaGraphDestroy(gg.graph);
+  }
+  p->grad_graphs.clear();
+  p->topo_version++;
   for (auto& br : p->pbr) {
     cudaFree(br.w_v);
     cudaFree(br.w_pair);
@@ -363,6 +373,7 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(br.w_part);
     cudaFree(br.w_red);
     cudaFree(br.w_pw);
+    cudaFree(br.w_ticket);
     if (br.stream) cudaStreamDestroy(br.stream);
     if (br.done) cudaEventDestroy(br.done);
   }
@@ -465,26 +476,56 @@ static int backward_sum(ms2g_plan* p, const FactorTables& f, const float* sino, 
   return allreduce(p, G, count, st);
 }
 
+// Single-rank plans reduce the backprojection's partial planes in a fused
+// epilogue (the step, the power iteration); with a communicator or peers the
+// partial image is summed over ranks first (G = allreduce), then consumed.
+static bool fused_epilogue(const ms2g_plan* p) { return p->peer_n == 0 && !p->comm; }
+
+// Pair images of v = S_s(src) for the forward: kind 0 fuses the s x s mean
+// into the pair prep (one launch); bicubic resamples into w_v first.
+static int prep_pairs(ms2g_plan* p, const FactorTables& f, int kind, int batch, const float* src, cudaStream_t st) {
+  if (f.factor > 1 && kind != 0) {
+    MS2G_TRY(launch_resample_down(p, f, kind, batch, src, p->w_v, st));   // v = S(y)
+    return launch_pair_prep(p, f.nc, batch, p->w_v, st);
+  }
+  return launch_pair_prep(p, f.nc, batch, src, st, f.factor);          // v = S(y) fused
+}
+
+// z = y - eta U_s (c A_s^T r)  (y == NULL: z = U_s (c A_s^T r)), summed over
+// ranks when attached: the G-step of Eq. 6/7.
+static int backward_step(ms2g_plan* p, const FactorTables& f, int kind, const float* sino, float c, const int* d_sel,
+                         int n_sel, int batch, const float* y, const float* eta_dev, float* z, cudaStream_t st,
+                         const int* bord) {
+  if (kind == 0 && fused_epilogue(p)) {
+    int npl = 0;
+    MS2G_TRY(launch_backward(p, f, sino, nullptr, c, 0, d_sel, n_sel, batch, st, 2, bord, &npl));
+    return launch_reduce_up_step(p->w_part, npl, f.nc, batch, c, y, eta_dev, z, f.factor, st);
+  }
+  if (kind == 0 && p->peer_n > 0) {   // NEXT-3: publish (fused chunk sum), reduce-scatter, all-gather + step
+    MS2G_TRY(peer_ok(p));
+    MS2G_TRY(launch_backward(p, f, sino, nullptr, c, 0, d_sel, n_sel, batch, st, 1, bord));
+    return launch_peer_finish_step(p, (size_t)f.nc * f.nc * batch, f.nc, f.factor, y, eta_dev, z, st);
+  }
+  float* G = (f.factor > 1 || y) ? p->w_G : z;
+  MS2G_TRY(backward_sum(p, f, sino, G, c, d_sel, n_sel, batch, st, bord));   // G = c A_s^T r (+ ranks)
+  if (f.factor > 1 || y) MS2G_TRY(launch_resample_up_step(p, f, kind, batch, G, y, eta_dev, 0.f, z, st));
+  return MS2G_OK;
+}
+
 // g = c U_s A_s^T (A_s S_s x - b), into a full-resolution image.
 static int enqueue_grad(ms2g_plan* p, const FactorTables& f, int kind, const float* x, const float* b, float* g,
                         const int* d_sel, int n_sel, float c, int batch, cudaStream_t st,
                         const int* ford = nullptr, const int* bord = nullptr) {
-  const int s = f.factor;
-  const float* v = x;
-  if (s > 1) {
-    MS2G_TRY(launch_resample_down(p, f, kind, batch, x, p->w_v, st));  // v = S(y)
-    v = p->w_v;
-  }
-  MS2G_TRY(launch_pair_prep(p, f.nc, batch, v, st));
+  MS2G_TRY(prep_pairs(p, f, kind, batch, x, st));
   MS2G_TRY(launch_forward(p, f, b, p->w_res, d_sel, n_sel, batch, st, ford));  // r = A_s v - b
-  float* G = (s > 1) ? p->w_G : g;
-  MS2G_TRY(backward_sum(p, f, p->w_res, G, c, d_sel, n_sel, batch, st, bord));  // G = c A_s^T r (+ ranks)
-  if (s > 1) MS2G_TRY(launch_resample_up_step(p, f, kind, batch, G, nullptr, nullptr, 0.f, g, st));  // U G
-  return MS2G_OK;
+  return backward_step(p, f, kind, p->w_res, c, d_sel, n_sel, batch, nullptr, nullptr, g, st, bord);
 }
 
 // O8 power iteration on the full view set (allreduced over ranks); the last
 // Rayleigh quotient goes to L_out / eta_out / etaf_out (device pointers).
+// Per iteration: forward, backprojection, the fused chunk-sum + dot/norm
+// step (k_reduce_power, last-block finalisation) and the pair prep of the
+// next v = w / ||w|| (scaled on the fly): 4 launches.
 static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double* L_out, double* eta_out,
                          float* etaf_out, cudaStream_t st) {
   const size_t np = (size_t)f.nc * f.nc;
@@ -493,13 +534,20 @@ static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double*
   MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_v, st));
   for (int k = 0; k < iters; ++k) {
     MS2G_TRY(launch_forward(p, f, nullptr, p->w_res, nullptr, p->V_r, 1, st));
-    MS2G_TRY(backward_sum(p, f, p->w_res, p->w_G, 1.f, nullptr, p->V_r, 1, st));
+    const float* part = p->w_G;
+    int npl = 1;
+    if (fused_epilogue(p)) {
+      MS2G_TRY(launch_backward(p, f, p->w_res, nullptr, 1.f, 0, nullptr, p->V_r, 1, st, 2, nullptr, &npl));
+      part = p->w_part;
+    } else {
+      MS2G_TRY(backward_sum(p, f, p->w_res, p->w_G, 1.f, nullptr, p->V_r, 1, st));   // G summed over ranks
+    }
     const bool last = (k == iters - 1);
     double* cache = f.d_Lcache;
-    MS2G_TRY(launch_power_step(f.nc, 1, p->w_v, p->w_G, p->w_red, p->red_blocks, p->w_pw, last ? cache : nullptr,
-                               last ? nullptr : p->w_v, last ? cache + 1 : nullptr,
-                               last ? reinterpret_cast<float*>(cache + 2) : nullptr, st));
-    if (!last) MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_v, st));
+    MS2G_TRY(launch_reduce_power(p, part, npl, np, p->w_G, p->w_v, p->w_red, p->red_blocks, p->w_ticket, p->w_pw,
+                                 last ? cache : nullptr, last ? cache + 1 : nullptr,
+                                 last ? reinterpret_cast<float*>(cache + 2) : nullptr, st));
+    if (!last) MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_G, st, 1, p->w_pw + 1, p->w_v));   // v = w / ||w||
   }
   // the last Rayleigh quotient went to the factor's cache (reused by solves
   // with power_iters = 0); hand it to the caller's slots
@@ -517,7 +565,7 @@ static int denoise_mix(ms2g_plan* p, const ms2g_denoiser& den, const float* z, c
       return launch_gauss_mix_mom(n, batch, den.sigma, z, xprev, xout, yout, alpha, a, mode, p->w_flag, iter, st);
     case 2:
       return launch_tv(n, batch, den.lambda, den.tau, den.inner_iters, z, p->w_p[0], p->w_p[1], xprev, xout, yout,
-                       alpha, a, mode, p->w_flag, iter, st);
+                       alpha, a, mode, p->w_flag, iter, st, &p->tvws);
     default:
       return set_error(MS2G_ERR_CONFIG, "unknown denoiser kind");
   }
@@ -690,6 +738,8 @@ static int ensure_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd) {
     MS2G_CUDA(cudaMalloc(&br.w_part, sizeof(float) * planes * np));
     MS2G_CUDA(cudaMalloc(&br.w_red, sizeof(double) * 2 * p->red_blocks));
     MS2G_CUDA(cudaMalloc(&br.w_pw, sizeof(double) * 8));
+    MS2G_CUDA(cudaMalloc(&br.w_ticket, sizeof(unsigned)));
+    MS2G_CUDA(cudaMemset(br.w_ticket, 0, sizeof(unsigned)));
     MS2G_CUDA(cudaStreamCreateWithFlags(&br.stream, cudaStreamNonBlocking));
     MS2G_CUDA(cudaEventCreateWithFlags(&br.done, cudaEventDisableTiming));
     p->pbr.push_back(br);
@@ -719,6 +769,7 @@ static int enqueue_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd, cudaS
     shadow.w_part = br.w_part;
     shadow.w_red = br.w_red;
     shadow.w_pw = br.w_pw;
+    shadow.w_ticket = br.w_ticket;
     const FactorTables* f = find_factor(p, br.factor);
     MS2G_TRY(enqueue_power(&shadow, *f, sd->power_iters, p->w_scal + first, p->w_scal + 64 + first,
                            p->w_etaf + first, br.stream));
@@ -760,12 +811,7 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
       const size_t ncimg = (size_t)f->nc * f->nc * batch;
       float* avg = p->w_saga + (size_t)sd->n_subsets * ncimg;
       MS2G_TRY(launch_fill(avg, ncimg, 0.f, st));
-      const float* v = p->w_y;
-      if (f->factor > 1) {
-        MS2G_TRY(launch_resample_down(p, *f, sd->resampler, batch, p->w_y, p->w_v, st));
-        v = p->w_v;
-      }
-      MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
+      MS2G_TRY(prep_pairs(p, *f, sd->resampler, batch, p->w_y, st));
       for (int q = 0; q < sd->n_subsets; ++q) {
         float* ph = p->w_saga + (size_t)q * ncimg;
         const float cq = (float)((double)p->d.n_views / (double)p->subset_global_len[q]);
@@ -798,45 +844,35 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
       }
       // G-step: z = y - eta_k U (c A_s^T (A_s S y - b_M))       (Options 1, 2)
       //         z = y - eta_k U (c A_M^T A_M S (y - xs) + mu)  (Option 3, SVRG)
-      const int s = f->factor;
       const size_t ncimg = (size_t)f->nc * f->nc * batch;
       const int kind = sd->resampler;
       if (sd->option == 3) {
         if (step_in_stage % sd->n_subsets == 0) {   // epoch start: snapshot xs = y, mu = g_s(xs) (all views)
           MS2G_CUDA(cudaMemcpyAsync(p->w_snap, p->w_y, sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
-          const float* vs = p->w_y;
-          if (s > 1) {
-            MS2G_TRY(launch_resample_down(p, *f, kind, batch, p->w_y, p->w_v, st));
-            vs = p->w_v;
-          }
-          MS2G_TRY(launch_pair_prep(p, f->nc, batch, vs, st));
+          MS2G_TRY(prep_pairs(p, *f, kind, batch, p->w_y, st));
           MS2G_TRY(launch_forward(p, *f, b, p->w_res, nullptr, p->V_r, batch, st));
           MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_mu, 1.f, nullptr, p->V_r, batch, st));
         }
         MS2G_TRY(launch_axpby(p->w_z, p->w_y, p->w_snap, 1.f, -1.f, img, st));   // d = y - xs
-        const float* vd = p->w_z;
-        if (s > 1) {
-          MS2G_TRY(launch_resample_down(p, *f, kind, batch, p->w_z, p->w_v, st));
-          vd = p->w_v;
-        }
-        MS2G_TRY(launch_pair_prep(p, f->nc, batch, vd, st));
+        MS2G_TRY(prep_pairs(p, *f, kind, batch, p->w_z, st));
         MS2G_TRY(launch_forward(p, *f, nullptr, p->w_res, d_sel, n_sel, batch, st, ford));
         MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st, bord));
         MS2G_TRY(launch_axpby(p->w_G, p->w_G, p->w_mu, 1.f, 1.f, ncimg, st));  // + mu
-      } else {
-        const float* v = p->w_y;
-        if (s > 1) {
-          MS2G_TRY(launch_resample_down(p, *f, kind, batch, p->w_y, p->w_v, st));
-          v = p->w_v;
-        }
-        MS2G_TRY(launch_pair_prep(p, f->nc, batch, v, st));
+      } else if (sd->option == 5) {
+        MS2G_TRY(prep_pairs(p, *f, kind, batch, p->w_y, st));
         MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st, ford));
         MS2G_TRY(backward_sum(p, *f, p->w_res, p->w_G, c, d_sel, n_sel, batch, st, bord));
-        if (sd->option == 5)   // G = new - phi_j + avg; phi_j = new; avg += (new - phi_j)/K
-          MS2G_TRY(launch_saga(p->w_G, p->w_saga + (size_t)e.subset * ncimg,
-                               p->w_saga + (size_t)sd->n_subsets * ncimg, sd->n_subsets, ncimg, st));
+        // G = new - phi_j + avg; phi_j = new; avg += (new - phi_j)/K
+        MS2G_TRY(launch_saga(p->w_G, p->w_saga + (size_t)e.subset * ncimg,
+                             p->w_saga + (size_t)sd->n_subsets * ncimg, sd->n_subsets, ncimg, st));
+      } else {   // Options 1, 2, 4: v = S y, r = A_s v - b_M, z = y - eta U (c A_s^T r) in 4 launches
+        MS2G_TRY(prep_pairs(p, *f, kind, batch, p->w_y, st));
+        MS2G_TRY(launch_forward(p, *f, b, p->w_res, d_sel, n_sel, batch, st, ford));
+        MS2G_TRY(backward_step(p, *f, kind, p->w_res, c, d_sel, n_sel, batch, p->w_y, p->w_etaf + k, p->w_z, st,
+                               bord));
       }
-      MS2G_TRY(launch_resample_up_step(p, *f, kind, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
+      if (sd->option == 3 || sd->option == 5)
+        MS2G_TRY(launch_resample_up_step(p, *f, kind, batch, p->w_G, p->w_y, p->w_etaf + k, 0.f, p->w_z, st));
       // x = (1-alpha) z + alpha D(z);  y = x + a_i (x - x_prev)
       MS2G_TRY(denoise_mix(p, sd->den, p->w_z, p->w_x[cur], p->w_x[cur ^ 1], p->w_y, sd->alpha, (float)e.a, 1,
                            e.i, batch, st));
@@ -943,10 +979,12 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
 }
 
 static int solve_status(ms2g_plan* p, cudaStream_t st) {
-  int flag = INT_MAX, perr = 0;
+  int flag = INT_MAX, perr = 0, tverr = 0;
   MS2G_CUDA(cudaMemcpyAsync(&flag, p->w_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (p->tvws.err) MS2G_CUDA(cudaMemcpyAsync(&tverr, p->tvws.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (p->w_peer_err) MS2G_CUDA(cudaMemcpyAsync(&perr, p->w_peer_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   MS2G_CUDA(cudaStreamSynchronize(st));
+  if (tverr) return set_error(MS2G_ERR_CUDA, "persistent TV-prox kernel: a neighbour wait timed out");
   if (perr) {
     p->peer_failed = true;     // epochs are out of step: refuse exchanges until every rank re-attaches
     return set_error(MS2G_ERR_NCCL, "peer allreduce: barrier timed out (a rank never arrived); "
@@ -1059,6 +1097,21 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
   e = cudaMalloc(&p->w_red, sizeof(double) * 2 * p->red_blocks);
   if (e == cudaSuccess) e = cudaMalloc(&p->w_scal, sizeof(double) * 128);
   if (e == cudaSuccess) e = cudaMalloc(&p->w_pw, sizeof(double) * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_ticket, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(p->w_ticket, 0, sizeof(unsigned));
+  {  // persistent TV-prox workspace: one CTA per SM at most, rows of the full-resolution grid
+    int optin = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    ms2g::TvWs& w = p->tvws;
+    w.max_ctas = sms;
+    w.smem_optin = optin;
+    if (e == cudaSuccess) e = cudaMalloc(&w.flags, sizeof(unsigned long long) * sms);
+    if (e == cudaSuccess) e = cudaMemset(w.flags, 0, sizeof(unsigned long long) * sms);
+    if (e == cudaSuccess) e = cudaMalloc(&w.gen_ticket, 2 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(w.gen_ticket, 0, 2 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&w.err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(w.err, 0, sizeof(int));
+  }
   if (e == cudaSuccess) e = cudaMalloc(&p->w_flag, sizeof(int));
   if (e == cudaSuccess) e = cudaMalloc(&p->w_sel, sizeof(int) * p->V_r * ms2g_plan::kSelRing);
   if (e == cudaSuccess) e = cudaMallocHost(&p->h_sel, sizeof(int) * p->V_r * ms2g_plan::kSelRing);
@@ -1139,6 +1192,12 @@ int ms2g_attach_nccl(ms2g_plan* p, const void* uid, int32_t rank, int32_t nranks
     p->comm = nullptr;
   }
   MS2G_NCCL(ncclCommInitRank(&p->comm, nranks, id, rank));
+  for (auto& gg : p->grad_graphs) {   // per-call gradient graphs captured without it
+    if (gg.exec) cudaGraphExecDestroy(gg.exec);
+    if (gg.graph) cudaGraphDestroy(gg.graph);
+  }
+  p->grad_graphs.clear();
+  p->topo_version++;
   p->rank = rank;
   p->nranks = nranks;
   if (p->sg.exec) {  // a cached solve graph captured without the communicator
@@ -1157,7 +1216,7 @@ struct PeerBlob {
   cudaIpcMemHandle_t buf, pad;
 };
 constexpr uint64_t kPeerMagic = 0x4d53324750454552ULL;   // "MS2GPEER"
-constexpr int kPadWords = 128;
+constexpr int kPadWords = 256;   // peer_reduce.cu: PUB[64], RED[64], epoch, time-out, ticket
 }  // namespace
 
 static int ensure_exchange(ms2g_plan* p) {
@@ -1227,6 +1286,12 @@ int ms2g_attach_peers(ms2g_plan* p, const void* blobs, int32_t rank, int32_t nra
   MS2G_CUDA(cudaMalloc(&p->d_peer_pads, sizeof(unsigned*) * nranks));
   MS2G_CUDA(cudaMemcpy(p->d_peer_bufs, bufs.data(), sizeof(float*) * nranks, cudaMemcpyHostToDevice));
   MS2G_CUDA(cudaMemcpy(p->d_peer_pads, pads.data(), sizeof(unsigned*) * nranks, cudaMemcpyHostToDevice));
+  for (auto& gg : p->grad_graphs) {   // per-call gradient graphs captured without it
+    if (gg.exec) cudaGraphExecDestroy(gg.exec);
+    if (gg.graph) cudaGraphDestroy(gg.graph);
+  }
+  p->grad_graphs.clear();
+  p->topo_version++;
   p->peer_rank = rank;
   p->peer_n = nranks;
   p->rank = rank;
@@ -1282,6 +1347,69 @@ static int do_grad(ms2g_plan* p, const FactorTables* f, int kind, const float* x
                    const Sel& s, cudaStream_t st) {
   const float c = (float)((double)p->d.n_views / (double)s.n_glob);
   return enqueue_grad(p, *f, kind, x, b, g, s.d_sel, s.n_sel, c, p->d.batch, st, s.ford, s.bord);
+}
+
+static void destroy_graph(SolveGraph& gg) {
+  if (gg.exec) cudaGraphExecDestroy(gg.exec);
+  if (gg.graph) cudaGraphDestroy(gg.graph);
+  gg = SolveGraph{};
+}
+
+// The standalone gradient is 4 launches (fused sketch + pair prep, forward,
+// backprojection, fused chunk sum + upsample); a loop of such calls (the
+// method's inner loop driven from outside) is launch-bound at small sizes,
+// so calls without host-side staging (all views or a registered subset) are
+// captured once per (factor, kind, selection, pointers) into a CUDA graph and
+// replayed: one launch per call (SURVEY §7 "small configs are launch-bound").
+static int grad_graph(ms2g_plan* p, const FactorTables* f, int kind, const float* x, const float* b, float* g,
+                      const Sel& s, int sel_id, cudaStream_t st) {
+  static const bool off = getenv("MS2G_GRAD_GRAPHS") && atoi(getenv("MS2G_GRAD_GRAPHS")) == 0;   // experiment switch
+  if (off || p->timing || t_capturing) return do_grad(p, f, kind, x, b, g, s, st);
+  std::ostringstream os;
+  os << f->factor << ':' << kind << ':' << sel_id << ':' << (const void*)x << ':' << (const void*)b << ':'
+     << (const void*)g << ':' << p->topo_version;
+  const std::string key = os.str();
+  for (size_t k = 0; k < p->grad_graphs.size(); ++k) {
+    if (p->grad_graphs[k].key != key) continue;
+    std::rotate(p->grad_graphs.begin(), p->grad_graphs.begin() + k, p->grad_graphs.begin() + k + 1);
+    MS2G_CUDA(cudaGraphLaunch(p->grad_graphs[0].exec, st));
+    count_launch(p->grad_graphs[0].kernel_nodes);
+    return MS2G_OK;
+  }
+  cudaStream_t cs;
+  MS2G_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return set_error(MS2G_ERR_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+  }
+  t_capturing = true;
+  t_captured = 0;
+  const int rc = do_grad(p, f, kind, x, b, g, s, cs);
+  t_capturing = false;
+  SolveGraph gg;
+  e = cudaStreamEndCapture(cs, &gg.graph);
+  cudaStreamDestroy(cs);
+  if (rc != MS2G_OK) {
+    destroy_graph(gg);
+    return rc;
+  }
+  if (e != cudaSuccess) return set_error(MS2G_ERR_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&gg.exec, gg.graph, 0);
+  if (e != cudaSuccess) {
+    destroy_graph(gg);
+    return set_error(MS2G_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+  }
+  gg.key = key;
+  gg.kernel_nodes = t_captured;
+  if ((int)p->grad_graphs.size() == ms2g_plan::kGradGraphs) {
+    destroy_graph(p->grad_graphs.back());
+    p->grad_graphs.pop_back();
+  }
+  p->grad_graphs.insert(p->grad_graphs.begin(), gg);
+  MS2G_CUDA(cudaGraphLaunch(p->grad_graphs[0].exec, st));
+  count_launch(gg.kernel_nodes);
+  return MS2G_OK;
 }
 
 static int check_fwd(ms2g_plan* p, int32_t factor, const float* x, const float* out, const FactorTables** f) {
@@ -1342,7 +1470,7 @@ int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* 
   cudaStream_t st = (cudaStream_t)stream;
   Sel s;
   MS2G_TRY(sel_host(p, subset, n_subset, st, &s));
-  const int rc = do_grad(p, f, kind, x, b, g, s, st);
+  const int rc = subset ? do_grad(p, f, kind, x, b, g, s, st) : grad_graph(p, f, kind, x, b, g, s, -1, st);
   MS2G_TRY(release_subset(p, s.slot, st));
   return rc;
 }
@@ -1378,6 +1506,8 @@ int ms2g_release_subset(ms2g_plan* p, int32_t id) {
   if (!p || id < 0 || id >= (int)p->reg.size() || !p->reg[id].d_sel)
     return set_error(MS2G_ERR_INPUT, "unknown or released subset id");
   MS2G_CUDA(cudaDeviceSynchronize());   // no kernel of any stream may still read it
+  for (auto& gg : p->grad_graphs) destroy_graph(gg);   // graphs may hold the list
+  p->grad_graphs.clear();
   auto& r = p->reg[id];
   cudaFree(r.d_sel);
   for (int* q : r.bp_order) cudaFree(q);
@@ -1410,7 +1540,7 @@ int ms2g_sketched_grad_registered(ms2g_plan* p, int32_t factor, int32_t kind, co
   MS2G_TRY(check_grad(p, factor, kind, x, b, g, &f));
   Sel s;
   MS2G_TRY(sel_registered(p, subset_id, f, &s));
-  return do_grad(p, f, kind, x, b, g, s, (cudaStream_t)stream);
+  return grad_graph(p, f, kind, x, b, g, s, subset_id, (cudaStream_t)stream);
 }
 
 int ms2g_sketch_down(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, float* v, void* stream) {

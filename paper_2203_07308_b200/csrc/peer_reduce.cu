@@ -1,33 +1,46 @@
 // peer_reduce.cu -- NEXT-3: the backprojection's cross-rank sum
 // over NVLink peer memory instead of a separate NCCL collective.
 //
-// Every rank's plan owns an IPC-shareable exchange buffer (two slots of
-// n_cmax^2 x batch floats) and a signal pad.  After ms2g_attach_peers each
-// rank holds device pointers to every peer's buffer and pad.  One allreduce
-// of the view-sharded partial image G_r:
-//   1. publish: the backprojector's chunk reduction writes scale * G_r
-//      straight into slot (epoch + 1) & 1 of the local exchange buffer (fused
-//      epilogue; a generic allreduce copies the buffer there instead),
-//   2. barrier: epoch += 1; store it into slot `rank` of every peer's pad
-//      (release, system scope); wait until every slot of the local pad holds
-//      it (acquire),
-//   3. sum: G = sum_{q = 0..P-1} slot_q of rank q's buffer, peer loads over
-//      NVLink in FIXED rank order: every rank gets a bitwise identical G and
-//      the result does not depend on a collective's algorithm.
-// Two slots alternate: a rank reuses a slot two allreduces later only after
-// the barrier in between, which every peer passes only after finishing its
-// sum of that slot (stream order), so no extra barrier is needed.
-// The wait in the barrier is bounded by 20 s of wall time (%globaltimer); on a
-// time-out it raises the plan's error flag instead of hanging the device, and
-// every later barrier / sum of the plan returns at once.  The host then sees
-// MS2G_ERR_NCCL and the plan refuses further exchanges until every rank calls
-// ms2g_attach_peers again (epochs restart from 0).
+// Every rank's plan owns an IPC-shareable exchange buffer of two regions --
+// PUB (this rank's partial image) and RED (the chunk of the sum this rank
+// owns) -- and a signal pad.  After ms2g_attach_peers each rank holds device
+// pointers to every peer's buffer and pad.  One allreduce of the view-sharded
+// partial images G_r is a reduce-scatter + all-gather in three
+// launches, with the barrier folded into them:
+//   1. publish: the backprojector's chunk reduction writes scale * G_r into
+//      PUB (fused epilogue; a generic allreduce copies the buffer instead);
+//      the LAST block of the launch (atomic ticket) bumps the epoch e and
+//      stores it into word PUB+rank of every peer's pad (release, system
+//      scope, after __threadfence_system);
+//   2. reduce-scatter: every block first waits until all P words PUB+q of
+//      the local pad reach e (acquire), then rank r sums its contiguous 1/P
+//      chunk of the image over the P PUB regions in FIXED rank order 0..P-1
+//      (peer loads over NVLink) into its RED region; the last block signals
+//      RED+rank = e to every peer;
+//   3. all-gather: every block waits for all RED words, then copies each
+//      element from the RED region of the rank that owns it -- or, fused,
+//      takes the step z = y - eta U_s G there with no G round trip.
+// Every rank ends with the bitwise same G (each chunk is summed once, by its
+// owner, in rank order).  NVLink traffic per rank: 2 (P-1)/P of the image
+// instead of (P-1) images for the one-shot sum.  One region of each kind
+// suffices: a rank rewrites PUB (next allreduce) only after its all-gather,
+// which waited for every peer's RED signal, which each peer raised after its
+// reduce-scatter had read every PUB region; and it rewrites RED only after
+// the next reduce-scatter's wait, i.e. after every peer published again,
+// which each did after its all-gather had read every RED region.
+// Waits are bounded by 20 s of wall time (%globaltimer): on a time-out the
+// kernel raises the plan's error flag (every later wait of the plan then
+// returns at once and the sum kernels leave their outputs untouched), the
+// host sees MS2G_ERR_NCCL and the plan refuses further exchanges until every
+// rank calls ms2g_attach_peers again (epochs restart from 0).
 #include "internal.cuh"
 
 namespace ms2g {
 
-constexpr int kEpoch = 64;                // pad word holding the local epoch
-constexpr int kTimeout = 65;              // pad word set on a barrier time-out
+// pad layout (unsigned words): [0, 64) PUB epochs by rank, [64, 128) RED
+// epochs by rank, then the local epoch, the time-out mark and the last-block
+// ticket of the running exchange kernel
+constexpr int kPub = 0, kRed = 64, kEpoch = 128, kTimeout = 129, kTicket = 130;
 
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -37,15 +50,72 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
-// scale * (sum of nplanes partial planes) -> the local exchange slot of the
-// NEXT epoch (fused publish of the backprojection).
-// grid.y = batch image (no index division)
-__global__ void k_chunk_reduce_publish(const float* __restrict__ part, int nplanes, size_t np,
-                                       float* __restrict__ xbuf, size_t slot_elems, const unsigned* __restrict__ pad,
+struct PeerArgs {
+  float* const* bufs;          // every rank's exchange buffer (PUB region first, RED at + slot)
+  unsigned* const* pads;       // every rank's signal pad
+  int rank, nranks;
+  size_t slot;                 // floats per region
+  int* err;                    // plan error flag (time-out)
+};
+
+// Wait until the words [base, base + P) of the local pad reach epoch e.
+// Bounded by WALL time, not a spin count; returns false on a time-out (after
+// raising the error flag) or at once when the flag is already up.
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+__device__ bool wait_words(const PeerArgs& a, int base, unsigned e) {
+  if (*(volatile int*)a.err) return false;
+  unsigned* mine = a.pads[a.rank];
+  const unsigned long long t0 = globaltimer_ns();
+  for (int q = 0; q < a.nranks; ++q) {
+    while ((int)(ld_acquire_sys(mine + base + q) - e) < 0) {
+      if (globaltimer_ns() - t0 > kPeerTimeoutNs || *(volatile int*)a.err) {
+        atomicExch(a.err, 1);
+        mine[kTimeout] = 1u;
+        return false;
+      }
+      __nanosleep(64);
+    }
+  }
+  return true;
+}
+
+// Block-wide wait: thread 0 polls, the block proceeds together; false when
+// the exchange has failed (outputs are then left untouched).
+__device__ bool block_wait(const PeerArgs& a, int base, unsigned e) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = wait_words(a, base, e) ? 1 : 0;
+  __syncthreads();
+  return ok != 0;
+}
+
+// The last block of the launch to finish signals word base + rank = e at
+// every peer (after all blocks' stores are visible system-wide); with
+// bump != 0 it first records e as the local epoch.
+__device__ void last_block_signal(const PeerArgs& a, int base, unsigned e, int bump) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned* mine = a.pads[a.rank];
+  __threadfence_system();
+  if (atomicAdd(mine + kTicket, 1u) != gridDim.x * gridDim.y - 1) return;
+  mine[kTicket] = 0u;
+  if (bump) mine[kEpoch] = e;
+  __threadfence_system();
+  for (int q = 0; q < a.nranks; ++q) st_release_sys(a.pads[q] + base + a.rank, e);
+}
+
+// 1a. publish, fused with the backprojection's chunk sum: PUB = scale * sum
+// of the nplanes partial planes (fixed order).  grid.y = batch image.
+__global__ void k_chunk_reduce_publish(const float* __restrict__ part, int nplanes, size_t np, PeerArgs a,
                                        float scale) {
+  const unsigned e = *(volatile unsigned*)(a.pads[a.rank] + kEpoch) + 1u;
   const size_t b = blockIdx.y;
-  float* dst = xbuf + (size_t)((pad[kEpoch] + 1u) & 1u) * slot_elems + b * np;
+  float* dst = a.bufs[a.rank] + b * np;
   const float* src0 = part + b * nplanes * np;
   for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
     const float* src = src0 + p;
@@ -53,83 +123,97 @@ __global__ void k_chunk_reduce_publish(const float* __restrict__ part, int nplan
     for (int c = 0; c < nplanes; ++c) s += src[(size_t)c * np];
     dst[p] = scale * s;
   }
+  last_block_signal(a, kPub, e, 1);
 }
 
-__global__ void k_publish_copy(const float* __restrict__ buf, size_t count, float* __restrict__ xbuf,
-                               size_t slot_elems, const unsigned* __restrict__ pad) {
-  float* dst = xbuf + (size_t)((pad[kEpoch] + 1u) & 1u) * slot_elems;
+// 1b. publish a buffer (generic allreduce: back_project(allreduce=1), ...)
+__global__ void k_publish_copy(const float* __restrict__ buf, size_t count, PeerArgs a) {
+  const unsigned e = *(volatile unsigned*)(a.pads[a.rank] + kEpoch) + 1u;
+  float* dst = a.bufs[a.rank];
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
     dst[i] = buf[i];
+  last_block_signal(a, kPub, e, 1);
 }
 
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
+__device__ __forceinline__ size_t chunk_lo(int q, int P, size_t count) { return ((size_t)q * count) / P; }
 
-// Wait until *slot has reached epoch e.  Bounded by WALL time (%globaltimer,
-// kPeerTimeoutNs), not by a spin count; returns false on a time-out (after
-// raising the plan's error flag) or at once when the flag is already up, so
-// a failed exchange costs one time-out, not one per later barrier.
-constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s
-__device__ bool wait_epoch(const unsigned* slot, unsigned e, int* err_flag, unsigned* timeout_word) {
-  if (*(volatile int*)err_flag) return false;
-  const unsigned long long t0 = globaltimer_ns();
-  while ((int)(ld_acquire_sys(slot) - e) < 0) {
-    if (globaltimer_ns() - t0 > kPeerTimeoutNs || *(volatile int*)err_flag) {
-      atomicExch(err_flag, 1);
-      *timeout_word = 1u;
-      return false;
+// 2. reduce-scatter: this rank's chunk of the sum, in rank order, into RED
+__global__ void k_peer_rs(size_t count, PeerArgs a) {
+  const unsigned e = *(volatile unsigned*)(a.pads[a.rank] + kEpoch);
+  if (block_wait(a, kPub, e)) {
+    const size_t lo = chunk_lo(a.rank, a.nranks, count), hi = chunk_lo(a.rank + 1, a.nranks, count);
+    float* red = a.bufs[a.rank] + a.slot;
+    for (size_t i = lo + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi; i += (size_t)gridDim.x * blockDim.x) {
+      float s = 0.f;
+      for (int q = 0; q < a.nranks; ++q) s += a.bufs[q][i];
+      red[i] = s;
     }
-    __nanosleep(64);
   }
-  return true;
+  last_block_signal(a, kRed, e, 0);
 }
 
-// one warp: lane q signals peer q and waits for peer q's signal
-__global__ void k_peer_barrier(unsigned* const* __restrict__ pads, int rank, int nranks, int* err_flag) {
-  unsigned* mine = pads[rank];
-  __shared__ unsigned e;
-  if (threadIdx.x == 0) {
-    e = mine[kEpoch] + 1u;
-    mine[kEpoch] = e;
-  }
-  __syncthreads();
-  __threadfence_system();            // this rank's published slot before the signal
-  for (int q = threadIdx.x; q < nranks; q += blockDim.x) st_release_sys(pads[q] + rank, e);
-  for (int q = threadIdx.x; q < nranks; q += blockDim.x) wait_epoch(mine + q, e, err_flag, mine + kTimeout);
+__device__ __forceinline__ float gathered(const PeerArgs& a, size_t i, size_t count) {
+  const int q = (int)((((unsigned long long)i + 1) * (unsigned long long)a.nranks - 1) / count);   // chunk owner
+  return a.bufs[q][a.slot + i];
 }
 
-// out = sum over ranks (fixed order) of the current epoch's slots
-__global__ void k_peer_sum(const float* const* __restrict__ bufs, int nranks, size_t slot_elems,
-                           const unsigned* __restrict__ pad, float* __restrict__ out, size_t count,
-                           const int* __restrict__ err_flag) {
-  if (*(volatile const int*)err_flag) return;   // a peer never arrived: its slot holds stale data
-  const size_t off = (size_t)(pad[kEpoch] & 1u) * slot_elems;
+// 3a. all-gather into out
+__global__ void k_peer_ag(size_t count, PeerArgs a, float* __restrict__ out) {
+  const unsigned e = *(volatile unsigned*)(a.pads[a.rank] + kEpoch);
+  if (!block_wait(a, kRed, e)) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = gathered(a, i, count);
+}
+
+// 3b. all-gather fused with the step z = y - eta U_s G (y == NULL: z = U_s G);
+// element i = coarse pixel (b, I, J) of the [batch][nc][nc] sum
+__global__ void k_peer_ag_step(size_t count, PeerArgs a, int nc, int s, const float* __restrict__ y,
+                               const float* __restrict__ eta_dev, float* __restrict__ z) {
+  const unsigned e = *(volatile unsigned*)(a.pads[a.rank] + kEpoch);
+  if (!block_wait(a, kRed, e)) return;
+  const float et = eta_dev ? *eta_dev : 0.f;
+  const int n = nc * s;
+  const size_t np = (size_t)nc * nc;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int q = 0; q < nranks; ++q) s += bufs[q][off + i];
-    out[i] = s;
+    const float G = gathered(a, i, count);
+    const size_t b = i / np, r = i - b * np;
+    const int I = (int)(r / nc), J = (int)(r - (size_t)I * nc);
+    for (int u = 0; u < s; ++u) {
+      const size_t row = (b * n + (size_t)(s * I + u)) * n + (size_t)s * J;
+      for (int q = 0; q < s; ++q) z[row + q] = y ? fmaf(-et, G, y[row + q]) : G;
+    }
   }
 }
 
-static int grid_for(size_t n) {
+static int grid_for(size_t n, int cap) {
   const size_t b = (n + 255) / 256;
-  return (int)(b < 4096 ? (b ? b : 1) : 4096);
+  return (int)(b < (size_t)cap ? (b ? b : 1) : cap);
+}
+
+static PeerArgs peer_args(ms2g_plan* p) {
+  return PeerArgs{p->d_peer_bufs, p->d_peer_pads, p->peer_rank, p->peer_n, p->xch_slot, p->w_peer_err};
 }
 
 int launch_peer_finish(ms2g_plan* p, float* out, size_t count, cudaStream_t st) {
-  k_peer_barrier<<<1, 32, 0, st>>>(p->d_peer_pads, p->peer_rank, p->peer_n, p->w_peer_err);
-  MS2G_TRY(check_launch("k_peer_barrier"));
-  k_peer_sum<<<grid_for(count), 256, 0, st>>>(p->d_peer_bufs, p->peer_n, p->xch_slot, p->xch_pad, out, count,
-                                               p->w_peer_err);
-  return check_launch("k_peer_sum");
+  const PeerArgs a = peer_args(p);
+  k_peer_rs<<<grid_for((count + p->peer_n - 1) / p->peer_n, 2 * p->sm_count), 256, 0, st>>>(count, a);
+  MS2G_TRY(check_launch("k_peer_rs"));
+  k_peer_ag<<<grid_for(count, 4 * p->sm_count), 256, 0, st>>>(count, a, out);
+  return check_launch("k_peer_ag");
+}
+
+int launch_peer_finish_step(ms2g_plan* p, size_t count, int nc, int s, const float* y, const float* eta_dev,
+                            float* z, cudaStream_t st) {
+  const PeerArgs a = peer_args(p);
+  k_peer_rs<<<grid_for((count + p->peer_n - 1) / p->peer_n, 2 * p->sm_count), 256, 0, st>>>(count, a);
+  MS2G_TRY(check_launch("k_peer_rs"));
+  k_peer_ag_step<<<grid_for(count, 4 * p->sm_count), 256, 0, st>>>(count, a, nc, s, y, eta_dev, z);
+  return check_launch("k_peer_ag_step");
 }
 
 int launch_peer_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
   if (count > p->xch_slot) return set_error(MS2G_ERR_CONFIG, "peer allreduce larger than the exchange slot");
-  k_publish_copy<<<grid_for(count), 256, 0, st>>>(buf, count, p->xch_buf, p->xch_slot, p->xch_pad);
+  k_publish_copy<<<grid_for(count, 4 * p->sm_count), 256, 0, st>>>(buf, count, peer_args(p));
   MS2G_TRY(check_launch("k_publish_copy"));
   return launch_peer_finish(p, buf, count, st);
 }
@@ -137,8 +221,8 @@ int launch_peer_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t s
 int launch_chunk_reduce_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
                                 cudaStream_t st) {
   if (total > p->xch_slot) return set_error(MS2G_ERR_CONFIG, "peer allreduce larger than the exchange slot");
-  k_chunk_reduce_publish<<<dim3(grid_for(np), (unsigned)(total / np)), 256, 0, st>>>(part, nplanes, np, p->xch_buf,
-                                                                                     p->xch_slot, p->xch_pad, scale);
+  k_chunk_reduce_publish<<<dim3(grid_for(np, 4 * p->sm_count), (unsigned)(total / np)), 256, 0, st>>>(
+      part, nplanes, np, peer_args(p), scale);
   return check_launch("k_chunk_reduce_publish");
 }
 

@@ -11,7 +11,9 @@
 // "precision").  Since the slope is in [0, 1), a column holds one segment or
 // two split at the grid line m0 + 1 (seg_weights).  Lengths are physical
 // (the oracle's (alpha_b - alpha_a) |d|).
+#include <algorithm>
 #include <climits>
+#include <cstring>
 
 #include "internal.cuh"
 
@@ -45,17 +47,42 @@ __device__ __forceinline__ void seg_weights(unsigned lo, bool cross, float Lc, f
 //      each line stored back to front (element nc - k holds it), so that the
 //      forward indexes every class the same way
 //   3 major-y, mirrored: as 1, reversed likewise
-__global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pairs, size_t pair_stride, int nc) {
+//
+// The kernel also forms its input on the fly (fused producers, one launch
+// instead of two): with s > 1 the coarse value is the s x s mean of the
+// full-resolution image (S_s, the same summation order as k_sketch_down);
+// with scale_dev != NULL it is w * (float)scale_dev[0] (the power iteration's
+// v = w / ||w||, as k_scale did).  v_out != NULL also stores the coarse values
+// (each block stores the rows it owns).
+__device__ __forceinline__ float pair_src(const float* __restrict__ xb, int k, int j, int nc, int s, int nsrc,
+                                          float inv_s2, float scale) {
+  if (s == 1) return xb[(size_t)k * nc + j] * scale;
+  float acc = 0.f;
+  for (int a = 0; a < s; ++a) {
+    const float* row = xb + (size_t)(s * k + a) * nsrc + (size_t)s * j;
+    for (int c = 0; c < s; ++c) acc += row[c];
+  }
+  return acc * inv_s2 * scale;
+}
+
+__global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pairs, size_t pair_stride, int nc,
+                            int s, const double* __restrict__ scale_dev, float* __restrict__ v_out) {
   __shared__ float T[33][33];
   const int bz = blockIdx.z;
-  const float* xb = x + (size_t)bz * nc * nc;
+  const int nsrc = nc * s;
+  const float* xb = x + (size_t)bz * nsrc * nsrc;
+  const float inv_s2 = 1.0f / (float)(s * s);
+  const float scale = scale_dev ? (float)scale_dev[0] : 1.f;
   const int L = nc + 3;
   const size_t ib = (size_t)bz * nc * L;
   const int O0 = blockIdx.x * 32, L0 = blockIdx.y * 32;   // output positions o, lines
-  // x rows k = O0-2 .. O0+30 for the column-pair images
+  // rows k = O0-2 .. O0+30 for the column-pair images (this block owns O0-2 .. O0+29)
   for (int r = threadIdx.y; r < 33; r += 8) {
     const int k = O0 - 2 + r, j = L0 + threadIdx.x;
-    T[r][threadIdx.x] = (k >= 0 && k < nc && j < nc) ? xb[(size_t)k * nc + j] : 0.f;
+    const bool in = k >= 0 && k < nc && j < nc;
+    const float val = in ? pair_src(xb, k, j, nc, s, nsrc, inv_s2, scale) : 0.f;
+    T[r][threadIdx.x] = val;
+    if (v_out && in && r < 32) v_out[((size_t)bz * nc + k) * nc + j] = val;
   }
   __syncthreads();
   const int o = O0 + threadIdx.x;
@@ -64,22 +91,22 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
     const int line = L0 + jj;
     if (line >= nc) break;
     const size_t e = ib + (size_t)line * L + o;
-    const float a = T[threadIdx.x][jj], b = T[threadIdx.x + 1][jj];   // x[o-2][line], x[o-1][line]
+    const float a = T[threadIdx.x][jj], b = T[threadIdx.x + 1][jj];   // v[o-2][line], v[o-1][line]
     const size_t er = ib + (size_t)line * L + (nc + 2 - o);   // back-to-front line
     pairs[e] = make_float2(a, b);
     pairs[2 * pair_stride + er] = make_float2(b, a);
     const int k = o - 2;
-    const float* row = xb + (size_t)line * nc;
-    const float c = (k >= 0 && k < nc) ? row[k] : 0.f;
-    const float d = (k + 1 >= 0 && k + 1 < nc) ? row[k + 1] : 0.f;
+    const float c = (k >= 0 && k < nc) ? pair_src(xb, line, k, nc, s, nsrc, inv_s2, scale) : 0.f;
+    const float d = (k + 1 >= 0 && k + 1 < nc) ? pair_src(xb, line, k + 1, nc, s, nsrc, inv_s2, scale) : 0.f;
     pairs[pair_stride + e] = make_float2(c, d);
     pairs[3 * pair_stride + er] = make_float2(d, c);
   }
 }
 
-int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s) {
+int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s, int factor,
+                     const double* scale_dev, float* v_out) {
   dim3 grid((nc + 3 + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
-  k_pair_prep<<<grid, block, 0, s>>>(x, p->w_pair, p->pair_stride, nc);
+  k_pair_prep<<<grid, block, 0, s>>>(x, p->w_pair, p->pair_stride, nc, factor, scale_dev, v_out);
   return check_launch("k_pair_prep");
 }
 
@@ -638,6 +665,65 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   }
 }
 
+// ------------------------------------------------ adjoint, gather variant --
+// Pixel-driven gather (north-star subsystem (2), first alternative): one
+// thread per pixel accumulates in a register over the views of its chunk;
+// per (pixel, view) the candidate bins are the detector interval of the
+// pixel's four corners (the fan projection of a convex pixel), and each
+// candidate ray's weight is evaluated with the SAME fixed-point end
+// coordinate as the forward and the scatter: with E = F0 + (c + 1) S at the
+// pixel's major column c, the pixel (frame row k) receives m Ly32 when
+// floor(E) = k and (S - m) Ly32 when floor(E) - 1 = k, m = min(frac32(E), S)
+// (zero otherwise).  No shared memory, no atomics, deterministic; partial
+// planes per view chunk as the scatter (k_chunk_reduce and the fused
+// epilogues sum them).  Kept as the measured alternative (MS2G_BP_VARIANT=
+// gather): its per-segment instruction count is ~3x the scatter's (DESIGN.md
+// "adjoint design", profiles/r02_adjoint_variants.md).
+__global__ void __launch_bounds__(256) k_backward_gather(const RayEntry* __restrict__ rays,
+                                                         const ViewEntry* __restrict__ views, int B,
+                                                         const int* __restrict__ sel, int n_sel,
+                                                         const float* __restrict__ sino, float* __restrict__ part,
+                                                         int nc, int vpc, int nplanes) {
+  const int tiles_x = (nc + 31) / 32, per = tiles_x * ((nc + 7) / 8);
+  const int chunk = blockIdx.x / per, ti = blockIdx.x - chunk * per;
+  const int j = (ti % tiles_x) * 32 + threadIdx.x, i = (ti / tiles_x) * 8 + threadIdx.y;
+  if (i >= nc || j >= nc) return;
+  const size_t bz = blockIdx.z, np = (size_t)nc * nc;
+  const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
+  const float* sb = sino + bz * n_sel * B;
+  float acc = 0.f;
+  for (int k = kb; k < ke; ++k) {
+    const int g = sel ? __ldg(sel + k) : k;
+    const ViewEntry V = views[g];
+    float tmin = INFINITY, tmax = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float dx = (float)(j + (q & 1)) - V.Sx, dy = (float)(i + (q >> 1)) - V.Sy;
+      const float tau = fmaf(V.scale, __fdividef(dx * V.ex + dy * V.ey, dx * V.nx + dy * V.ny), V.off);
+      tmin = fminf(tmin, tau);
+      tmax = fmaxf(tmax, tau);
+    }
+    const int t0 = max(0, (int)ceilf(tmin - 0.01f)), t1 = min(B - 1, (int)floorf(tmax + 0.01f));
+    const RayEntry* rv = rays + (size_t)g * B;
+    const float* rr = sb + (size_t)k * B;
+    for (int t = t0; t <= t1; ++t) {
+      const RayEntry R = rv[t];
+      const int cls = R.flags & 3;
+      const int c = (cls & kMajorY) ? i : j;
+      const int mn = (cls & kMajorY) ? j : i;
+      const int kf = (cls & kMirror) ? nc - 1 - mn : mn;
+      const long long E = R.F0 + (long long)(c + 1) * (long long)R.S;
+      const int fl = (int)(E >> 32);
+      const unsigned m = min((unsigned)E, R.S);
+      float w = 0.f;
+      if (fl == kf) w = (float)m * R.Ly32;
+      else if (fl - 1 == kf) w = (float)(R.S - m) * R.Ly32;
+      acc = fmaf(w, __ldg(rr + t), acc);
+    }
+  }
+  part[(bz * nplanes + chunk) * np + (size_t)i * nc + j] = acc;
+}
+
 // out = scale * sum of the nplanes partial planes (+ out if accumulate), fixed
 // order.  grid.y = batch image (no index division).
 __global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size_t np, float* __restrict__ out,
@@ -653,6 +739,114 @@ __global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size
     if (accumulate) v += ob[p];
     ob[p] = v;
   }
+}
+
+// Fused epilogues of the backprojection (the chunk sum feeds its consumer in
+// the same pass; no G round trip, one launch instead of two or four).
+//
+// G = c * sum of the planes (fixed order, as k_chunk_reduce), then the step
+// z = y - eta U_s G (as k_up_step) for the s x s fine pixels of each
+// coarse pixel (y == NULL: z = U_s G); grid = coarse pixels (x: columns,
+// y: rows, z: batch).
+__global__ void k_reduce_up_step(const float* __restrict__ part, int nplanes, int nc, float c,
+                                 const float* __restrict__ y, const float* __restrict__ eta_dev, float* __restrict__ z,
+                                 int s) {
+  const int J = blockIdx.x * 32 + threadIdx.x, I = blockIdx.y * 8 + threadIdx.y;
+  if (I >= nc || J >= nc) return;
+  const size_t b = blockIdx.z, np = (size_t)nc * nc;
+  const float* src = part + b * nplanes * np + (size_t)I * nc + J;
+  float acc = 0.f;
+  for (int q = 0; q < nplanes; ++q) acc += src[(size_t)q * np];
+  const float G = c * acc;
+  const float e = eta_dev ? *eta_dev : 0.f;
+  const int n = nc * s;
+  for (int a = 0; a < s; ++a) {
+    const size_t row = (b * n + (size_t)(s * I + a)) * n + (size_t)s * J;
+    for (int q = 0; q < s; ++q) z[row + q] = y ? fmaf(-e, G, y[row + q]) : G;   // one rounding, as k_up_step
+  }
+}
+
+// Power-iteration step (O8) fused with the chunk sum: w = sum of the planes
+// (written to w_out), fp64 block partials of <v, w> and <w, w>; the last
+// block to finish (atomic ticket) reduces the partials in fixed block order
+// (deterministic) into pw = {L = <v,w>, 1/||w||} and, if given, the step
+// L_out, eta_out = 1/L, etaf_out.  The next pair prep scales by pw[1].
+__global__ void __launch_bounds__(256) k_reduce_power(const float* __restrict__ part, int nplanes, size_t np,
+                                                      float* __restrict__ w_out, const float* __restrict__ v,
+                                                      double* __restrict__ red, unsigned* __restrict__ ticket,
+                                                      double* __restrict__ pw, double* L_out, double* eta_out,
+                                                      float* etaf_out) {
+  __shared__ double sd[256], sn[256];
+  __shared__ bool last;
+  double d = 0.0, q = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+    const float* src = part + i;
+    float w = 0.f;
+    for (int c = 0; c < nplanes; ++c) w += src[(size_t)c * np];
+    w_out[i] = w;
+    const double wd = w;
+    d += (double)v[i] * wd;
+    q += wd * wd;
+  }
+  sd[threadIdx.x] = d;
+  sn[threadIdx.x] = q;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sd[threadIdx.x] += sd[threadIdx.x + o];
+      sn[threadIdx.x] += sn[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    red[2 * blockIdx.x] = sd[0];
+    red[2 * blockIdx.x + 1] = sn[0];
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  d = 0.0;
+  q = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    d += __ldcg(red + 2 * b);
+    q += __ldcg(red + 2 * b + 1);
+  }
+  sd[threadIdx.x] = d;
+  sn[threadIdx.x] = q;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      sd[threadIdx.x] += sd[threadIdx.x + o];
+      sn[threadIdx.x] += sn[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  d = sd[0];
+  q = sn[0];
+  pw[0] = d;
+  pw[1] = q > 0.0 ? 1.0 / sqrt(q) : 0.0;
+  if (L_out) *L_out = d;
+  if (eta_out) *eta_out = 1.0 / d;
+  if (etaf_out) *etaf_out = (float)(1.0 / d);
+  *ticket = 0u;                        // ready for the next launch (graph replays)
+}
+
+int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, float c, const float* y,
+                          const float* eta_dev, float* z, int s, cudaStream_t st) {
+  dim3 grid((nc + 31) / 32, (nc + 7) / 8, batch);
+  k_reduce_up_step<<<grid, dim3(32, 8), 0, st>>>(part, nplanes, nc, c, y, eta_dev, z, s);
+  return check_launch("k_reduce_up_step");
+}
+
+int launch_reduce_power(ms2g_plan* p, const float* part, int nplanes, size_t np, float* w_out, const float* v,
+                        double* red, int red_blocks, unsigned* ticket, double* pw, double* L_out, double* eta_out,
+                        float* etaf_out, cudaStream_t st) {
+  k_reduce_power<<<red_blocks, 256, 0, st>>>(part, nplanes, np, w_out, v, red, ticket, pw, L_out, eta_out,
+                                             etaf_out);
+  return check_launch("k_reduce_power");
 }
 
 template <int H>
@@ -692,7 +886,30 @@ void bp_launch_chunks(const ms2g_plan* p, const FactorTables& f, int n_sel, int*
 
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish,
-                    const int* order_sel) {
+                    const int* order_sel, int* nplanes_out) {
+  const size_t np = (size_t)f.nc * f.nc, total = np * batch;
+  static const bool gather = getenv("MS2G_BP_VARIANT") && !strcmp(getenv("MS2G_BP_VARIANT"), "gather");
+  if (gather) {   // experiment switch: the pixel-driven gather variant
+    const int per = ((f.nc + 31) / 32) * ((f.nc + 7) / 8);
+    const int planes_alloc = f.bp_chunks[0] + f.bp_chunks[1];
+    const long long target = 24LL * p->sm_count;
+    int nch = (int)std::min<long long>(planes_alloc, std::max<long long>(1, (target + (long long)per * batch - 1) /
+                                                                              ((long long)per * batch)));
+    nch = std::max(1, std::min(nch, n_sel));
+    const int vpc = (n_sel + nch - 1) / nch;
+    nch = (n_sel + vpc - 1) / vpc;
+    const int slot = timing_begin(p, 1, f.factor, s);
+    k_backward_gather<<<dim3(per * nch, 1, batch), dim3(32, 8), 0, s>>>(f.d_rays, f.d_views, p->B, d_sel, n_sel, sino,
+                                                                       p->w_part, f.nc, vpc, nch);
+    MS2G_TRY(check_launch("k_backward_gather"));
+    timing_end(p, slot, s);
+    if (nplanes_out) *nplanes_out = nch;
+    if (publish == 2) return MS2G_OK;
+    if (publish) return launch_chunk_reduce_publish(p, p->w_part, nch, np, total, scale, s);
+    const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);
+    k_chunk_reduce<<<dim3(blocks, batch), 256, 0, s>>>(p->w_part, nch, np, img, scale, accumulate);
+    return check_launch("k_chunk_reduce");
+  }
   const int H = bp_height(f.nc);
   const BpTiling t = bp_tiling(f.nc, H);
   int ch[2], vpc[2];
@@ -708,7 +925,8 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
   MS2G_TRY(check_launch("k_backward"));
   timing_end(p, slot, s);
-  const size_t np = (size_t)f.nc * f.nc, total = np * batch;
+  if (nplanes_out) *nplanes_out = ch[0] + ch[1];
+  if (publish == 2) return MS2G_OK;   // partial planes only: the caller's fused epilogue sums them
   if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)
     return launch_chunk_reduce_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);
   const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);

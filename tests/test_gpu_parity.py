@@ -825,3 +825,83 @@ def test_host_x_out_is_written(P):
             xo = torch.full((1, n, n), -7.0)
             res = P.pnp_ms2g_solve(plan, [(1, 3, 0)], b, den=("gauss", 0.8), alpha=0.5, x_out=xo)
             assert res.data_ptr() == xo.data_ptr() and torch.equal(xo, ref)
+
+
+@pytest.mark.parametrize("n,batch", [(37, 3), (512, 1), (512, 8), (1024, 1), (130, 2)])
+def test_tv_persistent_kernel(P, n, batch):
+    """The single-launch persistent TV-prox (row strips per CTA, neighbour
+    flags) against the oracle's Chambolle iteration at several shapes (ragged
+    strips, strips crossing image boundaries in a batch), repeated calls
+    (launch generations) bit-identical, and bitwise equal to the K + 1-launch
+    form (MS2G_TV_PERSIST=0 in a subprocess) and to the persistent form with
+    short rounds (MS2G_TV_KROUND=3, =1: halo exchanges between rounds)."""
+    import os
+    import subprocess
+    import sys
+    zs = np.stack([S.random_image(n, 500 + i) for i in range(batch)]).astype(np.float32)
+    with P.plan_geometry(n, 8, 2 * n, factors=(1,), batch=batch) as plan:
+        zt = dev(zs)
+        outs = [host(P.denoise(plan, ("tv", 0.05, 10), zt)) for _ in range(3)]
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+    for i in {0, batch - 1}:
+        assert rel(outs[0][i], O.tv_chambolle(zs[i], 0.05, 10)) <= TOL_OP
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, %r); import ms2g_synth as S; "
+            "import paper_2203_07308_b200 as P; P.load(); n, b = %d, %d; "
+            "z = np.stack([S.random_image(n, 500 + i) for i in range(b)]).astype(np.float32); "
+            "pl = P.plan_geometry(n, 8, 2 * n, factors=(1,), batch=b); "
+            "o = P.denoise(pl, ('tv', 0.05, 10), torch.from_numpy(z).cuda()); torch.cuda.synchronize(); "
+            "sys.stdout.buffer.write(o.cpu().numpy().tobytes())" % (root, n, batch))
+    # the K + 1-launch form, and the persistent form forced to rounds of 3
+    # iterations (halo exchanges through global memory between rounds)
+    for extra in ({"MS2G_TV_PERSIST": "0"}, {"MS2G_TV_PERSIST": "1"}, {"MS2G_TV_PERSIST": "1", "MS2G_TV_KROUND": "3"},
+                  {"MS2G_TV_PERSIST": "1", "MS2G_TV_KROUND": "1"}):
+        env = dict(os.environ, **extra)
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, env=env, timeout=300)
+        assert out.returncode == 0, out.stderr.decode()[-2000:]
+        other = np.frombuffer(out.stdout, dtype=np.float32).reshape(outs[0].shape)
+        assert np.array_equal(other.astype(np.float64), outs[0]), extra
+
+
+def test_gather_adjoint_variant_parity(P):
+    """The pixel-driven gather adjoint (MS2G_BP_VARIANT=gather, the measured
+    alternative to the tile-driven scatter) against the oracle on zero-mean
+    sinograms: ragged grids, factors, a view subset and a batch, plus a short
+    solve -- run in a subprocess so the switch is read fresh."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import ms2g_synth as S, oracle as O, paper_2203_07308_b200 as P
+P.load()
+def rel(a, b):
+    d = a - b
+    return max(np.linalg.norm(d) / np.linalg.norm(b), np.abs(d).max() / np.sqrt(np.mean(b ** 2)) / 10)
+worst = 0.0
+for n, V, B, facs, batch, sub in ((64, 90, 96, (2, 1), 1, None), (40, 20, 62, (2, 1), 2, [1, 4, 7, 9, 15]),
+                                  (96, 33, 150, (3, 1), 1, list(range(0, 33, 3))), (256, 360, 384, (4, 1), 1, None)):
+    g = O.Geometry(n, V, B)
+    views = sub if sub is not None else list(range(V))
+    with P.plan_geometry(n, V, B, factors=facs, batch=batch) as plan:
+        for s in facs:
+            r = np.stack([S.random_sinogram((len(views), B), 90 + s + i) for i in range(batch)])
+            img = P.back_project(plan, s, torch.from_numpy(r).cuda(), subset=sub).cpu().numpy()
+            for i in range(batch):
+                worst = max(worst, rel(img[i].astype(np.float64), O.backward(g, s, r[i], views=sub)))
+pr = S.PRESETS[1]
+g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+b = S.gaussian_data(O.forward(g, 1, S.phantom(pr.n, pr.n_ellipses, S.config_seed(1))), 0.01, S.config_seed(1))
+with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1)) as plan:
+    xo = P.pnp_ms2g_solve(plan, pr.stages, torch.from_numpy(b).cuda()[None], den=pr.den, alpha=pr.alpha)
+xr, _, _ = O.pnp_ms2g(g, pr.stages, b, den=pr.den, alpha=pr.alpha)
+print(worst, np.linalg.norm(xo[0].cpu().numpy() - xr) / np.linalg.norm(xr))
+''' % root
+    env = dict(os.environ, MS2G_BP_VARIANT="gather")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    op_err, solve_err = map(float, out.stdout.split()[-2:])
+    assert op_err <= TOL_OP, op_err
+    assert solve_err <= TOL_SOLVE, solve_err

@@ -316,8 +316,35 @@ def shard_estimate(P, dev, pr, b_full, t_solve_1):
         out[f"N{nr}"] = {"max_shard_solve_ms": ts * 1e3, "shard_solve_ms": [round(v, 3) for v in shard_ms],
                          "allreduce_model_ms": t_ar * 1e3, "est_iters_per_s": pr.n_steps / t,
                          "est_speedup": t_solve_1 / t}
-    out["note"] = ("estimated: slowest rank shard timed on 1 GPU (L2 not flushed) + modelled allreduce; "
-                   "not measured scaling")
+    # the same at 8 ranks with the NEXT-3 peer path's graph shape (publish
+    # fused into the chunk sum, reduce-scatter, all-gather fused with the step;
+    # at one rank the exchange kernels run but move nothing across NVLink),
+    # plus a model of what they would move: 2 (P-1)/P of the image per rank at
+    # 700 GB/s and 5 us for the two signal hops, per gradient and power step
+    nr = 8
+    shard_ms = []
+    for r in range(nr):
+        vb, ve = P.view_shard(pr.n_views, r, nr)
+        with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), view_begin=vb, view_end=ve) as plan:
+            P.attach_peers(plan, 0, 1)
+            b = torch.from_numpy(np.ascontiguousarray(b_full[vb:ve])).to(dev)[None].contiguous()
+            x0 = torch.zeros((1, pr.n, pr.n), device=dev); xo = torch.empty_like(x0)
+            kw = dict(den=pr.den, alpha=pr.alpha, power_iters=pr.power_iters)
+            shard_ms.append(1e3 * time_calls(lambda: P.pnp_ms2g_solve_async(plan, pr.stages, b, x0, xo, **kw), 3,
+                                             warm=2))
+            try:
+                P.solve_status(plan)
+            except P.MS2GError:
+                pass
+    t_pe = sum(n * (5e-6 + 2 * (nr - 1) / nr * 4 * (pr.n // f) ** 2 / 700e9) for f, n in n_ar.items())
+    ts = max(shard_ms) / 1e3
+    out["N8_peer"] = {"max_shard_solve_ms": ts * 1e3, "shard_solve_ms": [round(v, 3) for v in shard_ms],
+                      "exchange_model_ms": t_pe * 1e3, "est_iters_per_s": pr.n_steps / (ts + t_pe),
+                      "est_speedup": t_solve_1 / (ts + t_pe)}
+    out["note"] = ("estimated: slowest rank shard timed on 1 GPU (L2 not flushed) + modelled allreduce (NCCL: 20 us + "
+                   "2 x bytes at 450 GB/s; N8_peer: NEXT-3 reduce-scatter/all-gather, 5 us + 2 (P-1)/P x bytes at "
+                   "700 GB/s -- at one rank its reduce-scatter still passes the whole image, P times its share at "
+                   "P ranks, so N8_peer overstates the shard time); not measured scaling")
     return out
 
 

@@ -100,6 +100,21 @@ int ms2g_attach_nccl(ms2g_plan* plan, const void* unique_id_128_bytes, int32_t r
  * lasts 20 s of wall time (a rank never arrived) gives up: the next
  * ms2g_solve_status / synchronous solve returns MS2G_ERR_NCCL and the plan
  * refuses exchanges until every rank calls ms2g_attach_peers again. */
+/* NEXT-3, NVLS form: the same sum reduced IN the NVSwitch (multimem.ld_reduce
+ * on a multicast object, broadcast with multimem.st), precedence over peers
+ * and NCCL once attached.  Rank 0 calls ms2g_mc_create (creates the object
+ * for nranks devices, writes ms2g_mc_blob_size() bytes: its pid and a POSIX
+ * file descriptor of the object); the caller broadcasts rank 0's blob; every
+ * rank calls ms2g_attach_multicast(phase 0) (import via pidfd_getfd, add its
+ * device), then -- after a process-group barrier -- phase 1 (allocate, bind,
+ * map).  MS2G_ERR_CUDA names the failing driver call: where NVLS multicast
+ * is unavailable (one GPU; no NVSwitch multicast) ms2g_mc_create fails
+ * cleanly and the plan keeps its other paths.  Unexercised beyond that
+ * failure on the single-GPU development pool. */
+int ms2g_mc_blob_size(void);
+int ms2g_mc_create(ms2g_plan* plan, int32_t nranks, void* blob_out);
+int ms2g_attach_multicast(ms2g_plan* plan, const void* blob_rank0, int32_t rank, int32_t nranks, int32_t phase);
+
 int ms2g_peer_blob_size(void);
 int ms2g_peer_export(ms2g_plan* plan, void* blob_out);
 int ms2g_attach_peers(ms2g_plan* plan, const void* blobs_all_ranks, int32_t rank, int32_t nranks);

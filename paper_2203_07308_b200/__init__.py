@@ -20,6 +20,7 @@ __all__ = [
     "sketch_up", "sketched_grad", "power_iteration", "denoise", "schedule", "schedule_views", "pnp_ms2g_solve",
     "pnp_ms2g_solve_async", "solve_status", "attach_nccl", "attach_peers", "view_shard", "set_kernel_timing",
     "kernel_time", "launch_count", "lib_path", "load", "register_subset", "release_subset", "RegisteredSubset",
+    "attach_multicast",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -107,6 +108,8 @@ def load():
     L.ms2g_last_error.restype = C.c_char_p
     L.ms2g_launch_count.restype = C.c_uint64
     L.ms2g_plan_info.argtypes = [p, i, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(i)]
+    L.ms2g_mc_create.argtypes = [p, i, p]
+    L.ms2g_attach_multicast.argtypes = [p, p, i, i, i]
     L.ms2g_register_subset.argtypes = [p, C.POINTER(C.c_int32), i, C.POINTER(i)]
     L.ms2g_release_subset.argtypes = [p, i]
     L.ms2g_forward_project_registered.argtypes = [p, i, p, p, p, i, p]
@@ -498,3 +501,33 @@ def view_shard(n_views: int, rank: int, nranks: int):
 
 def launch_count() -> int:
     return int(load().ms2g_launch_count())
+
+
+def attach_multicast(plan: Plan, rank: int, nranks: int, group=None):
+    """NEXT-3, NVLS form: rank 0 creates the NVSwitch multicast object, the
+    process group broadcasts its blob, every rank imports it and adds its
+    device, a barrier, then every rank binds and maps its buffer.  Raises
+    MS2GError (code 5, naming the driver call) where multicast is unavailable;
+    the plan then keeps its NCCL / peer paths."""
+    import torch.distributed as dist
+    L = load()
+    size = L.ms2g_mc_blob_size()
+    blob = None
+    err = None
+    if rank == 0:
+        buf = C.create_string_buffer(size)
+        rc = L.ms2g_mc_create(plan.handle, nranks, buf)
+        blob = buf.raw if rc == MS2G_OK else None
+        err = None if rc == MS2G_OK else (rc, L.ms2g_last_error().decode(errors="replace"))
+    if nranks > 1:
+        obj = [(blob, err)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        blob, err = obj[0]
+    if err is not None:
+        raise MS2GError(*err)
+    b = C.create_string_buffer(blob, len(blob))
+    _check(L.ms2g_attach_multicast(plan.handle, b, rank, nranks, 0))
+    if nranks > 1:
+        dist.barrier(group=group)
+    _check(L.ms2g_attach_multicast(plan.handle, b, rank, nranks, 1))
+    plan.rank, plan.nranks = rank, nranks

@@ -555,10 +555,14 @@ int launch_tv_persist(const TvWs& ws, int n, int batch, float lambda, float tau,
   static const bool off = getenv("MS2G_TV_PERSIST") && atoi(getenv("MS2G_TV_PERSIST")) == 0;   // experiment switch
   static const int kmax_env = getenv("MS2G_TV_KROUND") ? atoi(getenv("MS2G_TV_KROUND")) : 0;    // experiment switch
   if (off || !ws.flags || iters < 1) return MS2G_OK;
-  // Measured on B200 (scripts/tv_probe.py, K = 10): batch 8 at 512^2 126.7 vs
-  // 167.1 us, 1024^2 81.7 vs 106.5 us for the K + 1 launches; a single image
-  // at <= 512^2 is latency-bound either way (47-61 vs 50 us), so it keeps the
-  // per-iteration kernels (MS2G_TV_PERSIST=1 forces this form).
+  // Rounds of at most 5 iterations (measured on B200, scripts/tv_probe.py,
+  // profiles/r02_tv_probe.log, K = 10, us per call vs the K + 1 launches:
+  // 512^2 x 8 126.6 vs 167.1, 1024^2 81.7 vs 106.5; longer rounds recompute
+  // more halo rows than the exchanges they save).  A single image of at most
+  // 512^2 keeps the K + 1 launches: inside a solve graph they run back to
+  // back, and the C3 solve measured 1 ms slower with the persistent form
+  // (cached-step solve 6.54 vs 5.58 ms, profiles/r02_launches_solve_c3.md);
+  // MS2G_TV_PERSIST=1 forces it.
   static const bool force = getenv("MS2G_TV_PERSIST") && atoi(getenv("MS2G_TV_PERSIST")) == 1;
   if (!force && batch == 1 && n <= 512) return MS2G_OK;
   const int total_rows = n * batch;
@@ -568,7 +572,7 @@ int launch_tv_persist(const TvWs& ws, int n, int batch, float lambda, float tau,
   if (C > ws.max_ctas) return MS2G_OK;
   // the longest round that fits, with f in shared memory or (if that allows
   // fewer rounds) read from L2
-  const int kcap = kmax_env > 0 ? std::min(iters, kmax_env) : iters;
+  const int kcap = std::min(iters, kmax_env > 0 ? kmax_env : 5);
   auto kfit = [&](bool wf) {
     int kk = kcap;
     while (kk >= 1 && tv_persist_smem(n, rows_per, kk, wf) > (size_t)ws.smem_optin) --kk;

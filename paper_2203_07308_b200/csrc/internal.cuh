@@ -178,6 +178,13 @@ struct ms2g_plan {
   int* w_peer_err = nullptr;
   int peer_rank = 0, peer_n = 0;       // peer_n > 0: attached
   bool peer_failed = false;            // a barrier timed out: exchanges refused until re-attached
+  // NVLS multicast exchange (multicast.cu): object + physical memory handles,
+  // unicast and multicast views of the PUB | RED | flags buffer
+  unsigned long long mc_handle = 0, mc_mem = 0;
+  size_t mc_size = 0;
+  void* mc_uc = nullptr;
+  void* mc_mc = nullptr;
+  int mc_rank = 0, mc_n = 0;           // mc_n > 0: attached
   std::vector<void*> peer_opened;      // IPC mappings to close
   // Power-iteration branches of the solve graph: one per stage factor, each
   // with its own workspaces (batch 1), so the geometry-only power chains of
@@ -296,6 +303,18 @@ int launch_peer_finish_step(ms2g_plan* p, size_t count, int nc, int s, const flo
                             float* z, cudaStream_t st);
 int launch_chunk_reduce_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
                                 cudaStream_t st);
+
+// ---- NVLS multicast allreduce (multicast.cu, NEXT-3) ----
+int mc_blob_size();
+int mc_create(ms2g_plan* p, int nranks, void* blob_out);
+int mc_attach(ms2g_plan* p, const void* blob0, int rank, int nranks, int phase);
+void mc_release(ms2g_plan* p);
+int launch_mc_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
+                      cudaStream_t st);
+// reduce in the switch + all-gather into out (s == 0) or the step z = y - eta U_s G (out = z, s >= 1)
+int launch_mc_finish(ms2g_plan* p, size_t count, float* out, int nc, int s, const float* y, const float* eta_dev,
+                     cudaStream_t st);
+int launch_mc_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st);
 
 // ---- image kernels (image_ops.cu) ----
 int launch_sketch_down(int n, int s, int batch, const float* x, float* v, cudaStream_t st);

@@ -9,7 +9,19 @@
 #include <cstring>
 #include <sstream>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
+
+// NVTX range around every compute entry point (SURVEY §5 tracing): visible
+// to Nsight tools (ncu --nvtx-include, nsys) when they are attached; a no-op
+// otherwise (NVTX v3 is header-only and binds an injection library lazily).
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace ms2g {
 
@@ -379,6 +391,7 @@ static void free_plan(ms2g_plan* p) {
   }
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   for (void* q : p->peer_opened) cudaIpcCloseMemHandle(q);
+  mc_release(p);
   cudaFree(p->xch_buf);
   cudaFree(p->xch_pad);
   cudaFree(p->d_peer_bufs);
@@ -452,7 +465,11 @@ static int peer_ok(const ms2g_plan* p) {
 }
 
 static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
-  if (p->peer_n > 0) {                      // NEXT-3 peer path wins
+  if (p->mc_n > 0) {                        // NEXT-3 NVLS multicast path wins
+    MS2G_TRY(peer_ok(p));
+    return launch_mc_allreduce(p, buf, count, st);
+  }
+  if (p->peer_n > 0) {                      // then the NEXT-3 peer path
     MS2G_TRY(peer_ok(p));
     return launch_peer_allreduce(p, buf, count, st);
   }
@@ -467,6 +484,11 @@ static int allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t st) {
 static int backward_sum(ms2g_plan* p, const FactorTables& f, const float* sino, float* G, float c, const int* d_sel,
                         int n_sel, int batch, cudaStream_t st, const int* order_sel = nullptr) {
   const size_t count = (size_t)f.nc * f.nc * batch;
+  if (p->mc_n > 0) {
+    MS2G_TRY(peer_ok(p));
+    MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st, 3, order_sel));
+    return launch_mc_finish(p, count, G, 0, 0, nullptr, nullptr, st);
+  }
   if (p->peer_n > 0) {
     MS2G_TRY(peer_ok(p));
     MS2G_TRY(launch_backward(p, f, sino, G, c, 0, d_sel, n_sel, batch, st, 1, order_sel));
@@ -479,7 +501,7 @@ static int backward_sum(ms2g_plan* p, const FactorTables& f, const float* sino, 
 // Single-rank plans reduce the backprojection's partial planes in a fused
 // epilogue (the step, the power iteration); with a communicator or peers the
 // partial image is summed over ranks first (G = allreduce), then consumed.
-static bool fused_epilogue(const ms2g_plan* p) { return p->peer_n == 0 && !p->comm; }
+static bool fused_epilogue(const ms2g_plan* p) { return p->peer_n == 0 && p->mc_n == 0 && !p->comm; }
 
 // Pair images of v = S_s(src) for the forward: kind 0 fuses the s x s mean
 // into the pair prep (one launch); bicubic resamples into w_v first.
@@ -500,6 +522,11 @@ static int backward_step(ms2g_plan* p, const FactorTables& f, int kind, const fl
     int npl = 0;
     MS2G_TRY(launch_backward(p, f, sino, nullptr, c, 0, d_sel, n_sel, batch, st, 2, bord, &npl));
     return launch_reduce_up_step(p->w_part, npl, f.nc, batch, c, y, eta_dev, z, f.factor, st);
+  }
+  if (kind == 0 && p->mc_n > 0) {     // NEXT-3 NVLS: publish, in-switch reduce + broadcast, step
+    MS2G_TRY(peer_ok(p));
+    MS2G_TRY(launch_backward(p, f, sino, nullptr, c, 0, d_sel, n_sel, batch, st, 3, bord));
+    return launch_mc_finish(p, (size_t)f.nc * f.nc * batch, z, f.nc, f.factor, y, eta_dev, st);
   }
   if (kind == 0 && p->peer_n > 0) {   // NEXT-3: publish (fused chunk sum), reduce-scatter, all-gather + step
     MS2G_TRY(peer_ok(p));
@@ -715,7 +742,7 @@ static bool power_branching(const ms2g_plan* p) {
   static const bool off = getenv("MS2G_SERIAL_POWER") != nullptr;   // experiment switch
   // kernel timing wants each launch's own duration: concurrent branches would
   // share the GPU inside the timed intervals, so an instrumented solve is serial
-  return !off && !p->timing && p->nranks == 1 && !p->comm && p->peer_n == 0;
+  return !off && !p->timing && p->nranks == 1 && !p->comm && p->peer_n == 0 && p->mc_n == 0;
 }
 
 static int ensure_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd) {
@@ -907,7 +934,7 @@ static std::string solve_key(const ms2g_solve_desc* sd, const float* b, const fl
 static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b, const float* x0, float* x_out,
                         cudaStream_t st) {
   if (!b || !x0 || !x_out) return set_error(MS2G_ERR_INPUT, "NULL b/x0/x_out");
-  if (p->peer_n > 0) MS2G_TRY(peer_ok(p));   // a cached graph would replay the failed exchange
+  if (p->peer_n > 0 || p->mc_n > 0) MS2G_TRY(peer_ok(p));   // a cached graph would replay the failed exchange
   if (!(sd->alpha > 0.f && sd->alpha <= 1.f)) return set_error(MS2G_ERR_CONFIG, "alpha must be in (0, 1] (S:197)");
   if (sd->power_iters < 0) return set_error(MS2G_ERR_CONFIG, "power_iters must be >= 0");
   if (sd->resampler != 0 && sd->resampler != 1) return set_error(MS2G_ERR_CONFIG, "resampler must be 0 or 1");
@@ -1012,6 +1039,7 @@ const char* ms2g_last_error(void) { return t_err.c_str(); }
 uint64_t ms2g_launch_count(void) { return g_launches.load(); }
 
 int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32_t n_factors, ms2g_plan** out) {
+  NvtxRange nvtx_range__("ms2g_plan_geometry");
   t_err.clear();
   if (!desc || !out) return set_error(MS2G_ERR_INPUT, "NULL desc/out");
   *out = nullptr;
@@ -1077,7 +1105,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     MS2G_CUDA(cudaMalloc(q, sizeof(float) * (count ? count : 1)));
     return MS2G_OK;
   };
-  p->red_blocks = 2 * sms;
+  p->red_blocks = 8 * sms;   // k_reduce_power: enough blocks to stream the partial planes at full bandwidth
   p->pair_stride = (size_t)p->nmax_c * (p->nmax_c + 3) * bt;
   e = cudaMalloc(&p->w_pair, sizeof(float2) * 4 * p->pair_stride);
   if (e != cudaSuccess) {
@@ -1183,6 +1211,7 @@ int ms2g_nccl_unique_id(void* out) {
 }
 
 int ms2g_attach_nccl(ms2g_plan* p, const void* uid, int32_t rank, int32_t nranks) {
+  NvtxRange nvtx_range__("ms2g_attach_nccl");
   if (!p || !uid) return set_error(MS2G_ERR_INPUT, "NULL plan/id");
   if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(MS2G_ERR_CONFIG, "bad rank/nranks");
   ncclUniqueId id;
@@ -1245,6 +1274,7 @@ int ms2g_peer_export(ms2g_plan* p, void* blob) {
 }
 
 int ms2g_attach_peers(ms2g_plan* p, const void* blobs, int32_t rank, int32_t nranks) {
+  NvtxRange nvtx_range__("ms2g_attach_peers");
   if (!p || !blobs) return set_error(MS2G_ERR_INPUT, "NULL plan/blobs");
   if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) return set_error(MS2G_ERR_CONFIG, "bad rank/nranks");
   if (p->peer_n > 0 && !p->peer_failed) return set_error(MS2G_ERR_CONFIG, "peers already attached");
@@ -1424,7 +1454,7 @@ static int check_bwd(ms2g_plan* p, int32_t factor, const float* sino, const floa
   if (!p || !sino || !img) return set_error(MS2G_ERR_INPUT, "NULL plan/sino/img");
   *f = find_factor(p, factor);
   if (!*f) return set_error(MS2G_ERR_CONFIG, "factor not in plan");
-  if (do_allreduce && !p->comm && !p->peer_n && p->nranks > 1)
+  if (do_allreduce && !p->comm && !p->peer_n && !p->mc_n && p->nranks > 1)
     return set_error(MS2G_ERR_CONFIG, "allreduce needs attach_nccl or attach_peers");
   return MS2G_OK;
 }
@@ -1439,8 +1469,41 @@ static int check_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* x
   return MS2G_OK;
 }
 
+int ms2g_mc_blob_size(void) { return mc_blob_size(); }
+
+int ms2g_mc_create(ms2g_plan* p, int32_t nranks, void* blob_out) {
+  if (!p || !blob_out) return set_error(MS2G_ERR_INPUT, "NULL plan/blob");
+  if (p->mc_n > 0 || p->mc_handle) return set_error(MS2G_ERR_CONFIG, "multicast already created / attached");
+  if (!p->xch_slot) p->xch_slot = (size_t)p->nmax_c * p->nmax_c * p->d.batch;
+  return mc_create(p, nranks, blob_out);
+}
+
+int ms2g_attach_multicast(ms2g_plan* p, const void* blob_rank0, int32_t rank, int32_t nranks, int32_t phase) {
+  if (!p || !blob_rank0) return set_error(MS2G_ERR_INPUT, "NULL plan/blob");
+  if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks || (phase != 0 && phase != 1))
+    return set_error(MS2G_ERR_CONFIG, "bad rank/nranks/phase");
+  if (p->mc_n > 0) return set_error(MS2G_ERR_CONFIG, "multicast already attached");
+  if (!p->xch_slot) p->xch_slot = (size_t)p->nmax_c * p->nmax_c * p->d.batch;
+  MS2G_TRY(mc_attach(p, blob_rank0, rank, nranks, phase));
+  if (phase == 1) {
+    for (auto& gg : p->grad_graphs) {
+      if (gg.exec) cudaGraphExecDestroy(gg.exec);
+      if (gg.graph) cudaGraphDestroy(gg.graph);
+    }
+    p->grad_graphs.clear();
+    p->topo_version++;
+    if (p->sg.exec) {
+      cudaGraphExecDestroy(p->sg.exec);
+      cudaGraphDestroy(p->sg.graph);
+      p->sg = SolveGraph{};
+    }
+  }
+  return MS2G_OK;
+}
+
 int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* out,
                          const int32_t* subset, int32_t n_subset, void* stream) {
+  NvtxRange nvtx_range__("ms2g_forward_project");
   const FactorTables* f;
   MS2G_TRY(check_fwd(p, factor, x, out, &f));
   cudaStream_t st = (cudaStream_t)stream;
@@ -1453,6 +1516,7 @@ int ms2g_forward_project(ms2g_plan* p, int32_t factor, const float* x, const flo
 
 int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* img, float scale, int32_t accumulate,
                       const int32_t* subset, int32_t n_subset, int32_t do_allreduce, void* stream) {
+  NvtxRange nvtx_range__("ms2g_back_project");
   const FactorTables* f;
   MS2G_TRY(check_bwd(p, factor, sino, img, do_allreduce, &f));
   cudaStream_t st = (cudaStream_t)stream;
@@ -1465,6 +1529,7 @@ int ms2g_back_project(ms2g_plan* p, int32_t factor, const float* sino, float* im
 
 int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, const float* b, float* g,
                        const int32_t* subset, int32_t n_subset, void* stream) {
+  NvtxRange nvtx_range__("ms2g_sketched_grad");
   const FactorTables* f;
   MS2G_TRY(check_grad(p, factor, kind, x, b, g, &f));
   cudaStream_t st = (cudaStream_t)stream;
@@ -1476,6 +1541,7 @@ int ms2g_sketched_grad(ms2g_plan* p, int32_t factor, int32_t kind, const float* 
 }
 
 int ms2g_register_subset(ms2g_plan* p, const int32_t* subset, int32_t n_subset, int32_t* id) {
+  NvtxRange nvtx_range__("ms2g_register_subset");
   if (!p || !subset || !id) return set_error(MS2G_ERR_INPUT, "NULL plan/subset/id");
   int m = 0;
   MS2G_TRY(check_subset(p, subset, n_subset, &m));
@@ -1518,6 +1584,7 @@ int ms2g_release_subset(ms2g_plan* p, int32_t id) {
 
 int ms2g_forward_project_registered(ms2g_plan* p, int32_t factor, const float* x, const float* b, float* out,
                                     int32_t subset_id, void* stream) {
+  NvtxRange nvtx_range__("ms2g_forward_project_registered");
   const FactorTables* f;
   MS2G_TRY(check_fwd(p, factor, x, out, &f));
   Sel s;
@@ -1527,6 +1594,7 @@ int ms2g_forward_project_registered(ms2g_plan* p, int32_t factor, const float* x
 
 int ms2g_back_project_registered(ms2g_plan* p, int32_t factor, const float* sino, float* img, float scale,
                                  int32_t accumulate, int32_t subset_id, int32_t do_allreduce, void* stream) {
+  NvtxRange nvtx_range__("ms2g_back_project_registered");
   const FactorTables* f;
   MS2G_TRY(check_bwd(p, factor, sino, img, do_allreduce, &f));
   Sel s;
@@ -1536,6 +1604,7 @@ int ms2g_back_project_registered(ms2g_plan* p, int32_t factor, const float* sino
 
 int ms2g_sketched_grad_registered(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, const float* b,
                                   float* g, int32_t subset_id, void* stream) {
+  NvtxRange nvtx_range__("ms2g_sketched_grad_registered");
   const FactorTables* f;
   MS2G_TRY(check_grad(p, factor, kind, x, b, g, &f));
   Sel s;
@@ -1544,6 +1613,7 @@ int ms2g_sketched_grad_registered(ms2g_plan* p, int32_t factor, int32_t kind, co
 }
 
 int ms2g_sketch_down(ms2g_plan* p, int32_t factor, int32_t kind, const float* x, float* v, void* stream) {
+  NvtxRange nvtx_range__("ms2g_sketch_down");
   if (!p || !x || !v) return set_error(MS2G_ERR_INPUT, "NULL plan/x/v");
   if (factor < 1 || p->d.n % factor) return set_error(MS2G_ERR_CONFIG, "factor must divide n (S:127)");
   if (kind != 0 && kind != 1) return set_error(MS2G_ERR_CONFIG, "kind must be 0 (mean) or 1 (bicubic)");
@@ -1555,6 +1625,7 @@ int ms2g_sketch_down(ms2g_plan* p, int32_t factor, int32_t kind, const float* x,
 
 int ms2g_sketch_up(ms2g_plan* p, int32_t factor, int32_t kind, const float* g, const float* y, float eta, float* z,
                    void* stream) {
+  NvtxRange nvtx_range__("ms2g_sketch_up");
   if (!p || !g || !z) return set_error(MS2G_ERR_INPUT, "NULL plan/g/z");
   if (factor < 1 || p->d.n % factor) return set_error(MS2G_ERR_CONFIG, "factor must divide n");
   if (kind != 0 && kind != 1) return set_error(MS2G_ERR_CONFIG, "kind must be 0 (replicate) or 1 (bicubic)");
@@ -1565,6 +1636,7 @@ int ms2g_sketch_up(ms2g_plan* p, int32_t factor, int32_t kind, const float* g, c
 }
 
 int ms2g_power_iteration(ms2g_plan* p, int32_t factor, int32_t iters, double* L, void* stream) {
+  NvtxRange nvtx_range__("ms2g_power_iteration");
   if (!p || !L) return set_error(MS2G_ERR_INPUT, "NULL plan/L");
   if (iters < 1) return set_error(MS2G_ERR_CONFIG, "iters must be >= 1");
   const FactorTables* f = find_factor(p, factor);
@@ -1577,6 +1649,7 @@ int ms2g_power_iteration(ms2g_plan* p, int32_t factor, int32_t iters, double* L,
 }
 
 int ms2g_denoise(ms2g_plan* p, const ms2g_denoiser* den, const float* z, float* out, void* stream) {
+  NvtxRange nvtx_range__("ms2g_denoise");
   if (!p || !den || !z || !out) return set_error(MS2G_ERR_INPUT, "NULL plan/den/z/out");
   if (z == out) return set_error(MS2G_ERR_INPUT, "z and out must not alias");
   MS2G_TRY(check_denoiser(*den));
@@ -1619,6 +1692,7 @@ int ms2g_schedule_views(const ms2g_plan* p, const ms2g_solve_desc* sd, int32_t s
 
 int ms2g_pnp_ms2g_solve_async(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b, const float* x0,
                               float* x_out, void* stream) {
+  NvtxRange nvtx_range__("ms2g_pnp_ms2g_solve_async");
   if (!p || !sd) return set_error(MS2G_ERR_INPUT, "NULL plan/desc");
   return solve_launch(p, sd, b, x0, x_out, (cudaStream_t)stream);
 }
@@ -1630,6 +1704,7 @@ int ms2g_solve_status(ms2g_plan* p, void* stream) {
 
 int ms2g_pnp_ms2g_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b, const float* x0, float* x_out,
                         ms2g_sched_entry* trace, void* stream) {
+  NvtxRange nvtx_range__("ms2g_pnp_ms2g_solve");
   if (!p || !sd) return set_error(MS2G_ERR_INPUT, "NULL plan/desc");
   cudaStream_t st = (cudaStream_t)stream;
   MS2G_TRY(solve_launch(p, sd, b, x0, x_out, st));

@@ -844,8 +844,10 @@ int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, flo
 int launch_reduce_power(ms2g_plan* p, const float* part, int nplanes, size_t np, float* w_out, const float* v,
                         double* red, int red_blocks, unsigned* ticket, double* pw, double* L_out, double* eta_out,
                         float* etaf_out, cudaStream_t st) {
-  k_reduce_power<<<red_blocks, 256, 0, st>>>(part, nplanes, np, w_out, v, red, ticket, pw, L_out, eta_out,
-                                             etaf_out);
+  // one pass over nplanes x np floats: as many blocks as the buffer allows
+  // (the fixed-order last-block reduction handles any grid size)
+  const int blocks = (int)std::min<size_t>((size_t)red_blocks, std::max<size_t>(1, (np + 255) / 256));
+  k_reduce_power<<<blocks, 256, 0, st>>>(part, nplanes, np, w_out, v, red, ticket, pw, L_out, eta_out, etaf_out);
   return check_launch("k_reduce_power");
 }
 
@@ -905,6 +907,7 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
     timing_end(p, slot, s);
     if (nplanes_out) *nplanes_out = nch;
     if (publish == 2) return MS2G_OK;
+    if (publish == 3) return launch_mc_publish(p, p->w_part, nch, np, total, scale, s);
     if (publish) return launch_chunk_reduce_publish(p, p->w_part, nch, np, total, scale, s);
     const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);
     k_chunk_reduce<<<dim3(blocks, batch), 256, 0, s>>>(p->w_part, nch, np, img, scale, accumulate);
@@ -927,6 +930,7 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   timing_end(p, slot, s);
   if (nplanes_out) *nplanes_out = ch[0] + ch[1];
   if (publish == 2) return MS2G_OK;   // partial planes only: the caller's fused epilogue sums them
+  if (publish == 3) return launch_mc_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);   // NVLS
   if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)
     return launch_chunk_reduce_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);
   const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);

@@ -905,3 +905,25 @@ print(worst, np.linalg.norm(xo[0].cpu().numpy() - xr) / np.linalg.norm(xr))
     op_err, solve_err = map(float, out.stdout.split()[-2:])
     assert op_err <= TOL_OP, op_err
     assert solve_err <= TOL_SOLVE, solve_err
+
+
+def test_multicast_attach_fails_cleanly_on_one_gpu(P):
+    """NEXT-3 NVLS path: on this pool's single-GPU boxes cuMulticastCreate is
+    unavailable, so attach_multicast raises MS2G_ERR_CUDA naming the driver
+    call, and the plan keeps working (same gradient as before the attempt)."""
+    n, V, B = 64, 45, 96
+    x = S.phantom(n, 6, 3)
+    b = S.random_sinogram((V, B), 4, zero_mean=False)
+    with P.plan_geometry(n, V, B, factors=(2, 1)) as plan:
+        g0 = host(P.sketched_grad(plan, 2, dev(x)[None], dev(b)[None]))
+        try:
+            P.attach_multicast(plan, 0, 1)
+            attached = True
+        except P.MS2GError as e:
+            attached = False
+            assert e.code == 5 and "NVLS multicast" in str(e), str(e)
+        g1 = host(P.sketched_grad(plan, 2, dev(x)[None], dev(b)[None]))
+        if attached:      # a box with working multicast: the 1-rank in-switch sum is the identity
+            assert rel(g1, g0) <= 1e-6
+        else:
+            assert np.array_equal(g0, g1)

@@ -116,6 +116,7 @@ struct ms2g_plan {
   std::vector<ms2g::FactorTables> ft;
   int nmax_c = 0;                      // largest coarse side among the factors
   int sm_count = 148;                  // SMs of the plan's device
+  int class_mask = 15;                 // ray classes (flags & 3) present in the rank's views, bit per class
   // workspaces (all sized for batch)
   float2* w_pair = nullptr;            // forward gather images: 4 x [batch][n_c][n_c + 3] float2
   size_t pair_stride = 0;              // float2 elements per pair image
@@ -225,6 +226,60 @@ struct ms2g_plan {
 };
 
 namespace ms2g {
+
+// ---- the fixed-order sum of the backprojection's partial planes ----
+// Every consumer of the partial planes (k_chunk_reduce, the fused step and
+// power epilogues, the NEXT-3 publishes) sums them with THIS rule, so all
+// paths give bitwise equal images.  Two orders, chosen from (np, nplanes)
+// alone by plane_groups() -- identically for every consumer of a launch:
+//  * G = 1 (large images: the common case) -- thread t of a 256-thread block
+//    adds all planes of pixel p0 + t in increasing plane order (a 256-pixel
+//    tile per block iteration, loads of independent planes in flight);
+//  * G = 8 (small coarse grids with many view-chunk planes, e.g. 128^2 with
+//    360 planes): too few pixels to fill the GPU one thread per pixel, so
+//    thread (x, g) of the (32 x 8) block adds planes g, g + 8, ... of pixel
+//    p0 + x (a 32-pixel tile), then the 8 group sums are added in order
+//    g = 0..7.
+// sm.tot[t] receives the total of pixel p0 + t (t < plane_tile(G)); all
+// threads of the block must call it; pixels >= np read nothing.
+constexpr int kPlaneGroups = 8;
+struct PlaneSmem {
+  float g[kPlaneGroups][33];
+  float tot[256];
+};
+__host__ __device__ inline int plane_tile(int G) { return G == 1 ? 256 : 32; }
+inline int plane_groups(size_t np, int nplanes) { return (np <= 65536 && nplanes >= 16) ? kPlaneGroups : 1; }
+__device__ __forceinline__ void sum_planes(const float* __restrict__ part, int nplanes, size_t np, size_t p0, int G,
+                                           PlaneSmem& sm) {
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  if (G == 1) {
+    const size_t p = p0 + tid;
+    float s = 0.f;
+    if (p < np)
+      for (int c = 0; c < nplanes; ++c) s += part[(size_t)c * np + p];
+    sm.tot[tid] = s;
+    __syncthreads();
+    return;
+  }
+  const size_t p = p0 + threadIdx.x;
+  float s = 0.f;
+  if (p < np)
+    for (int c = threadIdx.y; c < nplanes; c += kPlaneGroups) s += part[(size_t)c * np + p];
+  sm.g[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (tid < 32) {
+    float t = 0.f;
+#pragma unroll
+    for (int g = 0; g < kPlaneGroups; ++g) t += sm.g[g][tid];
+    sm.tot[tid] = t;
+  }
+  __syncthreads();
+}
+// blocks for the plane sums of np pixels: one tile each, at most `cap`
+inline int plane_blocks(size_t np, int G, int cap) {
+  const size_t t = (np + plane_tile(G) - 1) / plane_tile(G);
+  return (int)(t < (size_t)cap ? (t ? t : 1) : cap);
+}
 
 // error handling (thread-local message)
 int set_error(int code, const std::string& msg);

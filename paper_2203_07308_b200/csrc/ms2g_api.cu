@@ -237,6 +237,8 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     }
     ve.seg_t[ve.nseg] = (short)B;
     views[vl] = ve;
+    if (f.factor == p->ft[0].factor)   // classes depend on the ray directions only (all factors alike)
+      for (int k = 0; k < ve.nseg; ++k) p->class_mask |= 1 << (ve.seg_cls[k] & 3);
   }
   MS2G_CUDA(cudaMalloc(&f.d_rays, sizeof(RayEntry) * rays.size()));
   MS2G_CUDA(cudaMalloc(&f.d_views, sizeof(ViewEntry) * views.size()));
@@ -1089,6 +1091,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
   int rc = MS2G_OK;
   size_t part = 1;
   p->sm_count = sms;
+  p->class_mask = 0;   // filled by build_tables
   for (auto& f : p->ft) {
     rc = build_tables(p, f, sms);
     if (rc != MS2G_OK) {
@@ -1105,7 +1108,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     MS2G_CUDA(cudaMalloc(q, sizeof(float) * (count ? count : 1)));
     return MS2G_OK;
   };
-  p->red_blocks = 8 * sms;   // k_reduce_power: enough blocks to stream the partial planes at full bandwidth
+  p->red_blocks = 8 * sms;   // k_reduce_power grid cap (fp64 partials per block)
   p->pair_stride = (size_t)p->nmax_c * (p->nmax_c + 3) * bt;
   e = cudaMalloc(&p->w_pair, sizeof(float2) * 4 * p->pair_stride);
   if (e != cudaSuccess) {

@@ -169,7 +169,7 @@ __device__ bool mc_wait(const McArgs& a, int w, unsigned target) {
 // the last block of the launch adds 1 to flag word w on every rank
 __device__ void mc_last_block_signal(const McArgs& a, int w) {
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x != 0 || threadIdx.y != 0) return;
   unsigned* local = mc_flags(a.uc, a.slot);
   __threadfence_system();
   if (atomicAdd(local + 3, 1u) != gridDim.x * gridDim.y - 1) return;   // word 3: ticket
@@ -178,15 +178,17 @@ __device__ void mc_last_block_signal(const McArgs& a, int w) {
   mc_red_add(mc_flags(a.mc, a.slot) + w, 1u);
 }
 
-__global__ void k_mc_publish(const float* __restrict__ part, int nplanes, size_t np, McArgs a, float scale) {
+__global__ void k_mc_publish(const float* __restrict__ part, int nplanes, size_t np, McArgs a, float scale, int G) {
+  __shared__ PlaneSmem sm;
   const size_t b = blockIdx.y;
   float* dst = a.uc + b * np;
-  const float* src0 = part + b * nplanes * np;
-  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-    const float* src = src0 + p;
-    float s = 0.f;
-    for (int c = 0; c < nplanes; ++c) s += src[(size_t)c * np];
-    dst[p] = scale * s;
+  const float* src = part + b * nplanes * np;
+  const int tid = threadIdx.y * 32 + threadIdx.x, tile = plane_tile(G);
+  for (size_t p0 = (size_t)blockIdx.x * tile; p0 < np; p0 += (size_t)gridDim.x * tile) {
+    sum_planes(src, nplanes, np, p0, G, sm);
+    const size_t p = p0 + tid;
+    if (tid < tile && p < np) dst[p] = scale * sm.tot[tid];
+    if (G != 1) __syncthreads();   // tot is rewritten by the next tile
   }
   mc_last_block_signal(a, 0);
 }
@@ -254,8 +256,9 @@ static int mc_grid(size_t n, int cap) {
 int launch_mc_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
                       cudaStream_t st) {
   if (total > p->xch_slot) return set_error(MS2G_ERR_CONFIG, "multicast allreduce larger than the exchange slot");
-  k_mc_publish<<<dim3(mc_grid(np, 4 * p->sm_count), (unsigned)(total / np)), 256, 0, st>>>(part, nplanes, np,
-                                                                                           mc_args(p), scale);
+  const int G = plane_groups(np, nplanes);
+  k_mc_publish<<<dim3(plane_blocks(np, G, 4096), (unsigned)(total / np)), dim3(32, kPlaneGroups), 0, st>>>(
+      part, nplanes, np, mc_args(p), scale, G);
   return check_launch("k_mc_publish");
 }
 

@@ -99,7 +99,7 @@ __device__ bool block_wait(const PeerArgs& a, int base, unsigned e) {
 // bump != 0 it first records e as the local epoch.
 __device__ void last_block_signal(const PeerArgs& a, int base, unsigned e, int bump) {
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x != 0 || threadIdx.y != 0) return;
   unsigned* mine = a.pads[a.rank];
   __threadfence_system();
   if (atomicAdd(mine + kTicket, 1u) != gridDim.x * gridDim.y - 1) return;
@@ -112,16 +112,18 @@ __device__ void last_block_signal(const PeerArgs& a, int base, unsigned e, int b
 // 1a. publish, fused with the backprojection's chunk sum: PUB = scale * sum
 // of the nplanes partial planes (fixed order).  grid.y = batch image.
 __global__ void k_chunk_reduce_publish(const float* __restrict__ part, int nplanes, size_t np, PeerArgs a,
-                                       float scale) {
+                                       float scale, int G) {
+  __shared__ PlaneSmem sm;
   const unsigned e = *(volatile unsigned*)(a.pads[a.rank] + kEpoch) + 1u;
   const size_t b = blockIdx.y;
   float* dst = a.bufs[a.rank] + b * np;
-  const float* src0 = part + b * nplanes * np;
-  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-    const float* src = src0 + p;
-    float s = 0.f;
-    for (int c = 0; c < nplanes; ++c) s += src[(size_t)c * np];
-    dst[p] = scale * s;
+  const float* src = part + b * nplanes * np;
+  const int tid = threadIdx.y * 32 + threadIdx.x, tile = plane_tile(G);
+  for (size_t p0 = (size_t)blockIdx.x * tile; p0 < np; p0 += (size_t)gridDim.x * tile) {
+    sum_planes(src, nplanes, np, p0, G, sm);
+    const size_t p = p0 + tid;
+    if (tid < tile && p < np) dst[p] = scale * sm.tot[tid];
+    if (G != 1) __syncthreads();   // tot is rewritten by the next tile
   }
   last_block_signal(a, kPub, e, 1);
 }
@@ -221,8 +223,9 @@ int launch_peer_allreduce(ms2g_plan* p, float* buf, size_t count, cudaStream_t s
 int launch_chunk_reduce_publish(ms2g_plan* p, const float* part, int nplanes, size_t np, size_t total, float scale,
                                 cudaStream_t st) {
   if (total > p->xch_slot) return set_error(MS2G_ERR_CONFIG, "peer allreduce larger than the exchange slot");
-  k_chunk_reduce_publish<<<dim3(grid_for(np, 4 * p->sm_count), (unsigned)(total / np)), 256, 0, st>>>(
-      part, nplanes, np, peer_args(p), scale);
+  const int G = plane_groups(np, nplanes);
+  k_chunk_reduce_publish<<<dim3(plane_blocks(np, G, 4096), (unsigned)(total / np)), dim3(32, kPlaneGroups), 0, st>>>(
+      part, nplanes, np, peer_args(p), scale, G);
   return check_launch("k_chunk_reduce_publish");
 }
 

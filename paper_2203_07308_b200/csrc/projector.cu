@@ -65,8 +65,13 @@ __device__ __forceinline__ float pair_src(const float* __restrict__ xb, int k, i
   return acc * inv_s2 * scale;
 }
 
+//
+// Batches with il = NB > 1 (experiment switch MS2G_FWD_INTERLEAVE; measured
+// slower, see fwd_launch_batch): the NB images of a group INTERLEAVED,
+// element (line, pos) holding NB consecutive pairs.
 __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pairs, size_t pair_stride, int nc,
-                            int s, const double* __restrict__ scale_dev, float* __restrict__ v_out) {
+                            int s, const double* __restrict__ scale_dev, float* __restrict__ v_out, int class_mask,
+                            int il) {
   __shared__ float T[33][33];
   const int bz = blockIdx.z;
   const int nsrc = nc * s;
@@ -74,7 +79,8 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
   const float inv_s2 = 1.0f / (float)(s * s);
   const float scale = scale_dev ? (float)scale_dev[0] : 1.f;
   const int L = nc + 3;
-  const size_t ib = (size_t)bz * nc * L;
+  const int mul = il > 1 ? il : 1, grp = bz / mul, sub = bz - grp * mul;   // interleaving group / slot
+  const size_t ib = (size_t)grp * nc * L;
   const int O0 = blockIdx.x * 32, L0 = blockIdx.y * 32;   // output positions o, lines
   // rows k = O0-2 .. O0+30 for the column-pair images (this block owns O0-2 .. O0+29)
   for (int r = threadIdx.y; r < 33; r += 8) {
@@ -90,23 +96,31 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
   for (int jj = threadIdx.y; jj < 32; jj += 8) {
     const int line = L0 + jj;
     if (line >= nc) break;
-    const size_t e = ib + (size_t)line * L + o;
+    const size_t e = (ib + (size_t)line * L + o) * mul + sub;
     const float a = T[threadIdx.x][jj], b = T[threadIdx.x + 1][jj];   // v[o-2][line], v[o-1][line]
-    const size_t er = ib + (size_t)line * L + (nc + 2 - o);   // back-to-front line
-    pairs[e] = make_float2(a, b);
-    pairs[2 * pair_stride + er] = make_float2(b, a);
+    const size_t er = (ib + (size_t)line * L + (nc + 2 - o)) * mul + sub;   // back-to-front line
+    // only the ray classes this plan's views contain (a view shard of 45
+    // degrees has one or two): the others are never read by the forward
+    if (class_mask & 1) pairs[e] = make_float2(a, b);
+    if (class_mask & 4) pairs[2 * pair_stride + er] = make_float2(b, a);
+    if (!(class_mask & 10)) continue;
     const int k = o - 2;
     const float c = (k >= 0 && k < nc) ? pair_src(xb, line, k, nc, s, nsrc, inv_s2, scale) : 0.f;
     const float d = (k + 1 >= 0 && k + 1 < nc) ? pair_src(xb, line, k + 1, nc, s, nsrc, inv_s2, scale) : 0.f;
-    pairs[pair_stride + e] = make_float2(c, d);
-    pairs[3 * pair_stride + er] = make_float2(d, c);
+    if (class_mask & 2) pairs[pair_stride + e] = make_float2(c, d);
+    if (class_mask & 8) pairs[3 * pair_stride + er] = make_float2(d, c);
   }
 }
+
+// group size of the batched forward (and of the pair interleaving) for a batch
+static int batch_group(int batch) { return (batch % 8 == 0) ? 8 : (batch % 4 == 0) ? 4 : (batch % 2 == 0) ? 2 : 1; }
 
 int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s, int factor,
                      const double* scale_dev, float* v_out) {
   dim3 grid((nc + 3 + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
-  k_pair_prep<<<grid, block, 0, s>>>(x, p->w_pair, p->pair_stride, nc, factor, scale_dev, v_out);
+  static const bool il_on = getenv("MS2G_FWD_INTERLEAVE") != nullptr;   // experiment switch
+  const int il = il_on ? batch_group(batch) : 1;
+  k_pair_prep<<<grid, block, 0, s>>>(x, p->w_pair, p->pair_stride, nc, factor, scale_dev, v_out, p->class_mask, il);
   return check_launch("k_pair_prep");
 }
 
@@ -245,7 +259,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
 // order.  Kept separate from the single-image kernel: with the segment loop
 // ptxas needs 72 instead of 56 registers at NB = 8 and the launch is 1.5x
 // slower (C5 batch 8, s=1: 0.73 vs 1.11 ms).
-template <int NB>
+template <int NB, bool IL>
 __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry* __restrict__ rays, int B, int V_r,
                                                                  const int* __restrict__ sel, int n_sel,
                                                                  const float2* __restrict__ pairs, size_t pair_stride,
@@ -283,6 +297,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
   if (wcl < wch) {
     const int L = nc + 3;
     const size_t istride = (size_t)nc * L;
+    // separate layout: image i's pair image at base + i istride; interleaved
+    // (IL): the group's NB pairs of element e at base + e NB
     const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
     const unsigned umax = (unsigned)(nc + 2);
     const long long Es = F0 + (long long)wcl * (long long)S + (long long)S + (1LL << 32);
@@ -295,13 +311,27 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
       const float mf = (float)min(elo, S);
       const unsigned e = offk + min(ehi, umax);
       MS2G_DASSERT(e < (unsigned)(nc * L));
+      if (IL) {
+        const float4* q = reinterpret_cast<const float4*>(base + (size_t)e * NB);
 #pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        float pl, pu;
-        asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
-            : "=f"(pl), "=f"(pu) : "r"(e), "l"(base + i * istride));
-        sa[i] += pl;
-        sb[i] = fmaf(mf, pu - pl, sb[i]);
+        for (int i = 0; i < NB; i += 2) {
+          float4 v;
+          asm("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+              : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q + i / 2));
+          sa[i] += v.x;
+          sb[i] = fmaf(mf, v.y - v.x, sb[i]);
+          sa[i + 1] += v.z;
+          sb[i + 1] = fmaf(mf, v.w - v.z, sb[i + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          float pl, pu;
+          asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
+              : "=f"(pl), "=f"(pu) : "r"(e), "l"(base + i * istride));
+          sa[i] += pl;
+          sb[i] = fmaf(mf, pu - pl, sb[i]);
+        }
       }
       elo = lo1;
       ehi = hi1;
@@ -332,8 +362,18 @@ template <int NB>
 static void fwd_launch_batch(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
                              const int* d_sel, const float* b, float* out) {
   dim3 grid((p->B + 31) / 32, (n_sel + kFwdWarps / 2 - 1) / (kFwdWarps / 2), batch / NB);
-  k_forward_batch<NB><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
-                                                      p->pair_stride, f.nc, b, out);
+  // Interleaved pairs (MS2G_FWD_INTERLEAVE, as the pair prep) measured 2x
+  // SLOWER (C5 batch 8, s=1: 1.53 vs 0.735 ms): a lane's 64 B come in four
+  // 16-B loads whose warp addresses are 64 B apart, so each load spans 16
+  // cache lines -- 4 x 16 L1 wavefronts per column against 8 x 2 for the
+  // separate layout (profiles/r02_fwd_batch_probe.log).  Kept as the switch.
+  static const bool il_on = getenv("MS2G_FWD_INTERLEAVE") != nullptr;
+  if (!il_on)
+    k_forward_batch<NB, false><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
+                                                               p->pair_stride, f.nc, b, out);
+  else
+    k_forward_batch<NB, true><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
+                                                              p->pair_stride, f.nc, b, out);
 }
 
 template <int NB, int SPLIT, int SEG>
@@ -363,7 +403,7 @@ int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch) {
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s, const int* order_sel) {
   if (n_sel <= 0) return MS2G_OK;
-  const int nb = (batch % 8 == 0) ? 8 : (batch % 4 == 0) ? 4 : (batch % 2 == 0) ? 2 : 1;
+  const int nb = batch_group(batch);
   const int slot = timing_begin(p, 0, f.factor, s);
   // Work-unit shape (measured on B200, CUDA events):
   //  * single images: 4 segments per ray; one warp takes all four (SPLIT 1:
@@ -726,18 +766,22 @@ __global__ void __launch_bounds__(256) k_backward_gather(const RayEntry* __restr
 
 // out = scale * sum of the nplanes partial planes (+ out if accumulate), fixed
 // order.  grid.y = batch image (no index division).
-__global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size_t np, float* __restrict__ out,
-                               float scale, int accumulate) {
+__global__ void __launch_bounds__(256) k_chunk_reduce(const float* __restrict__ part, int nplanes, size_t np,
+                                                      float* __restrict__ out, float scale, int accumulate, int G) {
+  __shared__ PlaneSmem sm;
   const size_t b = blockIdx.y;
-  const float* src0 = part + b * nplanes * np;
+  const float* src = part + b * nplanes * np;
   float* ob = out + b * np;
-  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < np; p += (size_t)gridDim.x * blockDim.x) {
-    const float* src = src0 + p;
-    float s = 0.f;
-    for (int c = 0; c < nplanes; ++c) s += src[(size_t)c * np];
-    float v = scale * s;
-    if (accumulate) v += ob[p];
-    ob[p] = v;
+  const int tid = threadIdx.y * 32 + threadIdx.x, tile = plane_tile(G);
+  for (size_t p0 = (size_t)blockIdx.x * tile; p0 < np; p0 += (size_t)gridDim.x * tile) {
+    sum_planes(src, nplanes, np, p0, G, sm);
+    const size_t p = p0 + tid;
+    if (tid < tile && p < np) {
+      float v = scale * sm.tot[tid];
+      if (accumulate) v += ob[p];
+      ob[p] = v;
+    }
+    if (G != 1) __syncthreads();   // tot is rewritten by the next tile
   }
 }
 
@@ -748,21 +792,45 @@ __global__ void k_chunk_reduce(const float* __restrict__ part, int nplanes, size
 // z = y - eta U_s G (as k_up_step) for the s x s fine pixels of each
 // coarse pixel (y == NULL: z = U_s G); grid = coarse pixels (x: columns,
 // y: rows, z: batch).
-__global__ void k_reduce_up_step(const float* __restrict__ part, int nplanes, int nc, float c,
-                                 const float* __restrict__ y, const float* __restrict__ eta_dev, float* __restrict__ z,
-                                 int s) {
-  const int J = blockIdx.x * 32 + threadIdx.x, I = blockIdx.y * 8 + threadIdx.y;
-  if (I >= nc || J >= nc) return;
-  const size_t b = blockIdx.z, np = (size_t)nc * nc;
-  const float* src = part + b * nplanes * np + (size_t)I * nc + J;
-  float acc = 0.f;
-  for (int q = 0; q < nplanes; ++q) acc += src[(size_t)q * np];
-  const float G = c * acc;
+__global__ void __launch_bounds__(256) k_reduce_up_step(const float* __restrict__ part, int nplanes, int nc, float c,
+                                                        const float* __restrict__ y,
+                                                        const float* __restrict__ eta_dev, float* __restrict__ z,
+                                                        int s, int G) {
+  __shared__ PlaneSmem sm;
+  const size_t b = blockIdx.y, np = (size_t)nc * nc;
+  const float* src = part + b * nplanes * np;
   const float e = eta_dev ? *eta_dev : 0.f;
-  const int n = nc * s;
-  for (int a = 0; a < s; ++a) {
-    const size_t row = (b * n + (size_t)(s * I + a)) * n + (size_t)s * J;
-    for (int q = 0; q < s; ++q) z[row + q] = y ? fmaf(-e, G, y[row + q]) : G;   // one rounding, as k_up_step
+  const int n = nc * s, tid = threadIdx.y * 32 + threadIdx.x, tile = plane_tile(G);
+  for (size_t p0 = (size_t)blockIdx.x * tile; p0 < np; p0 += (size_t)gridDim.x * tile) {
+    if (G == 1) {
+      // one thread per coarse pixel: its planes in order (the G = 1 rule of
+      // sum_planes, without the shared-memory hop), then its s x s fine pixels
+      const size_t p = p0 + tid;
+      if (p >= np) continue;
+      float acc = 0.f;
+      for (int q = 0; q < nplanes; ++q) acc += src[(size_t)q * np + p];
+      const float G_ = c * acc;
+      const unsigned I = (unsigned)(p / (unsigned)nc), J = (unsigned)(p - (size_t)I * nc);
+      for (int a = 0; a < s; ++a) {
+        const size_t row = (b * n + (size_t)(s * I + a)) * n + (size_t)s * J;
+        for (int u = 0; u < s; ++u) z[row + u] = y ? fmaf(-e, G_, y[row + u]) : G_;   // one rounding, as k_up_step
+      }
+      continue;
+    }
+    sum_planes(src, nplanes, np, p0, G, sm);
+    // the s x s fine pixels of the tile's 32 coarse pixels, spread over all
+    // 256 threads: consecutive threads write consecutive fine columns of a row
+    const unsigned I0 = (unsigned)(p0 / (unsigned)nc), J0 = (unsigned)(p0 - (size_t)I0 * nc);
+    for (int q = tid; q < tile * s * s; q += 256) {
+      const int a = q / (tile * s), r = q - a * tile * s, x = r / s, u = r - x * s;
+      if (p0 + x >= np) continue;
+      unsigned I = I0, J = J0 + x;              // coarse pixel p0 + x (the tile may wrap a row)
+      while (J >= (unsigned)nc) { J -= nc; ++I; }
+      const size_t idx = (b * n + (size_t)(s * I + a)) * n + (size_t)(s * J + u);
+      const float G_ = c * sm.tot[x];
+      z[idx] = y ? fmaf(-e, G_, y[idx]) : G_;   // one rounding, as k_up_step
+    }
+    __syncthreads();   // tot is rewritten by the next tile
   }
 }
 
@@ -775,30 +843,35 @@ __global__ void __launch_bounds__(256) k_reduce_power(const float* __restrict__ 
                                                       float* __restrict__ w_out, const float* __restrict__ v,
                                                       double* __restrict__ red, unsigned* __restrict__ ticket,
                                                       double* __restrict__ pw, double* L_out, double* eta_out,
-                                                      float* etaf_out) {
+                                                      float* etaf_out, int G) {
   __shared__ double sd[256], sn[256];
+  __shared__ PlaneSmem sm;
   __shared__ bool last;
+  const int tid = threadIdx.y * 32 + threadIdx.x, tile = plane_tile(G);
   double d = 0.0, q = 0.0;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
-    const float* src = part + i;
-    float w = 0.f;
-    for (int c = 0; c < nplanes; ++c) w += src[(size_t)c * np];
-    w_out[i] = w;
-    const double wd = w;
-    d += (double)v[i] * wd;
-    q += wd * wd;
+  for (size_t p0 = (size_t)blockIdx.x * tile; p0 < np; p0 += (size_t)gridDim.x * tile) {
+    sum_planes(part, nplanes, np, p0, G, sm);
+    const size_t i = p0 + tid;
+    if (tid < tile && i < np) {
+      const float w = sm.tot[tid];
+      w_out[i] = w;
+      const double wd = w;
+      d += (double)v[i] * wd;
+      q += wd * wd;
+    }
+    if (G != 1) __syncthreads();   // tot is rewritten by the next tile
   }
-  sd[threadIdx.x] = d;
-  sn[threadIdx.x] = q;
+  sd[tid] = d;
+  sn[tid] = q;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      sd[threadIdx.x] += sd[threadIdx.x + o];
-      sn[threadIdx.x] += sn[threadIdx.x + o];
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) {
+      sd[tid] += sd[tid + o];
+      sn[tid] += sn[tid + o];
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     red[2 * blockIdx.x] = sd[0];
     red[2 * blockIdx.x + 1] = sn[0];
     __threadfence();
@@ -809,21 +882,21 @@ __global__ void __launch_bounds__(256) k_reduce_power(const float* __restrict__ 
   __threadfence();
   d = 0.0;
   q = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+  for (int b = tid; b < (int)gridDim.x; b += 256) {
     d += __ldcg(red + 2 * b);
     q += __ldcg(red + 2 * b + 1);
   }
-  sd[threadIdx.x] = d;
-  sn[threadIdx.x] = q;
+  sd[tid] = d;
+  sn[tid] = q;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      sd[threadIdx.x] += sd[threadIdx.x + o];
-      sn[threadIdx.x] += sn[threadIdx.x + o];
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) {
+      sd[tid] += sd[tid + o];
+      sn[tid] += sn[tid + o];
     }
     __syncthreads();
   }
-  if (threadIdx.x != 0) return;
+  if (tid != 0) return;
   d = sd[0];
   q = sn[0];
   pw[0] = d;
@@ -836,8 +909,10 @@ __global__ void __launch_bounds__(256) k_reduce_power(const float* __restrict__ 
 
 int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, float c, const float* y,
                           const float* eta_dev, float* z, int s, cudaStream_t st) {
-  dim3 grid((nc + 31) / 32, (nc + 7) / 8, batch);
-  k_reduce_up_step<<<grid, dim3(32, 8), 0, st>>>(part, nplanes, nc, c, y, eta_dev, z, s);
+  const size_t np = (size_t)nc * nc;
+  const int G = plane_groups(np, nplanes);
+  dim3 grid(plane_blocks(np, G, 4096), batch);
+  k_reduce_up_step<<<grid, dim3(32, kPlaneGroups), 0, st>>>(part, nplanes, nc, c, y, eta_dev, z, s, G);
   return check_launch("k_reduce_up_step");
 }
 
@@ -846,8 +921,10 @@ int launch_reduce_power(ms2g_plan* p, const float* part, int nplanes, size_t np,
                         float* etaf_out, cudaStream_t st) {
   // one pass over nplanes x np floats: as many blocks as the buffer allows
   // (the fixed-order last-block reduction handles any grid size)
-  const int blocks = (int)std::min<size_t>((size_t)red_blocks, std::max<size_t>(1, (np + 255) / 256));
-  k_reduce_power<<<blocks, 256, 0, st>>>(part, nplanes, np, w_out, v, red, ticket, pw, L_out, eta_out, etaf_out);
+  const int G = plane_groups(np, nplanes);
+  const int blocks = plane_blocks(np, G, red_blocks);
+  k_reduce_power<<<blocks, dim3(32, kPlaneGroups), 0, st>>>(part, nplanes, np, w_out, v, red, ticket, pw, L_out,
+                                                            eta_out, etaf_out, G);
   return check_launch("k_reduce_power");
 }
 
@@ -909,8 +986,9 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
     if (publish == 2) return MS2G_OK;
     if (publish == 3) return launch_mc_publish(p, p->w_part, nch, np, total, scale, s);
     if (publish) return launch_chunk_reduce_publish(p, p->w_part, nch, np, total, scale, s);
-    const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);
-    k_chunk_reduce<<<dim3(blocks, batch), 256, 0, s>>>(p->w_part, nch, np, img, scale, accumulate);
+    const int G = plane_groups(np, nch);
+    k_chunk_reduce<<<dim3(plane_blocks(np, G, 4096), batch), dim3(32, kPlaneGroups), 0, s>>>(p->w_part, nch, np, img,
+                                                                                             scale, accumulate, G);
     return check_launch("k_chunk_reduce");
   }
   const int H = bp_height(f.nc);
@@ -933,8 +1011,9 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   if (publish == 3) return launch_mc_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);   // NVLS
   if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)
     return launch_chunk_reduce_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);
-  const int blocks = (int)((np + 255) / 256 < 4096 ? (np + 255) / 256 : 4096);
-  k_chunk_reduce<<<dim3(blocks, batch), 256, 0, s>>>(p->w_part, ch[0] + ch[1], np, img, scale, accumulate);
+  const int G = plane_groups(np, ch[0] + ch[1]);
+  k_chunk_reduce<<<dim3(plane_blocks(np, G, 4096), batch), dim3(32, kPlaneGroups), 0, s>>>(
+      p->w_part, ch[0] + ch[1], np, img, scale, accumulate, G);
   return check_launch("k_chunk_reduce");
 }
 

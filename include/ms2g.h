@@ -261,8 +261,10 @@ int ms2g_schedule_views(const ms2g_plan* plan, const ms2g_solve_desc* desc, int3
  *   x = (1-alpha) z + alpha D(z); y = x + a_i (x - x_prev).
  * x0 = y0, b [batch][V_r][B], x_out [batch][n][n] (may alias x0).
  * trace (optional, host) receives the schedule with eta filled in.
- * Synchronous on return (the divergence flag is read back): a non-finite
- * iterate returns MS2G_ERR_DIVERGED naming the stage and iteration. */
+ * Synchronous on return (the flags are read back): a NaN / Inf in b or x0
+ * (checked on the device at the solve's start) returns MS2G_ERR_INPUT; a
+ * non-finite iterate returns MS2G_ERR_DIVERGED naming the stage and
+ * iteration. */
 int ms2g_pnp_ms2g_solve(ms2g_plan* plan, const ms2g_solve_desc* desc, const float* b, const float* x0,
                         float* x_out, ms2g_sched_entry* trace, void* stream);
 
@@ -270,7 +272,8 @@ int ms2g_pnp_ms2g_solve(ms2g_plan* plan, const ms2g_solve_desc* desc, const floa
  * divergence flag is left on the device (read it with ms2g_solve_status). */
 int ms2g_pnp_ms2g_solve_async(ms2g_plan* plan, const ms2g_solve_desc* desc, const float* b,
                               const float* x0, float* x_out, void* stream);
-/* Synchronous: returns MS2G_OK or MS2G_ERR_DIVERGED for the last solve. */
+/* Synchronous: MS2G_OK, MS2G_ERR_INPUT (non-finite b / x0) or
+ * MS2G_ERR_DIVERGED for the last solve. */
 int ms2g_solve_status(ms2g_plan* plan, void* stream);
 
 /* Per-kernel timing inside the solve graph (measurement support).

@@ -655,7 +655,30 @@ int launch_cached_step(const double* cache, double* L_out, double* eta_out, floa
   return check_launch("k_cached_step");
 }
 
-__global__ void k_init_flag(int* flag) { *flag = INT_MAX; }
+// flag[0]: first non-finite global iteration (INT_MAX = none); flag[1]: a
+// non-finite INPUT (b or x0) was seen by k_check_finite
+__global__ void k_init_flag(int* flag) {
+  flag[0] = INT_MAX;
+  flag[1] = 0;
+}
+
+// Non-finite input check at the start of a solve (SURVEY §8(b):
+// "non-finite input ... -> MS2G_ERR_INPUT"): any NaN / Inf in b or x0 raises
+// flag[1].  One streaming pass over the inputs (C4: 13 MB).
+__global__ void k_check_finite(const float* __restrict__ a, size_t na, const float* __restrict__ c, size_t nc_,
+                               int* flag) {
+  bool bad = false;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < na + nc_; i += (size_t)gridDim.x * blockDim.x) {
+    const float v = i < na ? a[i] : c[i - na];
+    bad |= !isfinite(v);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag + 1, 1);
+}
+
+int launch_check_finite(const float* a, size_t na, const float* c, size_t nc_, int* flag, cudaStream_t st) {
+  k_check_finite<<<grid1d(na + nc_, 256, 148 * 8), 256, 0, st>>>(a, na, c, nc_, flag);
+  return check_launch("k_check_finite");
+}
 
 int launch_init_flag(int* flag, cudaStream_t st) {
   k_init_flag<<<1, 1, 0, st>>>(flag);

@@ -25,6 +25,8 @@ struct NvtxRange {
 
 namespace ms2g {
 
+int launch_check_finite(const float* a, size_t na, const float* c, size_t nc_, int* flag, cudaStream_t st);
+
 std::atomic<uint64_t> g_launches{0};
 thread_local bool t_capturing = false;
 thread_local uint64_t t_captured = 0;
@@ -816,6 +818,7 @@ static int enqueue_solve(ms2g_plan* p, const ms2g_solve_desc* sd, const std::vec
   const int n = p->d.n, batch = p->d.batch;
   const size_t img = (size_t)n * n * batch;
   MS2G_TRY(launch_init_flag(p->w_flag, st));
+  MS2G_TRY(launch_check_finite(b, (size_t)p->V_r * p->B * batch, x0, img, p->w_flag, st));
   // x_0 = y_0 = x0, x_prev = x_0
   MS2G_CUDA(cudaMemcpyAsync(p->w_x[0], x0, sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
   MS2G_CUDA(cudaMemcpyAsync(p->w_y, x0, sizeof(float) * img, cudaMemcpyDeviceToDevice, st));
@@ -1008,12 +1011,14 @@ static int solve_launch(ms2g_plan* p, const ms2g_solve_desc* sd, const float* b,
 }
 
 static int solve_status(ms2g_plan* p, cudaStream_t st) {
-  int flag = INT_MAX, perr = 0, tverr = 0;
-  MS2G_CUDA(cudaMemcpyAsync(&flag, p->w_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int flags[2] = {INT_MAX, 0}, perr = 0, tverr = 0;
+  MS2G_CUDA(cudaMemcpyAsync(flags, p->w_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  const int flag = flags[0];
   if (p->tvws.err) MS2G_CUDA(cudaMemcpyAsync(&tverr, p->tvws.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (p->w_peer_err) MS2G_CUDA(cudaMemcpyAsync(&perr, p->w_peer_err, sizeof(int), cudaMemcpyDeviceToHost, st));
   MS2G_CUDA(cudaStreamSynchronize(st));
   if (tverr) return set_error(MS2G_ERR_CUDA, "persistent TV-prox kernel: a neighbour wait timed out");
+  if (flags[1]) return set_error(MS2G_ERR_INPUT, "non-finite value (NaN or Inf) in b or x0 (S:258)");
   if (perr) {
     p->peer_failed = true;     // epochs are out of step: refuse exchanges until every rank re-attaches
     return set_error(MS2G_ERR_NCCL, "peer allreduce: barrier timed out (a rank never arrived); "
@@ -1143,12 +1148,13 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     if (e == cudaSuccess) e = cudaMalloc(&w.err, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(w.err, 0, sizeof(int));
   }
-  if (e == cudaSuccess) e = cudaMalloc(&p->w_flag, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_flag, 2 * sizeof(int));   // {diverged iteration, input flag}
   if (e == cudaSuccess) e = cudaMalloc(&p->w_sel, sizeof(int) * p->V_r * ms2g_plan::kSelRing);
   if (e == cudaSuccess) e = cudaMallocHost(&p->h_sel, sizeof(int) * p->V_r * ms2g_plan::kSelRing);
   for (int k = 0; k < ms2g_plan::kSelRing && e == cudaSuccess; ++k)
     e = cudaEventCreateWithFlags(&p->sel_ev[k], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMemset(p->w_flag, 0x7f, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(p->w_flag + 1, 0, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(p->w_scal, 0, sizeof(double) * 128);
   if (e != cudaSuccess) {
     free_plan(p);
@@ -1398,6 +1404,7 @@ static int grad_graph(ms2g_plan* p, const FactorTables* f, int kind, const float
                       const Sel& s, int sel_id, cudaStream_t st) {
   static const bool off = getenv("MS2G_GRAD_GRAPHS") && atoi(getenv("MS2G_GRAD_GRAPHS")) == 0;   // experiment switch
   if (off || p->timing || t_capturing) return do_grad(p, f, kind, x, b, g, s, st);
+  if (p->peer_n > 0 || p->mc_n > 0) MS2G_TRY(peer_ok(p));   // a cached graph would replay a failed exchange
   std::ostringstream os;
   os << f->factor << ':' << kind << ':' << sel_id << ':' << (const void*)x << ':' << (const void*)b << ':'
      << (const void*)g << ':' << p->topo_version;

@@ -792,6 +792,28 @@ __global__ void __launch_bounds__(256) k_chunk_reduce(const float* __restrict__ 
 // z = y - eta U_s G (as k_up_step) for the s x s fine pixels of each
 // coarse pixel (y == NULL: z = U_s G); grid = coarse pixels (x: columns,
 // y: rows, z: batch).
+// The G = 1 rule of sum_planes (one thread per coarse pixel adding its planes
+// in order) on a (columns, rows, batch) grid of (32 x 8) blocks: no index
+// division, each thread writes its s x s fine pixels.
+__global__ void __launch_bounds__(256) k_reduce_up_step_px(const float* __restrict__ part, int nplanes, int nc,
+                                                           float c, const float* __restrict__ y,
+                                                           const float* __restrict__ eta_dev, float* __restrict__ z,
+                                                           int s) {
+  const int J = blockIdx.x * 32 + threadIdx.x, I = blockIdx.y * 8 + threadIdx.y;
+  if (I >= nc || J >= nc) return;
+  const size_t b = blockIdx.z, np = (size_t)nc * nc;
+  const float* src = part + b * nplanes * np + (size_t)I * nc + J;
+  float acc = 0.f;
+  for (int q = 0; q < nplanes; ++q) acc += src[(size_t)q * np];
+  const float G = c * acc;
+  const float e = eta_dev ? *eta_dev : 0.f;
+  const int n = nc * s;
+  for (int a = 0; a < s; ++a) {
+    const size_t row = (b * n + (size_t)(s * I + a)) * n + (size_t)s * J;
+    for (int q = 0; q < s; ++q) z[row + q] = y ? fmaf(-e, G, y[row + q]) : G;   // one rounding, as k_up_step
+  }
+}
+
 __global__ void __launch_bounds__(256) k_reduce_up_step(const float* __restrict__ part, int nplanes, int nc, float c,
                                                         const float* __restrict__ y,
                                                         const float* __restrict__ eta_dev, float* __restrict__ z,
@@ -802,21 +824,6 @@ __global__ void __launch_bounds__(256) k_reduce_up_step(const float* __restrict_
   const float e = eta_dev ? *eta_dev : 0.f;
   const int n = nc * s, tid = threadIdx.y * 32 + threadIdx.x, tile = plane_tile(G);
   for (size_t p0 = (size_t)blockIdx.x * tile; p0 < np; p0 += (size_t)gridDim.x * tile) {
-    if (G == 1) {
-      // one thread per coarse pixel: its planes in order (the G = 1 rule of
-      // sum_planes, without the shared-memory hop), then its s x s fine pixels
-      const size_t p = p0 + tid;
-      if (p >= np) continue;
-      float acc = 0.f;
-      for (int q = 0; q < nplanes; ++q) acc += src[(size_t)q * np + p];
-      const float G_ = c * acc;
-      const unsigned I = (unsigned)(p / (unsigned)nc), J = (unsigned)(p - (size_t)I * nc);
-      for (int a = 0; a < s; ++a) {
-        const size_t row = (b * n + (size_t)(s * I + a)) * n + (size_t)s * J;
-        for (int u = 0; u < s; ++u) z[row + u] = y ? fmaf(-e, G_, y[row + u]) : G_;   // one rounding, as k_up_step
-      }
-      continue;
-    }
     sum_planes(src, nplanes, np, p0, G, sm);
     // the s x s fine pixels of the tile's 32 coarse pixels, spread over all
     // 256 threads: consecutive threads write consecutive fine columns of a row
@@ -911,6 +918,11 @@ int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, flo
                           const float* eta_dev, float* z, int s, cudaStream_t st) {
   const size_t np = (size_t)nc * nc;
   const int G = plane_groups(np, nplanes);
+  if (G == 1) {
+    dim3 grid((nc + 31) / 32, (nc + 7) / 8, batch);
+    k_reduce_up_step_px<<<grid, dim3(32, 8), 0, st>>>(part, nplanes, nc, c, y, eta_dev, z, s);
+    return check_launch("k_reduce_up_step_px");
+  }
   dim3 grid(plane_blocks(np, G, 4096), batch);
   k_reduce_up_step<<<grid, dim3(32, kPlaneGroups), 0, st>>>(part, nplanes, nc, c, y, eta_dev, z, s, G);
   return check_launch("k_reduce_up_step");

@@ -324,11 +324,24 @@ def test_full_size_sampled_c4(P):
 
 
 def test_divergence_reported(P):
+    """S:258 / SURVEY §8(b): a NaN planted in b is an INPUT error (code 7,
+    checked on the device at the solve's start); iterates that overflow are
+    a divergence (code 3) naming the stage and iteration."""
     n, V, B = 64, 30, 96
     b = np.ones((V, B), np.float32); b[3, 7] = np.nan
     with P.plan_geometry(n, V, B, factors=(2, 1)) as plan:
-        with pytest.raises(P.DivergedError, match="iteration 1"):
+        with pytest.raises(P.MS2GError, match="non-finite") as e:
             P.pnp_ms2g_solve(plan, [(2, 2, 0), (1, 1, 0)], dev(b)[None])
+        assert e.value.code == 7
+        x0 = torch.zeros((1, n, n), device="cuda"); x0[0, 5, 5] = float("inf")
+        with pytest.raises(P.MS2GError) as e:
+            P.pnp_ms2g_solve(plan, [(1, 1, 0)], dev(np.ones((V, B), np.float32))[None], x0=x0)
+        assert e.value.code == 7
+        big = np.full((V, B), 3e38, np.float32)    # finite data whose gradient overflows fp32
+        with pytest.raises(P.DivergedError, match="non-finite iterate at stage"):
+            P.pnp_ms2g_solve(plan, [(2, 2, 0), (1, 1, 0)], dev(big)[None])
+        ok = P.pnp_ms2g_solve(plan, [(2, 2, 0), (1, 1, 0)], dev(np.ones((V, B), np.float32))[None])
+        assert torch.isfinite(ok).all()          # the flags are reset for the next solve
 
 
 def test_config_errors(P):

@@ -255,6 +255,16 @@ __device__ __forceinline__ float tv_div(const float* __restrict__ px, const floa
 // a (8+1) x (32+1) shared tile (instead of three times per pixel), then
 // q = grad w and the p update.  first != 0: p^0 = 0 (no warm start, pin not
 // read), so w = -f / lambda.
+// Programmatic dependent launch (PDL) of the TV chain: each kernel of the
+// K + 1 is launched with programmatic stream serialisation, so it is
+// scheduled while its predecessor drains; it reads what does not depend on
+// the predecessor (f = z, written before the chain) first, then waits
+// (griddepcontrol.wait: the predecessor has completed and its writes are
+// visible), then lets its own successor launch.  Both instructions are
+// no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __global__ void __launch_bounds__(256) k_tv_iter(const float* __restrict__ f, const float* __restrict__ pin,
                                                  float* __restrict__ pout, int n, float inv_lambda, float tau,
                                                  int first) {
@@ -265,12 +275,30 @@ __global__ void __launch_bounds__(256) k_tv_iter(const float* __restrict__ f, co
   const float* fb = f + b * np;
   const float* px = pin + b * 2 * np;
   const float* py = px + np;
-  for (int e = ty * 32 + tx; e < 9 * 33; e += 256) {
+  // the <= 2 tile entries of this thread: f first (unless this is the first
+  // iteration, whose predecessor produced f)
+  float fe[2] = {0.f, 0.f};
+  if (!first) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int e = ty * 32 + tx + 256 * k;
+      if (e >= 9 * 33) break;
+      const int gi = i0 + e / 33, gj = j0 + e % 33;
+      if (gi < n && gj < n) fe[k] = fb[(size_t)gi * n + gj];
+    }
+  }
+  pdl_wait();
+  pdl_release();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int e = ty * 32 + tx + 256 * k;
+    if (e >= 9 * 33) break;
     const int li = e / 33, lj = e % 33, gi = i0 + li, gj = j0 + lj;
     float w = 0.f;
     if (gi < n && gj < n) {
       const size_t q = (size_t)gi * n + gj;
-      w = (first ? 0.f : tv_div(px, py, n, gi, gj)) - fb[q] * inv_lambda;
+      const float fq = first ? fb[q] : fe[k];
+      w = (first ? 0.f : tv_div(px, py, n, gi, gj)) - fq * inv_lambda;
     }
     sw[li][lj] = w;
   }
@@ -290,14 +318,18 @@ __global__ void __launch_bounds__(256) k_tv_iter(const float* __restrict__ f, co
   ox[p] = ((first ? 0.f : px[p]) + tau * qx) * rden;
   ox[np + p] = ((first ? 0.f : py[p]) + tau * qy) * rden;
 }
-
 __global__ void k_tv_final(const float* __restrict__ f, const float* __restrict__ pin,
                            const float* __restrict__ xprev, float* __restrict__ xout, float* __restrict__ yout,
                            int n, float lambda, float alpha, float a, int mode, int* flag, int iter) {
-  PIXEL_IJB(n, n);
+  const int j = blockIdx.x * 32 + threadIdx.x, i = blockIdx.y * 8 + threadIdx.y;
+  const size_t b = blockIdx.z;
+  const bool in = i < n && j < n;
   const size_t np = (size_t)n * n, idx = b * np + (size_t)i * n + j;
   const float* px = pin + b * 2 * np;
-  const float fv = f[idx];
+  const float fv = in ? f[idx] : 0.f;     // f precedes the TV chain (PDL: read before the wait)
+  pdl_wait();
+  pdl_release();
+  if (!in) return;
   const float u = fv - lambda * tv_div(px, px + np, n, i, j);
   mix_momentum(idx, fv, u, xprev, xout, yout, alpha, a, mode, flag, iter);
 }
@@ -610,6 +642,23 @@ int launch_tv_persist(const TvWs& ws, int n, int batch, float lambda, float tau,
   return MS2G_OK;
 }
 
+// launch with programmatic stream serialisation (PDL; MS2G_PDL=0 disables it)
+template <typename... KArgs, typename... Args>
+static int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  static const bool off = getenv("MS2G_PDL") && atoi(getenv("MS2G_PDL")) == 0;   // experiment switch
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  MS2G_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+  return MS2G_OK;
+}
+
 int launch_tv(int n, int batch, float lambda, float tau, int iters, const float* f, float* p0, float* p1,
               const float* xprev, float* xout, float* yout, float alpha, float a, int mode, int* flag, int iter,
               cudaStream_t st, const TvWs* ws) {
@@ -628,14 +677,15 @@ int launch_tv(int n, int batch, float lambda, float tau, int iters, const float*
   float* pin = p0;
   float* pout = p1;
   for (int k = 0; k < iters; ++k) {
-    k_tv_iter<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(f, pin, pout, n, 1.f / lambda, tau, k == 0);
+    MS2G_TRY(launch_pdl(k_tv_iter, px_grid(n, n, batch), kPxBlock, st, f, (const float*)pin, pout, n, 1.f / lambda,
+                        tau, (int)(k == 0)));
     MS2G_TRY(check_launch("k_tv_iter"));
     float* tmp = pin;
     pin = pout;
     pout = tmp;
   }
-  k_tv_final<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(f, pin, xprev, xout, yout, n, lambda, alpha, a, mode, flag,
-                                                        iter);
+  MS2G_TRY(launch_pdl(k_tv_final, px_grid(n, n, batch), kPxBlock, st, f, (const float*)pin, xprev, xout, yout, n,
+                      lambda, alpha, a, mode, flag, iter));
   return check_launch("k_tv_final");
 }
 

@@ -196,6 +196,8 @@ __device__ __forceinline__ void mix_momentum(size_t idx, float zv, float dv, con
 __global__ void k_gauss_mm(const float* __restrict__ z, const float* __restrict__ xprev, float* __restrict__ xout,
                            float* __restrict__ yout, int n, float w0, float w1, float alpha, float a, int mode,
                            int* flag, int iter) {
+  pdl_wait();
+  pdl_release();
   PIXEL_IJB(n, n);
   const size_t np = (size_t)n * n;
   const float* zb = z + b * np;
@@ -216,8 +218,8 @@ int launch_gauss_mix_mom(int n, int batch, float sigma, const float* z, const fl
                          float* yout, float alpha, float a, int mode, int* flag, int iter, cudaStream_t st) {
   const double e = exp(-1.0 / (2.0 * (double)sigma * (double)sigma));
   const float w1 = (float)(e / (1.0 + 2.0 * e)), w0 = (float)(1.0 / (1.0 + 2.0 * e));
-  k_gauss_mm<<<px_grid(n, n, batch), kPxBlock, 0, st>>>(z, xprev, xout, yout, n, w0, w1, alpha, a, mode, flag,
-                                                        iter);
+  MS2G_CUDA(launch_k(k_gauss_mm, px_grid(n, n, batch), kPxBlock, 0, st, z, xprev, xout, yout, n, w0, w1, alpha, a,
+                     mode, flag, iter));
   return check_launch("k_gauss_mm");
 }
 
@@ -255,15 +257,13 @@ __device__ __forceinline__ float tv_div(const float* __restrict__ px, const floa
 // a (8+1) x (32+1) shared tile (instead of three times per pixel), then
 // q = grad w and the p update.  first != 0: p^0 = 0 (no warm start, pin not
 // read), so w = -f / lambda.
-// Programmatic dependent launch (PDL) of the TV chain: each kernel of the
-// K + 1 is launched with programmatic stream serialisation, so it is
-// scheduled while its predecessor drains; it reads what does not depend on
-// the predecessor (f = z, written before the chain) first, then waits
-// (griddepcontrol.wait: the predecessor has completed and its writes are
-// visible), then lets its own successor launch.  Both instructions are
-// no-ops for an ordinary launch.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// The TV chain is launched with programmatic dependent launch (launch_k,
+// internal.cuh): each of the K + 1 kernels reads what does not depend on its
+// predecessor (f = z, written before the chain) before griddepcontrol.wait.
+bool pdl_enabled() {
+  static const bool on = !(getenv("MS2G_PDL") && atoi(getenv("MS2G_PDL")) == 0);   // experiment switch
+  return on;
+}
 
 __global__ void __launch_bounds__(256) k_tv_iter(const float* __restrict__ f, const float* __restrict__ pin,
                                                  float* __restrict__ pout, int n, float inv_lambda, float tau,
@@ -642,23 +642,6 @@ int launch_tv_persist(const TvWs& ws, int n, int batch, float lambda, float tau,
   return MS2G_OK;
 }
 
-// launch with programmatic stream serialisation (PDL; MS2G_PDL=0 disables it)
-template <typename... KArgs, typename... Args>
-static int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
-  static const bool off = getenv("MS2G_PDL") && atoi(getenv("MS2G_PDL")) == 0;   // experiment switch
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = off ? 0 : 1;
-  MS2G_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
-  return MS2G_OK;
-}
-
 int launch_tv(int n, int batch, float lambda, float tau, int iters, const float* f, float* p0, float* p1,
               const float* xprev, float* xout, float* yout, float alpha, float a, int mode, int* flag, int iter,
               cudaStream_t st, const TvWs* ws) {
@@ -677,15 +660,15 @@ int launch_tv(int n, int batch, float lambda, float tau, int iters, const float*
   float* pin = p0;
   float* pout = p1;
   for (int k = 0; k < iters; ++k) {
-    MS2G_TRY(launch_pdl(k_tv_iter, px_grid(n, n, batch), kPxBlock, st, f, (const float*)pin, pout, n, 1.f / lambda,
-                        tau, (int)(k == 0)));
+    MS2G_CUDA(launch_k_pdl(k_tv_iter, px_grid(n, n, batch), kPxBlock, 0, st, f, (const float*)pin, pout, n, 1.f / lambda,
+                       tau, (int)(k == 0)));
     MS2G_TRY(check_launch("k_tv_iter"));
     float* tmp = pin;
     pin = pout;
     pout = tmp;
   }
-  MS2G_TRY(launch_pdl(k_tv_final, px_grid(n, n, batch), kPxBlock, st, f, (const float*)pin, xprev, xout, yout, n,
-                      lambda, alpha, a, mode, flag, iter));
+  MS2G_CUDA(launch_k_pdl(k_tv_final, px_grid(n, n, batch), kPxBlock, 0, st, f, (const float*)pin, xprev, xout, yout, n,
+                     lambda, alpha, a, mode, flag, iter));
   return check_launch("k_tv_final");
 }
 

@@ -227,6 +227,47 @@ struct ms2g_plan {
 
 namespace ms2g {
 
+// ---- programmatic dependent launch (PDL) ----
+// launch_k_pdl launches with programmatic stream serialisation: the kernel is
+// scheduled while its predecessor drains, reads only what does not depend on
+// the predecessor before griddepcontrol.wait (pdl_wait: the predecessor has
+// completed and its writes are visible), then lets its own successor launch
+// (pdl_release, after the wait, so visibility stays transitive).  Used for
+// the TV chain (K + 1 short dependent launches per denoise).  The other hot
+// kernels also wait / release (no-ops for an ordinary launch) but are
+// launched ordinarily with launch_k: launched with PDL, their resident
+// waiting CTAs took occupancy from the predecessor's last wave (C3 cached-
+// step solve 5.48 -> 6.85 ms, C4 355 -> 350 iterations/s).  MS2G_PDL=0
+// disables PDL everywhere.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_cfg(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+  return launch_cfg(false, kern, grid, block, smem, st, args...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                Args... args) {
+  return launch_cfg(true, kern, grid, block, smem, st, args...);
+}
+
 // ---- the fixed-order sum of the backprojection's partial planes ----
 // Every consumer of the partial planes (k_chunk_reduce, the fused step and
 // power epilogues, the NEXT-3 publishes) sums them with THIS rule, so all

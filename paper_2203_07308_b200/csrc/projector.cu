@@ -73,6 +73,8 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
                             int s, const double* __restrict__ scale_dev, float* __restrict__ v_out, int class_mask,
                             int il) {
   __shared__ float T[33][33];
+  pdl_wait();
+  pdl_release();
   const int bz = blockIdx.z;
   const int nsrc = nc * s;
   const float* xb = x + (size_t)bz * nsrc * nsrc;
@@ -120,7 +122,8 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
   dim3 grid((nc + 3 + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
   static const bool il_on = getenv("MS2G_FWD_INTERLEAVE") != nullptr;   // experiment switch
   const int il = il_on ? batch_group(batch) : 1;
-  k_pair_prep<<<grid, block, 0, s>>>(x, p->w_pair, p->pair_stride, nc, factor, scale_dev, v_out, p->class_mask, il);
+  MS2G_CUDA(launch_k(k_pair_prep, grid, block, 0, s, x, p->w_pair, p->pair_stride, nc, factor, scale_dev, v_out,
+                     p->class_mask, il));
   return check_launch("k_pair_prep");
 }
 
@@ -193,6 +196,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
     F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; cls = R.flags & 3;
     if (R.c_lo < R.c_hi) { cl = R.c_lo; ch = R.c_hi; }
   }
+  pdl_wait();      // the ray table is static; the pair images and b come from the predecessors
+  pdl_release();
   const int wcl = __reduce_min_sync(0xffffffffu, cl);
   const int wch = __reduce_max_sync(0xffffffffu, ch);
   const int len = wch > wcl ? wch - wcl : 0;
@@ -283,6 +288,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
     F0 = R.F0; S = R.S; Lc = R.Lc; Ly32 = R.Ly32; cls = R.flags & 3;
     if (R.c_lo < R.c_hi) { cl = R.c_lo; ch = R.c_hi; }
   }
+  pdl_wait();      // the ray table is static; the pair images and b come from the predecessors
+  pdl_release();
   int wcl = __reduce_min_sync(0xffffffffu, cl);
   int wch = __reduce_max_sync(0xffffffffu, ch);
   if (wcl < wch) {
@@ -369,11 +376,11 @@ static void fwd_launch_batch(int n_sel, int batch, cudaStream_t s, ms2g_plan* p,
   // separate layout (profiles/r02_fwd_batch_probe.log).  Kept as the switch.
   static const bool il_on = getenv("MS2G_FWD_INTERLEAVE") != nullptr;
   if (!il_on)
-    k_forward_batch<NB, false><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
-                                                               p->pair_stride, f.nc, b, out);
+    (void)launch_k(k_forward_batch<NB, false>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
+                   (const float2*)p->w_pair, p->pair_stride, f.nc, b, out);
   else
-    k_forward_batch<NB, true><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
-                                                              p->pair_stride, f.nc, b, out);
+    (void)launch_k(k_forward_batch<NB, true>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
+                   (const float2*)p->w_pair, p->pair_stride, f.nc, b, out);
 }
 
 template <int NB, int SPLIT, int SEG>
@@ -387,8 +394,8 @@ static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, cons
   const int* order = no_order ? nullptr
                               : (d_sel ? order_sel
                                        : ((n_sel == p->V_r && f.fwd_order_vpb == VPB) ? f.d_fwd_order : nullptr));
-  k_forward<NB, SPLIT, SEG><<<grid, 32 * kFwdWarps, 0, s>>>(f.d_rays, p->B, p->V_r, d_sel, n_sel, p->w_pair,
-                                                            p->pair_stride, f.nc, b, out, order);
+  (void)launch_k(k_forward<NB, SPLIT, SEG>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
+                 (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, order);
 }
 
 // views per block of the single-image forward kernel for a launch of n_sel
@@ -557,6 +564,8 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   float* T = acc + (kPadR + warp * kWinR) * kBT;
   for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * kBW) acc[i] = 0.f;
   __syncthreads();
+  pdl_wait();      // the residual sinogram comes from the forward
+  pdl_release();
   const int kb = chunk * vpc, ke = min(n_sel, kb + vpc);
   const float* sb = sino + (size_t)bz * n_sel * B;
   const int4* trange = ranges + (size_t)tile * V_r;
@@ -768,6 +777,8 @@ __global__ void __launch_bounds__(256) k_backward_gather(const RayEntry* __restr
 // order.  grid.y = batch image (no index division).
 __global__ void __launch_bounds__(256) k_chunk_reduce(const float* __restrict__ part, int nplanes, size_t np,
                                                       float* __restrict__ out, float scale, int accumulate, int G) {
+  pdl_wait();
+  pdl_release();
   __shared__ PlaneSmem sm;
   const size_t b = blockIdx.y;
   const float* src = part + b * nplanes * np;
@@ -799,6 +810,8 @@ __global__ void __launch_bounds__(256) k_reduce_up_step_px(const float* __restri
                                                            float c, const float* __restrict__ y,
                                                            const float* __restrict__ eta_dev, float* __restrict__ z,
                                                            int s) {
+  pdl_wait();
+  pdl_release();
   const int J = blockIdx.x * 32 + threadIdx.x, I = blockIdx.y * 8 + threadIdx.y;
   if (I >= nc || J >= nc) return;
   const size_t b = blockIdx.z, np = (size_t)nc * nc;
@@ -818,6 +831,8 @@ __global__ void __launch_bounds__(256) k_reduce_up_step(const float* __restrict_
                                                         const float* __restrict__ y,
                                                         const float* __restrict__ eta_dev, float* __restrict__ z,
                                                         int s, int G) {
+  pdl_wait();
+  pdl_release();
   __shared__ PlaneSmem sm;
   const size_t b = blockIdx.y, np = (size_t)nc * nc;
   const float* src = part + b * nplanes * np;
@@ -851,6 +866,8 @@ __global__ void __launch_bounds__(256) k_reduce_power(const float* __restrict__ 
                                                       double* __restrict__ red, unsigned* __restrict__ ticket,
                                                       double* __restrict__ pw, double* L_out, double* eta_out,
                                                       float* etaf_out, int G) {
+  pdl_wait();
+  pdl_release();
   __shared__ double sd[256], sn[256];
   __shared__ PlaneSmem sm;
   __shared__ bool last;
@@ -920,11 +937,12 @@ int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, flo
   const int G = plane_groups(np, nplanes);
   if (G == 1) {
     dim3 grid((nc + 31) / 32, (nc + 7) / 8, batch);
-    k_reduce_up_step_px<<<grid, dim3(32, 8), 0, st>>>(part, nplanes, nc, c, y, eta_dev, z, s);
+    MS2G_CUDA(launch_k(k_reduce_up_step_px, grid, dim3(32, 8), 0, st, part, nplanes, nc, c, y, eta_dev, z, s));
     return check_launch("k_reduce_up_step_px");
   }
   dim3 grid(plane_blocks(np, G, 4096), batch);
-  k_reduce_up_step<<<grid, dim3(32, kPlaneGroups), 0, st>>>(part, nplanes, nc, c, y, eta_dev, z, s, G);
+  MS2G_CUDA(launch_k(k_reduce_up_step, grid, dim3(32, kPlaneGroups), 0, st, part, nplanes, nc, c, y, eta_dev, z, s,
+                     G));
   return check_launch("k_reduce_up_step");
 }
 
@@ -935,8 +953,8 @@ int launch_reduce_power(ms2g_plan* p, const float* part, int nplanes, size_t np,
   // (the fixed-order last-block reduction handles any grid size)
   const int G = plane_groups(np, nplanes);
   const int blocks = plane_blocks(np, G, red_blocks);
-  k_reduce_power<<<blocks, dim3(32, kPlaneGroups), 0, st>>>(part, nplanes, np, w_out, v, red, ticket, pw, L_out,
-                                                            eta_out, etaf_out, G);
+  MS2G_CUDA(launch_k(k_reduce_power, dim3(blocks), dim3(32, kPlaneGroups), 0, st, part, nplanes, np, w_out, v, red,
+                     ticket, pw, L_out, eta_out, etaf_out, G));
   return check_launch("k_reduce_power");
 }
 
@@ -956,8 +974,8 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_devices.fetch_or(bit);
   }
-  k_backward<H><<<grid, 32 * kBW, smem, s>>>(f.d_rays, f.d_bpr, p->V_r, p->B, d_sel, n_sel, sino, p->w_part,
-                                             f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order);
+  MS2G_CUDA(launch_k(k_backward<H>, grid, dim3(32 * kBW), smem, s, f.d_rays, (const int4*)f.d_bpr, p->V_r, p->B,
+                     d_sel, n_sel, sino, p->w_part, f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order));
   return MS2G_OK;
 }
 
@@ -1024,8 +1042,8 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   if (publish)   // NEXT-3: the chunk sum goes straight to the peer exchange slot (peer_reduce.cu)
     return launch_chunk_reduce_publish(p, p->w_part, ch[0] + ch[1], np, total, scale, s);
   const int G = plane_groups(np, ch[0] + ch[1]);
-  k_chunk_reduce<<<dim3(plane_blocks(np, G, 4096), batch), dim3(32, kPlaneGroups), 0, s>>>(
-      p->w_part, ch[0] + ch[1], np, img, scale, accumulate, G);
+  MS2G_CUDA(launch_k(k_chunk_reduce, dim3(plane_blocks(np, G, 4096), batch), dim3(32, kPlaneGroups), 0, s,
+                     (const float*)p->w_part, ch[0] + ch[1], np, img, scale, accumulate, G));
   return check_launch("k_chunk_reduce");
 }
 

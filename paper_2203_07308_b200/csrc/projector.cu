@@ -60,7 +60,15 @@ __device__ __forceinline__ float pair_src(const float* __restrict__ xb, int k, i
   float acc = 0.f;
   for (int a = 0; a < s; ++a) {
     const float* row = xb + (size_t)(s * k + a) * nsrc + (size_t)s * j;
-    for (int c = 0; c < s; ++c) acc += row[c];
+    if (s == 4) {            // one 16-byte load per row (same summation order)
+      const float4 v = *reinterpret_cast<const float4*>(row);
+      acc += v.x; acc += v.y; acc += v.z; acc += v.w;
+    } else if (s == 2) {
+      const float2 v = *reinterpret_cast<const float2*>(row);
+      acc += v.x; acc += v.y;
+    } else {
+      for (int c = 0; c < s; ++c) acc += row[c];
+    }
   }
   return acc * inv_s2 * scale;
 }
@@ -72,7 +80,10 @@ __device__ __forceinline__ float pair_src(const float* __restrict__ xb, int k, i
 __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pairs, size_t pair_stride, int nc,
                             int s, const double* __restrict__ scale_dev, float* __restrict__ v_out, int class_mask,
                             int il) {
-  __shared__ float T[33][33];
+  // T[r][c] = v[O0-2+r][L0+c] (column pairs, classes 0/2); with s > 1 also
+  // T2[r][c] = v[L0+r][O0-2+c] (row pairs, classes 1/3), so each s x s mean
+  // is formed once per tile (s = 1 reads the row pairs directly)
+  __shared__ float T[33][33], T2[32][34];
   pdl_wait();
   pdl_release();
   const int bz = blockIdx.z;
@@ -92,6 +103,13 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
     T[r][threadIdx.x] = val;
     if (v_out && in && r < 32) v_out[((size_t)bz * nc + k) * nc + j] = val;
   }
+  const bool rows2 = s > 1 && (class_mask & 10);
+  if (rows2)
+    for (int r = threadIdx.y; r < 32; r += 8)
+      for (int c = threadIdx.x; c < 33; c += 32) {
+        const int i = L0 + r, k = O0 - 2 + c;
+        T2[r][c] = (i < nc && k >= 0 && k < nc) ? pair_src(xb, i, k, nc, s, nsrc, inv_s2, scale) : 0.f;
+      }
   __syncthreads();
   const int o = O0 + threadIdx.x;
   if (o >= L) return;
@@ -107,8 +125,14 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
     if (class_mask & 4) pairs[2 * pair_stride + er] = make_float2(b, a);
     if (!(class_mask & 10)) continue;
     const int k = o - 2;
-    const float c = (k >= 0 && k < nc) ? pair_src(xb, line, k, nc, s, nsrc, inv_s2, scale) : 0.f;
-    const float d = (k + 1 >= 0 && k + 1 < nc) ? pair_src(xb, line, k + 1, nc, s, nsrc, inv_s2, scale) : 0.f;
+    float c, d;
+    if (rows2) {
+      c = T2[jj][threadIdx.x];
+      d = T2[jj][threadIdx.x + 1];
+    } else {
+      c = (k >= 0 && k < nc) ? pair_src(xb, line, k, nc, s, nsrc, inv_s2, scale) : 0.f;
+      d = (k + 1 >= 0 && k + 1 < nc) ? pair_src(xb, line, k + 1, nc, s, nsrc, inv_s2, scale) : 0.f;
+    }
     if (class_mask & 2) pairs[pair_stride + e] = make_float2(c, d);
     if (class_mask & 8) pairs[3 * pair_stride + er] = make_float2(d, c);
   }
@@ -422,9 +446,12 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
   if (nb == 8) fwd_launch_batch<8>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 4) fwd_launch_batch<4>(n_sel, batch, s, p, f, d_sel, b, out);
   else if (nb == 2) fwd_launch_batch<2>(n_sel, batch, s, p, f, d_sel, b, out);
-  else if (fwd_views_per_block(p, n_sel, batch) != kFwdWarps)
+  else if (fwd_views_per_block(p, n_sel, batch) != kFwdWarps) {
+    // short launches (view shards, registered subsets): 4 warps per view,
+    // 4 segments per ray; SPLIT x SEG = 2 x 4, 4 x 8, 2 x 8 measured slower
+    // ("tried and measured")
     fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
-  else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+  } else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
   const int rc = check_launch("k_forward");
   timing_end(p, slot, s);
   return rc;

@@ -30,6 +30,12 @@ namespace ms2g {
   } while (0)
 #endif
 
+// Zero entries on each side of every pair-image line beyond the two the
+// layout needs: a forward warp whose rays leave the grid by at most this many
+// rows inside its column range reads them without a clamp (projector.cu).
+constexpr int kPairPad = 64;
+__host__ __device__ inline size_t pair_line(int nc) { return (size_t)nc + 3 + 2 * kPairPad; }
+
 // Fixed-point minor coordinate: 32 fractional bits (1 unit = 2^-32 pixel).
 constexpr double kFix = 4294967296.0;
 
@@ -118,7 +124,7 @@ struct ms2g_plan {
   int sm_count = 148;                  // SMs of the plan's device
   int class_mask = 15;                 // ray classes (flags & 3) present in the rank's views, bit per class
   // workspaces (all sized for batch)
-  float2* w_pair = nullptr;            // forward gather images: 4 x [batch][n_c][n_c + 3] float2
+  float2* w_pair = nullptr;            // forward gather images: 4 x [batch][n_c][n_c + 3 + 2 kPairPad] float2
   size_t pair_stride = 0;              // float2 elements per pair image
   float* w_v = nullptr;                // coarse sketch
   float* w_rs = nullptr;               // separable-resampling intermediate [batch][n][n]

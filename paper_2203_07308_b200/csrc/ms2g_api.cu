@@ -759,7 +759,7 @@ static int ensure_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd) {
     ms2g_plan::PowerBranch br;
     br.factor = fac;
     const size_t nc = (size_t)f->nc, np = nc * nc;
-    br.pair_stride = nc * (nc + 3);
+    br.pair_stride = nc * pair_line(nc);
     const size_t planes = (size_t)(f->bp_chunks[0] + f->bp_chunks[1]);
     MS2G_CUDA(cudaMalloc(&br.w_v, sizeof(float) * np));
     MS2G_CUDA(cudaMalloc(&br.w_pair, sizeof(float2) * 4 * br.pair_stride));
@@ -1114,7 +1114,7 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
     return MS2G_OK;
   };
   p->red_blocks = 8 * sms;   // k_reduce_power grid cap (fp64 partials per block)
-  p->pair_stride = (size_t)p->nmax_c * (p->nmax_c + 3) * bt;
+  p->pair_stride = (size_t)p->nmax_c * pair_line(p->nmax_c) * bt;
   e = cudaMalloc(&p->w_pair, sizeof(float2) * 4 * p->pair_stride);
   if (e != cudaSuccess) {
     free_plan(p);

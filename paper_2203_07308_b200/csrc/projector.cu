@@ -39,11 +39,13 @@ __device__ __forceinline__ void seg_weights(unsigned lo, bool cross, float Lc, f
 // ------------------------------------------------------------ pair prep --
 // The forward projector gathers the two pixels (m0, m0+1) of a column with
 // ONE 8-byte load from "pair images": for every line of the minor-contiguous
-// layout, element k+2 (k = -2 .. n_c) holds (v[k], v[k+1]) with zeros outside
-// the grid.  Four images, indexed by the ray class (flags & 3):
+// layout, element kPairPad + k + 2 (k = -2 .. n_c) holds (v[k], v[k+1] - v[k])
+// with zeros outside the grid (the difference the forward's end-coordinate
+// weights need, formed once here in the same fp32 subtraction), and kPairPad
+// zero elements pad each end of a line.  Four images, indexed by the ray class (flags & 3):
 //   0 major-x      : lines = columns j of x, pairs along rows     (x^T)
 //   1 major-y      : lines = rows i of x,    pairs along columns
-//   2 major-x, mirrored: as 0 with each pair reversed (v[k+1], v[k]) and
+//   2 major-x, mirrored: as 0 with each pair reversed (v[k+1], v[k] - v[k+1]) and
 //      each line stored back to front (element nc - k holds it), so that the
 //      forward indexes every class the same way
 //   3 major-y, mirrored: as 1, reversed likewise
@@ -91,10 +93,11 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
   const float* xb = x + (size_t)bz * nsrc * nsrc;
   const float inv_s2 = 1.0f / (float)(s * s);
   const float scale = scale_dev ? (float)scale_dev[0] : 1.f;
-  const int L = nc + 3;
+  const int L = (int)pair_line(nc);
   const int mul = il > 1 ? il : 1, grp = bz / mul, sub = bz - grp * mul;   // interleaving group / slot
-  const size_t ib = (size_t)grp * nc * L;
-  const int O0 = blockIdx.x * 32, L0 = blockIdx.y * 32;   // output positions o, lines
+  const size_t ib = (size_t)grp * nc * L + kPairPad;                       // + the leading pad of a line
+  // output positions o = -kPairPad .. nc + 2 + kPairPad (outside 0 .. nc + 2: the zero pads), lines
+  const int O0 = blockIdx.x * 32 - kPairPad, L0 = blockIdx.y * 32;
   // rows k = O0-2 .. O0+30 for the column-pair images (this block owns O0-2 .. O0+29)
   for (int r = threadIdx.y; r < 33; r += 8) {
     const int k = O0 - 2 + r, j = L0 + threadIdx.x;
@@ -112,7 +115,7 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
       }
   __syncthreads();
   const int o = O0 + threadIdx.x;
-  if (o >= L) return;
+  if (o > nc + 2 + kPairPad) return;
   for (int jj = threadIdx.y; jj < 32; jj += 8) {
     const int line = L0 + jj;
     if (line >= nc) break;
@@ -121,8 +124,8 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
     const size_t er = (ib + (size_t)line * L + (nc + 2 - o)) * mul + sub;   // back-to-front line
     // only the ray classes this plan's views contain (a view shard of 45
     // degrees has one or two): the others are never read by the forward
-    if (class_mask & 1) pairs[e] = make_float2(a, b);
-    if (class_mask & 4) pairs[2 * pair_stride + er] = make_float2(b, a);
+    if (class_mask & 1) pairs[e] = make_float2(a, b - a);
+    if (class_mask & 4) pairs[2 * pair_stride + er] = make_float2(b, a - b);
     if (!(class_mask & 10)) continue;
     const int k = o - 2;
     float c, d;
@@ -133,8 +136,8 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
       c = (k >= 0 && k < nc) ? pair_src(xb, line, k, nc, s, nsrc, inv_s2, scale) : 0.f;
       d = (k + 1 >= 0 && k + 1 < nc) ? pair_src(xb, line, k + 1, nc, s, nsrc, inv_s2, scale) : 0.f;
     }
-    if (class_mask & 2) pairs[pair_stride + e] = make_float2(c, d);
-    if (class_mask & 8) pairs[3 * pair_stride + er] = make_float2(d, c);
+    if (class_mask & 2) pairs[pair_stride + e] = make_float2(c, d - c);
+    if (class_mask & 8) pairs[3 * pair_stride + er] = make_float2(d, c - d);
   }
 }
 
@@ -143,7 +146,7 @@ static int batch_group(int batch) { return (batch % 8 == 0) ? 8 : (batch % 4 == 
 
 int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream_t s, int factor,
                      const double* scale_dev, float* v_out) {
-  dim3 grid((nc + 3 + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
+  dim3 grid(((int)pair_line(nc) + 31) / 32, (nc + 31) / 32, batch), block(32, 8);
   static const bool il_on = getenv("MS2G_FWD_INTERLEAVE") != nullptr;   // experiment switch
   const int il = il_on ? batch_group(batch) : 1;
   MS2G_CUDA(launch_k(k_pair_prep, grid, block, 0, s, x, p->w_pair, p->pair_stride, nc, factor, scale_dev, v_out,
@@ -176,6 +179,32 @@ constexpr int kFwdWarps = MS2G_FWD_WARPS;
 #endif
 constexpr int kFwdUnroll = MS2G_FWD_UNROLL;
 
+
+// (pl, pu) = pair element e of a pair image (one 8-byte non-coherent load)
+__device__ __forceinline__ void fwd_ld_pair(const float2* base, unsigned e, float& pl, float& pu) {
+  asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
+      : "=f"(pl), "=f"(pu) : "r"(e), "l"(base));
+}
+
+// A lane whose ray misses the grid reads the zero element u = 0 throughout
+// (F0 = -1, S = 0).  The warp may skip the clamp when every lane's pair index
+// u stays within kPairPad of 0 .. nc + 2 over the warp's columns [wcl, wch)
+// (u is monotone in c: the ends decide).  99 % of the warps of the C3 / C4
+// geometries stay within ~60 rows; the others are mostly warps whose rays
+// change ray class (frame) inside the warp.
+__device__ __forceinline__ bool fwd_fast_warp(bool valid, int cl, int ch, int wcl, int wch, int nc, long long& F0,
+                                              unsigned& S) {
+  bool fit = true;
+  if (valid && cl > ch) {
+    F0 = -(1LL << 32);
+    S = 0;
+  } else if (valid && wcl < wch) {
+    const long long e0 = F0 + (long long)(wcl + 1) * (long long)S;   // E at the first column
+    const long long e1 = F0 + (long long)wch * (long long)S;         // E at the last column
+    fit = (e0 >> 32) + 1 >= -kPairPad && (e1 >> 32) + 1 <= nc + 2 + kPairPad;
+  }
+  return __all_sync(0xffffffffu, fit);
+}
 
 // Single images (NB = 1 here; batches use k_forward_batch below).
 // Each warp's column range is cut into SEG equal segments whose partial sums
@@ -225,12 +254,16 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
   const int wcl = __reduce_min_sync(0xffffffffu, cl);
   const int wch = __reduce_max_sync(0xffffffffu, ch);
   const int len = wch > wcl ? wch - wcl : 0;
-  const int L = nc + 3;
+  const int L = (int)pair_line(nc);
   const size_t istride = (size_t)nc * L;            // pair-image stride between batch images
   const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
-  // element of pair index u on line c: c L + u for every class (the mirrored
-  // images are stored back to front); u is clamped to the zero pads
-  // (unsigned: negatives clamp too)
+  const bool fast = fwd_fast_warp(valid, cl, ch, wcl, wch, nc, F0, S);
+  // element of pair index u on line c: c L + kPairPad + u for every class
+  // (the mirrored images are stored back to front).  Fast warps (all rays
+  // within kPairPad rows of the grid over the warp's columns) advance
+  // (u + c L, frac) as ONE 64-bit fixed-point number: one add.cc/addc pair
+  // per column gives both the element and the weight.  Other warps clamp u
+  // to the zero pads (unsigned: negatives clamp too).
   const unsigned umax = (unsigned)(nc + 2);
 #pragma unroll 1
   for (int j = 0; j < SPW; ++j) {
@@ -242,25 +275,45 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
     if (c0 < c1) {
       const long long Es = F0 + (long long)c0 * (long long)S + (long long)S + (1LL << 32);
       unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
-      unsigned offk = (unsigned)(c0 * L);
+      if (fast) {
+        unsigned qhi = ehi + (unsigned)(c0 * L + kPairPad);
 #pragma unroll kFwdUnroll
-      for (int c = c0; c < c1; ++c) {
-        unsigned lo1, hi1;
-        asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
-        const float mf = (float)min(elo, S);
-        const unsigned e = offk + min(ehi, umax);
-        MS2G_DASSERT(e < (unsigned)(nc * L));
+        for (int c = c0; c < c1; ++c) {
+          unsigned lo1, hi1;
+          asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;" : "=r"(lo1), "=r"(hi1)
+              : "r"(elo), "r"(qhi), "r"(S), "r"(L));
+          const float mf = (float)min(elo, S);
+          MS2G_DASSERT(qhi < (unsigned)(nc * L));
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          float pl, pu;
-          asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
-              : "=f"(pl), "=f"(pu) : "r"(e), "l"(base + i * istride));
-          sa[i] += pl;
-          sb[i] = fmaf(mf, pu - pl, sb[i]);
+          for (int i = 0; i < NB; ++i) {
+            float pl, pu;
+            fwd_ld_pair(base + i * istride, qhi, pl, pu);
+            sa[i] += pl;
+            sb[i] = fmaf(mf, pu, sb[i]);
+          }
+          elo = lo1;
+          qhi = hi1;
         }
-        elo = lo1;
-        ehi = hi1;
-        offk += L;
+      } else {
+        unsigned offk = (unsigned)(c0 * L + kPairPad);
+#pragma unroll kFwdUnroll
+        for (int c = c0; c < c1; ++c) {
+          unsigned lo1, hi1;
+          asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
+          const float mf = (float)min(elo, S);
+          const unsigned e = offk + min(ehi, umax);
+          MS2G_DASSERT(e < (unsigned)(nc * L));
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            float pl, pu;
+            fwd_ld_pair(base + i * istride, e, pl, pu);
+            sa[i] += pl;
+            sb[i] = fmaf(mf, pu, sb[i]);
+          }
+          elo = lo1;
+          ehi = hi1;
+          offk += L;
+        }
       }
     }
 #pragma unroll
@@ -326,7 +379,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
 #pragma unroll
   for (int i = 0; i < NB; ++i) { sa[i] = 0.f; sb[i] = 0.f; }
   if (wcl < wch) {
-    const int L = nc + 3;
+    const int L = (int)pair_line(nc);
     const size_t istride = (size_t)nc * L;
     // separate layout: image i's pair image at base + i istride; interleaved
     // (IL): the group's NB pairs of element e at base + e NB
@@ -334,7 +387,9 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
     const unsigned umax = (unsigned)(nc + 2);
     const long long Es = F0 + (long long)wcl * (long long)S + (long long)S + (1LL << 32);
     unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
-    unsigned offk = (unsigned)(wcl * L);
+    // u clamped to the zero pads (the carry-chained form of k_forward saves
+    // 2 of ~5 NB instructions per column here and costs 6 registers at NB = 8)
+    unsigned offk = (unsigned)(wcl * L + kPairPad);
 #pragma unroll kFwdUnroll
     for (int c = wcl; c < wch; ++c) {
       unsigned lo1, hi1;
@@ -350,9 +405,9 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
           asm("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(q + i / 2));
           sa[i] += v.x;
-          sb[i] = fmaf(mf, v.y - v.x, sb[i]);
+          sb[i] = fmaf(mf, v.y, sb[i]);
           sa[i + 1] += v.z;
-          sb[i + 1] = fmaf(mf, v.w - v.z, sb[i + 1]);
+          sb[i + 1] = fmaf(mf, v.w, sb[i + 1]);
         }
       } else {
 #pragma unroll
@@ -361,7 +416,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
           asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
               : "=f"(pl), "=f"(pu) : "r"(e), "l"(base + i * istride));
           sa[i] += pl;
-          sb[i] = fmaf(mf, pu - pl, sb[i]);
+          sb[i] = fmaf(mf, pu, sb[i]);
         }
       }
       elo = lo1;

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out,
-                                                 const int* __restrict__ order) {
+                                                 const int* __restrict__ order, int allow_fast) {
   constexpr int VPB = kFwdWarps / SPLIT;             // views per block
   constexpr int SPW = SEG / SPLIT;                   // segments per warp
 
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
   const int L = (int)pair_line(nc);
   const size_t istride = (size_t)nc * L;            // pair-image stride between batch images
   const float2* base = pairs + cls * pair_stride + (size_t)bz0 * istride;
-  const bool fast = fwd_fast_warp(valid, cl, ch, wcl, wch, nc, F0, S);
+  const bool fast = fwd_fast_warp(valid, cl, ch, wcl, wch, nc, F0, S) && allow_fast;
   // element of pair index u on line c: c L + kPairPad + u for every class
   // (the mirrored images are stored back to front).  Fast warps (all rays
   // within kPairPad rows of the grid over the warp's columns) advance
@@ -473,8 +473,10 @@ static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, cons
   const int* order = no_order ? nullptr
                               : (d_sel ? order_sel
                                        : ((n_sel == p->V_r && f.fwd_order_vpb == VPB) ? f.d_fwd_order : nullptr));
+  // experiment / test switch: every warp on the clamped path (bitwise equal)
+  static const int allow_fast = getenv("MS2G_FWD_NO_FAST") ? 0 : 1;
   (void)launch_k(k_forward<NB, SPLIT, SEG>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
-                 (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, order);
+                 (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, order, allow_fast);
 }
 
 // views per block of the single-image forward kernel for a launch of n_sel

@@ -876,6 +876,40 @@ def test_tv_persistent_kernel(P, n, batch):
         assert np.array_equal(other.astype(np.float64), outs[0]), extra
 
 
+def test_forward_fast_path_bitwise(P):
+    """The forward's carry-chained element index (warps whose rays stay within
+    kPairPad rows of the grid) against the clamped path for every warp
+    (MS2G_FWD_NO_FAST=1, subprocess): bitwise equal on ragged grids, factors
+    2 and 3, a view subset, a 45-degree view shard, an odd batch and a tiny
+    grid narrower than the pad."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import ms2g_synth as S, paper_2203_07308_b200 as P
+P.load()
+outs = []
+for n, V, B, facs, batch, sub, vb, ve in ((64, 90, 96, (2, 1), 1, None, 0, None), (40, 20, 62, (2, 1), 3, [1, 4, 7, 9, 15], 0, None),
+                                          (96, 33, 150, (3, 1), 1, list(range(0, 33, 3)), 0, None),
+                                          (256, 360, 384, (2, 1), 1, None, 45, 90), (8, 12, 14, (1,), 1, None, 0, None)):
+    with P.plan_geometry(n, V, B, factors=facs, batch=batch, view_begin=vb, view_end=ve) as plan:
+        for s in facs:
+            x = np.stack([S.random_image(n, 30 + s + i) for i in range(batch)]).astype(np.float32)
+            outs.append(P.forward_project(plan, s, torch.from_numpy(x).cuda(), subset=sub).cpu().numpy().ravel())
+sys.stdout.buffer.write(np.concatenate(outs).astype(np.float32).tobytes())
+''' % root
+    res = []
+    for extra in ({}, {"MS2G_FWD_NO_FAST": "1"}):
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, env=dict(os.environ, **extra),
+                             timeout=600)
+        assert out.returncode == 0, out.stderr.decode()[-2000:]
+        res.append(np.frombuffer(out.stdout, dtype=np.float32))
+    assert res[0].size > 0 and np.array_equal(res[0], res[1])
+
+
 def test_gather_adjoint_variant_parity(P):
     """The pixel-driven gather adjoint (MS2G_BP_VARIANT=gather, the measured
     alternative to the tile-driven scatter) against the oracle on zero-mean

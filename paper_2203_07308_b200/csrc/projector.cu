@@ -539,8 +539,9 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
 // negatives clamp too) and every warp window has two pad rows on each side
 // (shared between neighbouring windows), so no predicate is needed.  Record
 // per ray: {lo(Et), hi(Et), S, Ly32 r}, one broadcast LDS.128 per step.  The
-// kernel is bound by the L1/shared data pipe: 6 wavefronts per step (the
-// broadcast LDS.128 costs 2, each 32-bit LDS / STS 1), 91-95 % of the peak.
+// kernel is bound by the L1/shared data pipe (91-95 % of the peak): ~4.2
+// shared-memory wavefronts per step (each 32-bit LDS / STS 1, the broadcast
+// record almost free; ncu at C4 s=1) plus the ray-record / residual loads.
 //
 // The X- and Y-families write separate partial planes (per view chunk too);
 // k_chunk_reduce sums them in fixed order.

@@ -252,6 +252,21 @@ __device__ __forceinline__ float tv_div(const float* __restrict__ px, const floa
   return a + b;
 }
 
+// The per-point arithmetic of every TV-prox form, in one explicit order (no
+// compiler contraction choices), so that all forms produce the same bits:
+//   w = d - f / lambda  (d = div p, 0 at p^0 = 0)
+//   p' = (p + tau q) / (1 + tau |q|)  with the MUFU square root / reciprocal
+//   u = f - lambda div p
+__device__ __forceinline__ float tv_w(float d, float f, float inv_lambda) { return fmaf(-f, inv_lambda, d); }
+__device__ __forceinline__ float tv_rden(float qx, float qy, float tau) {
+  float sq, rden;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(fmaf(qy, qy, qx * qx)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rden) : "f"(fmaf(tau, sq, 1.f)));
+  return rden;
+}
+__device__ __forceinline__ float tv_p(float p, float q, float tau, float rden) { return fmaf(tau, q, p) * rden; }
+__device__ __forceinline__ float tv_u(float f, float div, float lambda) { return fmaf(-lambda, div, f); }
+
 // One dual iteration.  The block's 32 x 8 pixels need w = div p - f / lambda
 // on themselves and one column / row beyond: w is formed once per point into
 // a (8+1) x (32+1) shared tile (instead of three times per pixel), then
@@ -298,7 +313,7 @@ __global__ void __launch_bounds__(256) k_tv_iter(const float* __restrict__ f, co
     if (gi < n && gj < n) {
       const size_t q = (size_t)gi * n + gj;
       const float fq = first ? fb[q] : fe[k];
-      w = (first ? 0.f : tv_div(px, py, n, gi, gj)) - fq * inv_lambda;
+      w = tv_w(first ? 0.f : tv_div(px, py, n, gi, gj), fq, inv_lambda);
     }
     sw[li][lj] = w;
   }
@@ -311,12 +326,10 @@ __global__ void __launch_bounds__(256) k_tv_iter(const float* __restrict__ f, co
   const float qy = (i < n - 1) ? sw[ty + 1][tx] - wc : 0.f;
   // 1 / (1 + tau |q|) with the MUFU square root and reciprocal (relative error
   // ~1e-7 per call, far inside the 1e-5 operator gate; the geometry is exact)
-  float sq, rden;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(qx * qx + qy * qy));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rden) : "f"(fmaf(tau, sq, 1.f)));
+  const float rden = tv_rden(qx, qy, tau);
   float* ox = pout + b * 2 * np;
-  ox[p] = ((first ? 0.f : px[p]) + tau * qx) * rden;
-  ox[np + p] = ((first ? 0.f : py[p]) + tau * qy) * rden;
+  ox[p] = tv_p(first ? 0.f : px[p], qx, tau, rden);
+  ox[np + p] = tv_p(first ? 0.f : py[p], qy, tau, rden);
 }
 __global__ void k_tv_final(const float* __restrict__ f, const float* __restrict__ pin,
                            const float* __restrict__ xprev, float* __restrict__ xout, float* __restrict__ yout,
@@ -330,7 +343,7 @@ __global__ void k_tv_final(const float* __restrict__ f, const float* __restrict_
   pdl_wait();
   pdl_release();
   if (!in) return;
-  const float u = fv - lambda * tv_div(px, px + np, n, i, j);
+  const float u = tv_u(fv, tv_div(px, px + np, n, i, j), lambda);
   mix_momentum(idx, fv, u, xprev, xout, yout, alpha, a, mode, flag, iter);
 }
 
@@ -501,7 +514,7 @@ __global__ void __launch_bounds__(1024, 1) k_tv_persist(const float* __restrict_
             const float by = (i < n - 1 ? pyr[j] : 0.f) - (i > 0 ? pyr[j - n] : 0.f);
             d = ax + by;
           }
-          w[(size_t)r * n + j] = d - fr[j] * inv_lambda;
+          w[(size_t)r * n + j] = tv_w(d, fr[j], inv_lambda);
         }
       }
       __syncthreads();
@@ -514,11 +527,9 @@ __global__ void __launch_bounds__(1024, 1) k_tv_persist(const float* __restrict_
           const float wc = wr[j];
           const float qx = (j < n - 1) ? wr[j + 1] - wc : 0.f;
           const float qy = (i < n - 1) ? wr[j + n] - wc : 0.f;
-          float sq, rden;
-          asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(qx * qx + qy * qy));
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rden) : "f"(fmaf(tau, sq, 1.f)));
-          pxr[j] = ((first ? 0.f : pxr[j]) + tau * qx) * rden;
-          pyr[j] = ((first ? 0.f : pyr[j]) + tau * qy) * rden;
+          const float rden = tv_rden(qx, qy, tau);
+          pxr[j] = tv_p(first ? 0.f : pxr[j], qx, tau, rden);
+          pyr[j] = tv_p(first ? 0.f : pyr[j], qy, tau, rden);
         }
       }
       __syncthreads();
@@ -558,7 +569,7 @@ __global__ void __launch_bounds__(1024, 1) k_tv_persist(const float* __restrict_
       }
       const size_t idx = (size_t)R * n + j;
       const float fv = f[idx];
-      mix_momentum(idx, fv, fv - lambda * dv, xprev, xout, yout, alpha, a, mode, flag, iter);
+      mix_momentum(idx, fv, tv_u(fv, dv, lambda), xprev, xout, yout, alpha, a, mode, flag, iter);
     }
   }
   // the last CTA to finish advances the generation for the next launch
@@ -660,8 +671,8 @@ int launch_tv(int n, int batch, float lambda, float tau, int iters, const float*
   float* pin = p0;
   float* pout = p1;
   for (int k = 0; k < iters; ++k) {
-    MS2G_CUDA(launch_k_pdl(k_tv_iter, px_grid(n, n, batch), kPxBlock, 0, st, f, (const float*)pin, pout, n, 1.f / lambda,
-                       tau, (int)(k == 0)));
+    MS2G_CUDA(launch_k_pdl(k_tv_iter, px_grid(n, n, batch), kPxBlock, 0, st, f, (const float*)pin, pout, n,
+                           1.f / lambda, tau, (int)(k == 0)));
     MS2G_TRY(check_launch("k_tv_iter"));
     float* tmp = pin;
     pin = pout;

@@ -2,6 +2,7 @@
 # Reproduce profiles/ (round 2) on one B200 (run under gpurun from the repo
 # root), then summarise here:
 #   gpurun -- bash scripts/refresh_profiles.sh   &&   bash scripts/refresh_profiles.sh --summarise
+# (profiles/parity_r02.md: run the GPU tests with MS2G_PARITY_LOG=gpurun_out/parity_r02.json first)
 # Every ncu capture runs only after the same command exited 0 without ncu
 # (B200_PROFILING.md); ncu timings are never bench values.  The projector
 # capture is summarised into profiles/ncu_traffic.json on the box BEFORE the
@@ -23,6 +24,12 @@ if [ "$1" = "--summarise" ]; then
   python scripts/ncu_summary.py full gpurun_out/prof_gather.ncu-rep profiles/${R}_ncu_full_adjoint_gather.md > /dev/null
   python scripts/ncu_summary.py full gpurun_out/prof_c5fwd.ncu-rep profiles/${R}_ncu_full_forward_batch8.md > /dev/null
   cp gpurun_out/adjoint_variants.log profiles/${R}_adjoint_variants.log
+  python scripts/ncu_summary.py launches gpurun_out/launches_shard8.csv profiles/${R}_launches_shard8.md --last-solve > /dev/null
+  cp gpurun_out/launches_shard8.csv profiles/${R}_launches_shard8.csv
+  cp gpurun_out/tv_probe.log profiles/${R}_tv_probe.log
+  if [ -f gpurun_out/parity_r02.json ]; then
+    python scripts/parity_report.py gpurun_out/parity_r02.json profiles/parity_r02.md
+  fi
   exit 0
 fi
 mkdir -p gpurun_out
@@ -44,6 +51,10 @@ for c in 3 5; do
         python scripts/profile_solve.py --cfg $c > gpurun_out/ncu_c$c.log 2>&1
 done
 python scripts/adjoint_variants.py > gpurun_out/adjoint_variants.log 2>&1
+python scripts/profile_small.py shard > gpurun_out/plain5.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_shard8.csv \
+      python scripts/profile_small.py shard > gpurun_out/ncu5.log 2>&1
+python scripts/tv_probe.py > gpurun_out/tv_probe.log 2>&1
 MS2G_BP_VARIANT=gather python scripts/profile_run.py --mode kernels > gpurun_out/plain3.log 2>&1 && \
   MS2G_BP_VARIANT=gather ncu --set full --clock-control none --import-source on -k regex:"k_backward_gather" -s 1 \
       -c 1 -o gpurun_out/prof_gather -f python scripts/profile_run.py --mode kernels > gpurun_out/ncu3.log 2>&1

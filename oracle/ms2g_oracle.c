@@ -16,8 +16,10 @@
  * disks/ellipses), adjoint identity, A_s = A U_s, mass conservation of S_s /
  * U_s, finite differences of the LS objective, subset-partition identity,
  * SVD of the dense A, Gaussian closed-form weights, TV 2x2 closed form and
- * duality gap, SplitMix64 known answers, CG normal-equation optimum.
- * "parity unpinned": the K=10 TV output beyond its recurrence.
+ * duality gap, TV at finite K (K = 1 by hand on a 3x3 impulse; mean,
+ * translation / scale covariance, transposition, |u - f| <= 4 lam and the
+ * non-increasing dual energy at K = 1, 2, 3, 10), SplitMix64 known answers,
+ * CG normal-equation optimum.
  */
 #include <math.h>
 #include <pthread.h>

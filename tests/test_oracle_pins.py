@@ -400,6 +400,48 @@ def test_tv_two_by_two_closed_form():
     assert np.max(np.abs(u - np.array([[a, b], [b, b]]))) < 1e-7
 
 
+def test_tv_one_iteration_closed_form():
+    """K = 1 by hand (Z18; tau = 1/8, t = tau/lam): from p^0 = 0,
+    p^1 = -t grad f / (1 + t |grad f|), u = f - lam div p^1.  For the 3x3
+    unit impulse f (forward differences, zero last row / column) grad f is
+    (1, 0) at (1,0), (0, 1) at (0,1), (-1, -1) at (1,1), so
+      u(1,1) = 1 - lam (2t/(1+t) + 2t/(1+sqrt2 t)),
+      u(1,0) = u(0,1) = lam t/(1+t),  u(1,2) = u(2,1) = lam t/(1+sqrt2 t),
+    corners 0 (the left/top neighbours receive the 1-norm-1 fluxes, the
+    right/bottom ones the diagonal flux)."""
+    lam = 0.1
+    t = 0.125 / lam
+    f = np.zeros((3, 3)); f[1, 1] = 1.0
+    u = O.tv_chambolle(f, lam, 1)
+    a, d = t / (1 + t), t / (1 + np.sqrt(2) * t)
+    want = np.array([[0.0, lam * a, 0.0], [lam * a, 1 - lam * (2 * a + 2 * d), lam * d], [0.0, lam * d, 0.0]])
+    assert np.max(np.abs(u - want)) < 1e-15
+
+
+def test_tv_finite_k_invariants():
+    """Properties of Chambolle's iteration at every K (what K = 10 is
+    pinned by): the mean is preserved (div has zero sum under the zero-flux
+    boundary), translation and scale covariance u(f + c) = u(f) + c and
+    u(c f; c lam) = c u(f; lam), transposition symmetry, |u - f| <= 4 lam
+    (dual feasibility |p| <= 1), and the dual energy ||f - lam div p^n||^2
+    non-increasing in n for tau <= 1/8 (Chambolle 2004, Thm 3.1)."""
+    rng = np.random.default_rng(3)
+    f = S.phantom(24, 5, 7).astype(np.float64) + 0.05 * rng.standard_normal((24, 24))
+    lam = 0.05
+    for K in (1, 2, 3, 10):
+        u = O.tv_chambolle(f, lam, K)
+        assert abs(u.sum() - f.sum()) <= 1e-12 * np.abs(f).sum()
+        assert np.max(np.abs(O.tv_chambolle(f + 0.3, lam, K) - (u + 0.3))) < 1e-14
+        assert np.max(np.abs(O.tv_chambolle(2.5 * f, 2.5 * lam, K) - 2.5 * u)) < 1e-14
+        assert np.array_equal(O.tv_chambolle(np.ascontiguousarray(f.T), lam, K), u.T)
+        assert np.max(np.abs(u - f)) <= 4 * lam * (1 + 1e-12)
+    E = []
+    for K in range(0, 25):
+        _, p = O.tv_chambolle(f, lam, K, return_dual=True)
+        E.append(np.sum((f - lam * O.div(p[0], p[1])) ** 2))
+    assert all(E[k + 1] <= E[k] * (1 + 1e-14) for k in range(len(E) - 1)) and E[-1] < E[0]
+
+
 # ------------------------------------------------------------- O11 / O13
 def test_momentum_values():
     """a_i = (i-1)/(i+3): a1 = 0, a2 = 0.2, a5 = 0.5, a9 = 2/3 (P:156, S:251)."""

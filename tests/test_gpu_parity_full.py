@@ -148,3 +148,24 @@ def test_c5_batch8_solve_full(P):
     for im in (0, pr.batch - 1):
         xr, _, _ = O.pnp_ms2g(g, pr.stages, bs[im], den=pr.den, alpha=pr.alpha)
         measure(f"C5 batch-8 solve, image {im}", xb[im], xr, TOL_SOLVE)
+
+
+def test_c5_ranks_spot_check(P):
+    """C5 over 8 ranks x batch 8 (64 images, BASELINE configs[4]; SURVEY
+    §8(d) "images {0, 21, 42, 63}"): rank r solves images 8r .. 8r+7 with no
+    collective in the data path (bench.py --cfg 5), so the ranks owning
+    images 21, 42 and 63 (ranks 2, 5, 7) are run one after another on one
+    GPU, each as its full batch of 8, and those images are compared with
+    their own oracle solves (image 0, rank 0: test_c5_batch8_solve_full)."""
+    pr = S.PRESETS[5]
+    g = O.Geometry(pr.n, pr.n_views, pr.n_bins)
+    with P.plan_geometry(pr.n, pr.n_views, pr.n_bins, factors=(2, 1), batch=pr.batch) as plan:
+        for im in (21, 42, 63):
+            rank = im // pr.batch
+            bs = []
+            for j in range(rank * pr.batch, (rank + 1) * pr.batch):
+                xt = S.phantom(pr.n, pr.n_ellipses, S.config_seed(5, j))
+                bs.append(S.poisson_data(O.forward(g, 1, xt), pr.noise[1], S.config_seed(5, j)))
+            xb = host(P.pnp_ms2g_solve(plan, pr.stages, dev(np.stack(bs)), den=pr.den, alpha=pr.alpha))
+            xr, _, _ = O.pnp_ms2g(g, pr.stages, bs[im % pr.batch], den=pr.den, alpha=pr.alpha)
+            measure(f"C5 rank {rank} of 8 (batch 8), image {im}", xb[im % pr.batch], xr, TOL_SOLVE)

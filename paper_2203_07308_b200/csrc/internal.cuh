@@ -57,6 +57,15 @@ struct __align__(16) RayEntry {
 };
 static_assert(sizeof(RayEntry) == 32, "RayEntry must be 32 bytes");
 
+// The adjoint's half of a ray (16 bytes, same values as RayEntry): its
+// record loads are part of the L1 data pipe the adjoint is bound by.
+struct __align__(16) RayBp {
+  long long F0;
+  unsigned S;
+  float Ly32;
+};
+static_assert(sizeof(RayBp) == 16, "RayBp must be 16 bytes");
+
 // Per-view constants.  Detector coordinate of a point P (pixel units of the
 // n_c grid): tau(P) = off + scale * ((P-S).e) / ((P-S).n).  The bins of a view
 // split into <= 4 contiguous runs of one ray class (the ray angle is monotone
@@ -72,6 +81,7 @@ static_assert(sizeof(ViewEntry) == 48, "ViewEntry must be 48 bytes");
 struct FactorTables {
   int factor = 0, nc = 0;
   RayEntry* d_rays = nullptr;     // [V_r][B]
+  RayBp* d_rays_bp = nullptr;     // [V_r][B], the adjoint's fields
   ViewEntry* d_views = nullptr;   // [V_r]
   int bp_chunks[2] = {1, 1};      // view chunks of the backprojector per tile family (X, Y)
   // step size cached per factor by the last power iteration on this plan:

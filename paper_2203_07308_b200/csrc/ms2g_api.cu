@@ -245,6 +245,12 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   MS2G_CUDA(cudaMalloc(&f.d_rays, sizeof(RayEntry) * rays.size()));
   MS2G_CUDA(cudaMalloc(&f.d_views, sizeof(ViewEntry) * views.size()));
   MS2G_CUDA(cudaMemcpy(f.d_rays, rays.data(), sizeof(RayEntry) * rays.size(), cudaMemcpyHostToDevice));
+  {
+    std::vector<RayBp> bp(rays.size());
+    for (size_t i = 0; i < rays.size(); ++i) bp[i] = RayBp{rays[i].F0, rays[i].S, rays[i].Ly32};
+    MS2G_CUDA(cudaMalloc(&f.d_rays_bp, sizeof(RayBp) * bp.size()));
+    MS2G_CUDA(cudaMemcpy(f.d_rays_bp, bp.data(), sizeof(RayBp) * bp.size(), cudaMemcpyHostToDevice));
+  }
   MS2G_CUDA(cudaMemcpy(f.d_views, views.data(), sizeof(ViewEntry) * views.size(), cudaMemcpyHostToDevice));
   MS2G_TRY(build_bicubic_tables(f, d.n));
   MS2G_CUDA(cudaMalloc(&f.d_Lcache, 3 * sizeof(double)));
@@ -337,6 +343,7 @@ static void free_plan(ms2g_plan* p) {
   if (!p) return;
   for (auto& f : p->ft) {
     cudaFree(f.d_rays);
+    cudaFree(f.d_rays_bp);
     cudaFree(f.d_views);
     cudaFree(f.d_bpr);
     cudaFree(f.d_bp_order);

@@ -625,7 +625,7 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
 }
 
 template <int H>
-__global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(const RayEntry* __restrict__ rays,
+__global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(const RayBp* __restrict__ rays,
                                                           const int4* __restrict__ ranges, int V_r, int B,
                                                           const int* __restrict__ sel, int n_sel,
                                                           const float* __restrict__ sino, float* __restrict__ part,
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
 
   run = 0; nr = 0; te = -1; tb = 0;
   bool have = next_round();
-  RayEntry Rn;
+  RayBp Rn;
   float rn = 0.f;
   int tn = tb + lane;
   if (have && tn <= te) {
@@ -1059,7 +1059,7 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_devices.fetch_or(bit);
   }
-  MS2G_CUDA(launch_k(k_backward<H>, grid, dim3(32 * kBW), smem, s, f.d_rays, (const int4*)f.d_bpr, p->V_r, p->B,
+  MS2G_CUDA(launch_k(k_backward<H>, grid, dim3(32 * kBW), smem, s, f.d_rays_bp, (const int4*)f.d_bpr, p->V_r, p->B,
                      d_sel, n_sel, sino, p->w_part, f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order));
   return MS2G_OK;
 }

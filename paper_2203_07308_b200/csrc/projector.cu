@@ -624,6 +624,50 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
   return check_launch("k_bp_ranges");
 }
 
+// The adjoint's steps over one round of <= 32 ray records (one broadcast
+// LDS.128 each): per step the lane's end coordinate, the two weights and two
+// shared read-modify-writes, the lower row at a compile-time offset.
+template <bool MIR, int H>
+__device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, int nrays, int lane, unsigned sbase,
+                                         unsigned acc0, unsigned acc1) {
+  constexpr int kStride = MIR ? -4 * kBT : 4 * kBT;   // bytes per row step of u
+  (void)acc0;
+  (void)acc1;
+  float4 a = p4[0];
+#pragma unroll 4
+  for (int q = 0; q < nrays; ++q) {
+    const float4 an = p4[q + 1];
+    const unsigned S = __float_as_uint(a.z);
+    unsigned lo, u;
+    asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;"
+        : "=r"(lo), "=r"(u)
+        : "r"((unsigned)lane), "r"(S), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
+    const unsigned m = min(lo, S);
+    const float mu = (float)m, ml = (float)(S - m);
+    const unsigned adu = sbase + min(u, (unsigned)(H + 2)) * (unsigned)kStride;
+    MS2G_DASSERT(adu >= acc0 && adu < acc1 && adu - kStride >= acc0 && adu - kStride < acc1);
+    if (MIR)
+      asm volatile("{\n\t.reg .f32 c0, c1;\n\t"
+                   "ld.shared.f32 c0, [%0];\n\t"
+                   "ld.shared.f32 c1, [%0+128];\n\t"
+                   "fma.rn.f32 c0, %1, %3, c0;\n\t"
+                   "fma.rn.f32 c1, %2, %3, c1;\n\t"
+                   "st.shared.f32 [%0], c0;\n\t"
+                   "st.shared.f32 [%0+128], c1;\n\t}"
+                   :: "r"(adu), "f"(mu), "f"(ml), "f"(a.w) : "memory");
+    else
+      asm volatile("{\n\t.reg .f32 c0, c1;\n\t"
+                   "ld.shared.f32 c0, [%0];\n\t"
+                   "ld.shared.f32 c1, [%0+-128];\n\t"
+                   "fma.rn.f32 c0, %1, %3, c0;\n\t"
+                   "fma.rn.f32 c1, %2, %3, c1;\n\t"
+                   "st.shared.f32 [%0], c0;\n\t"
+                   "st.shared.f32 [%0+-128], c1;\n\t}"
+                   :: "r"(adu), "f"(mu), "f"(ml), "f"(a.w) : "memory");
+    a = an;
+  }
+}
+
 template <int H>
 __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(const RayBp* __restrict__ rays,
                                                           const int4* __restrict__ ranges, int V_r, int B,
@@ -725,37 +769,13 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
       Rn = rays[(size_t)g * B + tn];
       rn = __ldg(sb + (size_t)k * B + tn);
     }
-    // upper row u - 1 -> byte address sbase + u * sstride; lower = that - sstride
+    // upper row u - 1 -> byte address sbase + u * stride, the lower row one
+    // stride back (an immediate offset: the loop is instantiated per sign)
     //   plain:  phys row = u - 1      (sbase at row -1)
     //   mirror: phys row = kBH - u    (sbase at row kBH, negative stride)
-    const unsigned sbase = tbase + (mir ? 4u * kBT * kBH : (unsigned)(-4 * kBT));
-    const unsigned sstride = mir ? (unsigned)(-4 * kBT) : 4u * kBT;
     const int nrays = min(32, cte - ctb + 1);
-    const float4* p4 = st4[warp];
-    float4 a = p4[0];
-#pragma unroll 2
-    for (int q = 0; q < nrays; ++q) {
-      const float4 an = p4[q + 1];
-      const unsigned S = __float_as_uint(a.z);
-      unsigned lo, u;
-      asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\tmadc.hi.u32 %1, %2, %3, %5;"
-          : "=r"(lo), "=r"(u)
-          : "r"((unsigned)lane), "r"(S), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
-      const unsigned m = min(lo, S);
-      const float mu = (float)m, ml = (float)(S - m);
-      const unsigned adu = sbase + min(u, (unsigned)(kBH + 2)) * sstride;
-      const unsigned adl = adu - sstride;
-      MS2G_DASSERT(adu >= acc0 && adu < acc1 && adl >= acc0 && adl < acc1);
-      asm volatile("{\n\t.reg .f32 c0, c1;\n\t"
-                   "ld.shared.f32 c0, [%0];\n\t"
-                   "ld.shared.f32 c1, [%1];\n\t"
-                   "fma.rn.f32 c0, %2, %4, c0;\n\t"
-                   "fma.rn.f32 c1, %3, %4, c1;\n\t"
-                   "st.shared.f32 [%0], c0;\n\t"
-                   "st.shared.f32 [%1], c1;\n\t}"
-                   :: "r"(adu), "r"(adl), "f"(mu), "f"(ml), "f"(a.w) : "memory");
-      a = an;
-    }
+    if (mir) bp_steps<true, kBH>(st4[warp], nrays, lane, tbase + 4u * kBT * kBH, acc0, acc1);
+    else bp_steps<false, kBH>(st4[warp], nrays, lane, tbase - 4u * kBT, acc0, acc1);
     __syncwarp();
   }
   __syncthreads();

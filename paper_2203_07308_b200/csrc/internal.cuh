@@ -82,6 +82,10 @@ struct FactorTables {
   int factor = 0, nc = 0;
   RayEntry* d_rays = nullptr;     // [V_r][B]
   RayBp* d_rays_bp = nullptr;     // [V_r][B], the adjoint's fields
+  // adjoint fixed-point scale bounds: per (tile family, view) an upper bound
+  // of the weight one pixel receives from the view's rays; the largest Lc
+  float* d_bpw = nullptr;         // [2][V_r]
+  float lc_max = 0.f;
   ViewEntry* d_views = nullptr;   // [V_r]
   int bp_chunks[2] = {1, 1};      // view chunks of the backprojector per tile family (X, Y)
   // step size cached per factor by the last power iteration on this plan:
@@ -155,6 +159,7 @@ struct ms2g_plan {
   float* w_etaf = nullptr;             // fp32 eta per stage [64]
   double* w_pw = nullptr;              // power-iteration scalars (dot, inv_norm)
   unsigned* w_ticket = nullptr;        // last-block ticket of k_reduce_power (0 between launches)
+  unsigned* w_rmaxv = nullptr;         // [batch][V_r] max |r| per view (float bits) of the last forward(s)
   int* w_flag = nullptr;               // first non-finite global iteration (INT_MAX = none)
   // ad-hoc host subsets: a ring of kSelRing (pinned host, device) list slots;
   // slot k is reused only after the event recorded behind its last consumer
@@ -218,6 +223,7 @@ struct ms2g_plan {
     double* w_red = nullptr;
     double* w_pw = nullptr;
     unsigned* w_ticket = nullptr;
+    unsigned* w_rmaxv = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
   };
@@ -402,9 +408,12 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
 // fused epilogues of the backprojection (projector.cu)
 int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, float c, const float* y,
                           const float* eta_dev, float* z, int s, cudaStream_t st);
+// per-view max |sino| (float bits) into p->w_rmaxv, for a backprojection of a
+// sinogram that did not come from launch_forward (the fixed-point scale)
+int launch_view_absmax(ms2g_plan* p, const float* sino, int n_sel, int batch, cudaStream_t s);
 int launch_reduce_power(ms2g_plan* p, const float* part, int nplanes, size_t np, float* w_out, const float* v,
                         double* red, int red_blocks, unsigned* ticket, double* pw, double* L_out, double* eta_out,
-                        float* etaf_out, cudaStream_t st);
+                        float* etaf_out, cudaStream_t st, int tile_planes = 0);
 void bp_launch_chunks(const ms2g_plan* p, const FactorTables& f, int n_sel, int* ch);
 
 // ---- peer-memory allreduce (peer_reduce.cu, NEXT-3) ----

@@ -161,6 +161,51 @@ static int check_grid_ties(const ms2g_geom_desc& d, double pitch, const int32_t*
   return MS2G_OK;
 }
 
+// Scale bounds of the fixed-point adjoint (projector.cu, k_backward): per
+// (tile family, view), an upper bound of the weight one pixel receives from
+// the view's rays.  Within a run of one ray class the rays do not cross
+// inside the grid and, in a column, ray t covers the minor interval
+// [F_t(c), F_t(c) + S_t] (length S_t <= 1, in pixels) with weight Lc_t times
+// the covered fraction: a pixel row [rho, rho + 1) meets at most
+// (1 + S_max) / delta_min + 1 of them (delta_min = the smallest gap between
+// neighbouring rays, at c = 0 or c = n_c since F is linear in c), each
+// giving at most Lc_max.  Runs of a family add up.
+static int plan_bp_bounds(FactorTables& f, const std::vector<RayEntry>& rays, const std::vector<ViewEntry>& views,
+                          int V_r, int B, int nc) {
+  std::vector<float> w(2 * (size_t)V_r, 0.f);
+  double lcm = 0.0;
+  for (int v = 0; v < V_r; ++v) {
+    const ViewEntry& ve = views[v];
+    for (int sg = 0; sg < ve.nseg; ++sg) {
+      const int fam = (ve.seg_cls[sg] & kMajorY) ? 1 : 0;
+      double lmax = 0.0, smax = 0.0, dmin = 1e300;
+      int cnt = 0, prev = -1;
+      for (int t = ve.seg_t[sg]; t < ve.seg_t[sg + 1]; ++t) {
+        const RayEntry& R = rays[(size_t)v * B + t];
+        if (R.c_lo >= R.c_hi) continue;          // misses the grid
+        ++cnt;
+        lmax = std::max(lmax, (double)R.Lc);
+        smax = std::max(smax, (double)R.S / kFix);
+        if (prev >= 0) {
+          const RayEntry& Q = rays[(size_t)v * B + prev];
+          const double d0 = std::fabs((double)(R.F0 - Q.F0)) / kFix;
+          const double d1 = std::fabs((double)(R.F0 - Q.F0) + (double)nc * ((double)R.S - (double)Q.S)) / kFix;
+          dmin = std::min(dmin, std::min(d0, d1));
+        }
+        prev = t;
+      }
+      if (!cnt) continue;
+      const double count = cnt == 1 ? 1.0 : std::min((double)cnt, (1.0 + smax) / std::max(dmin, 1e-6) + 1.0);
+      w[(size_t)fam * V_r + v] += (float)(lmax * count * 1.001 + 1e-30);
+      lcm = std::max(lcm, lmax);
+    }
+  }
+  f.lc_max = (float)(lcm * 1.001);
+  MS2G_CUDA(cudaMalloc(&f.d_bpw, sizeof(float) * w.size()));
+  MS2G_CUDA(cudaMemcpy(f.d_bpw, w.data(), sizeof(float) * w.size(), cudaMemcpyHostToDevice));
+  return MS2G_OK;
+}
+
 // Geometry plan: per-view and
 // per-ray constants computed in fp64 on the host, rounded once.
 static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
@@ -251,6 +296,7 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     MS2G_CUDA(cudaMalloc(&f.d_rays_bp, sizeof(RayBp) * bp.size()));
     MS2G_CUDA(cudaMemcpy(f.d_rays_bp, bp.data(), sizeof(RayBp) * bp.size(), cudaMemcpyHostToDevice));
   }
+  MS2G_TRY(plan_bp_bounds(f, rays, views, V_r, B, nc));
   MS2G_CUDA(cudaMemcpy(f.d_views, views.data(), sizeof(ViewEntry) * views.size(), cudaMemcpyHostToDevice));
   MS2G_TRY(build_bicubic_tables(f, d.n));
   MS2G_CUDA(cudaMalloc(&f.d_Lcache, 3 * sizeof(double)));
@@ -344,6 +390,7 @@ static void free_plan(ms2g_plan* p) {
   for (auto& f : p->ft) {
     cudaFree(f.d_rays);
     cudaFree(f.d_rays_bp);
+    cudaFree(f.d_bpw);
     cudaFree(f.d_views);
     cudaFree(f.d_bpr);
     cudaFree(f.d_bp_order);
@@ -364,6 +411,7 @@ static void free_plan(ms2g_plan* p) {
   cudaFree(p->w_scal);
   cudaFree(p->w_pw);
   cudaFree(p->w_ticket);
+  cudaFree(p->w_rmaxv);
   cudaFree(p->tvws.flags);
   cudaFree(p->tvws.gen_ticket);
   cudaFree(p->tvws.err);
@@ -397,6 +445,7 @@ static void free_plan(ms2g_plan* p) {
     cudaFree(br.w_red);
     cudaFree(br.w_pw);
     cudaFree(br.w_ticket);
+    cudaFree(br.w_rmaxv);
     if (br.stream) cudaStreamDestroy(br.stream);
     if (br.done) cudaEventDestroy(br.done);
   }
@@ -573,7 +622,9 @@ static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double*
   for (int k = 0; k < iters; ++k) {
     MS2G_TRY(launch_forward(p, f, nullptr, p->w_res, nullptr, p->V_r, 1, st));
     const float* part = p->w_G;
-    int npl = 1;
+    int npl = 1, ch[2];
+    bp_launch_chunks(p, f, p->V_r, ch);
+    const int npl_bp = ch[0] + ch[1];   // the backprojection's plane count (tiling of the reduction)
     if (fused_epilogue(p)) {
       MS2G_TRY(launch_backward(p, f, p->w_res, nullptr, 1.f, 0, nullptr, p->V_r, 1, st, 2, nullptr, &npl));
       part = p->w_part;
@@ -584,7 +635,7 @@ static int enqueue_power(ms2g_plan* p, const FactorTables& f, int iters, double*
     double* cache = f.d_Lcache;
     MS2G_TRY(launch_reduce_power(p, part, npl, np, p->w_G, p->w_v, p->w_red, p->red_blocks, p->w_ticket, p->w_pw,
                                  last ? cache : nullptr, last ? cache + 1 : nullptr,
-                                 last ? reinterpret_cast<float*>(cache + 2) : nullptr, st));
+                                 last ? reinterpret_cast<float*>(cache + 2) : nullptr, st, npl_bp));
     if (!last) MS2G_TRY(launch_pair_prep(p, f.nc, 1, p->w_G, st, 1, p->w_pw + 1, p->w_v));   // v = w / ||w||
   }
   // the last Rayleigh quotient went to the factor's cache (reused by solves
@@ -778,6 +829,8 @@ static int ensure_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd) {
     MS2G_CUDA(cudaMalloc(&br.w_pw, sizeof(double) * 8));
     MS2G_CUDA(cudaMalloc(&br.w_ticket, sizeof(unsigned)));
     MS2G_CUDA(cudaMemset(br.w_ticket, 0, sizeof(unsigned)));
+    MS2G_CUDA(cudaMalloc(&br.w_rmaxv, sizeof(unsigned) * (size_t)p->V_r));
+    MS2G_CUDA(cudaMemset(br.w_rmaxv, 0, sizeof(unsigned) * (size_t)p->V_r));
     MS2G_CUDA(cudaStreamCreateWithFlags(&br.stream, cudaStreamNonBlocking));
     MS2G_CUDA(cudaEventCreateWithFlags(&br.done, cudaEventDisableTiming));
     p->pbr.push_back(br);
@@ -808,6 +861,7 @@ static int enqueue_power_branches(ms2g_plan* p, const ms2g_solve_desc* sd, cudaS
     shadow.w_red = br.w_red;
     shadow.w_pw = br.w_pw;
     shadow.w_ticket = br.w_ticket;
+    shadow.w_rmaxv = br.w_rmaxv;
     const FactorTables* f = find_factor(p, br.factor);
     MS2G_TRY(enqueue_power(&shadow, *f, sd->power_iters, p->w_scal + first, p->w_scal + 64 + first,
                            p->w_etaf + first, br.stream));
@@ -1142,6 +1196,8 @@ int ms2g_plan_geometry(const ms2g_geom_desc* desc, const int32_t* factors, int32
   if (e == cudaSuccess) e = cudaMalloc(&p->w_pw, sizeof(double) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&p->w_ticket, sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemset(p->w_ticket, 0, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMalloc(&p->w_rmaxv, sizeof(unsigned) * (size_t)p->V_r * bt);
+  if (e == cudaSuccess) e = cudaMemset(p->w_rmaxv, 0, sizeof(unsigned) * (size_t)p->V_r * bt);
   {  // persistent TV-prox workspace: one CTA per SM at most, rows of the full-resolution grid
     int optin = 0;
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1384,6 +1440,7 @@ static int do_forward(ms2g_plan* p, const FactorTables* f, const float* x, const
 
 static int do_backward(ms2g_plan* p, const FactorTables* f, const float* sino, float* img, float scale,
                        int accumulate, int do_allreduce, const Sel& s, cudaStream_t st) {
+  MS2G_TRY(launch_view_absmax(p, sino, s.n_sel, p->d.batch, st));   // a caller's sinogram: its per-view bounds
   MS2G_TRY(launch_backward(p, *f, sino, img, scale, accumulate, s.d_sel, s.n_sel, p->d.batch, st, 0, s.bord));
   if (do_allreduce) MS2G_TRY(allreduce(p, img, (size_t)f->nc * f->nc * p->d.batch, st));
   return MS2G_OK;

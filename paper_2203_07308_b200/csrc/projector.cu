@@ -81,7 +81,7 @@ __device__ __forceinline__ float pair_src(const float* __restrict__ xb, int k, i
 // element (line, pos) holding NB consecutive pairs.
 __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pairs, size_t pair_stride, int nc,
                             int s, const double* __restrict__ scale_dev, float* __restrict__ v_out, int class_mask,
-                            int il) {
+                            int il, unsigned* __restrict__ rmaxv, int V_r) {
   // T[r][c] = v[O0-2+r][L0+c] (column pairs, classes 0/2); with s > 1 also
   // T2[r][c] = v[L0+r][O0-2+c] (row pairs, classes 1/3), so each s x s mean
   // is formed once per tile (s = 1 reads the row pairs directly)
@@ -89,6 +89,8 @@ __global__ void k_pair_prep(const float* __restrict__ x, float2* __restrict__ pa
   pdl_wait();
   pdl_release();
   const int bz = blockIdx.z;
+  if (rmaxv && blockIdx.x == 0 && blockIdx.y == 0)   // the next forward's per-view maxima start at 0
+    for (int i = threadIdx.y * 32 + threadIdx.x; i < V_r; i += 256) rmaxv[(size_t)bz * V_r + i] = 0u;
   const int nsrc = nc * s;
   const float* xb = x + (size_t)bz * nsrc * nsrc;
   const float inv_s2 = 1.0f / (float)(s * s);
@@ -150,7 +152,7 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
   static const bool il_on = getenv("MS2G_FWD_INTERLEAVE") != nullptr;   // experiment switch
   const int il = il_on ? batch_group(batch) : 1;
   MS2G_CUDA(launch_k(k_pair_prep, grid, block, 0, s, x, p->w_pair, p->pair_stride, nc, factor, scale_dev, v_out,
-                     p->class_mask, il));
+                     p->class_mask, il, p->w_rmaxv, p->V_r));
   return check_launch("k_pair_prep");
 }
 
@@ -179,6 +181,14 @@ constexpr int kFwdWarps = MS2G_FWD_WARPS;
 #endif
 constexpr int kFwdUnroll = MS2G_FWD_UNROLL;
 
+
+// max |r| of the warp's rays into the view's word (float bits: for r >= 0 the
+// unsigned order is the float order, NaN above +inf) -- the bound of the
+// fixed-point adjoint's scale.  The words are zeroed by the pair prep.
+__device__ __forceinline__ void fwd_view_max(unsigned* rmaxv, size_t idx, bool vk, bool valid, float r) {
+  const unsigned bits = __reduce_max_sync(0xffffffffu, valid ? __float_as_uint(fabsf(r)) : 0u);
+  if (rmaxv && vk && (threadIdx.x & 31) == 0) atomicMax(rmaxv + idx, bits);
+}
 
 // (pl, pu) = pair element e of a pair image (one 8-byte non-coherent load)
 __device__ __forceinline__ void fwd_ld_pair(const float2* base, unsigned e, float& pl, float& pu) {
@@ -218,7 +228,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out,
-                                                 const int* __restrict__ order, int allow_fast) {
+                                                 const int* __restrict__ order, int allow_fast,
+                                                 unsigned* __restrict__ rmaxv) {
   constexpr int VPB = kFwdWarps / SPLIT;             // views per block
   constexpr int SPW = SEG / SPLIT;                   // segments per warp
 
@@ -320,19 +331,23 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __re
     for (int i = 0; i < NB; ++i) red[vw][sg][i][lane] = make_float2(sa[i], sb[i]);
   }
   __syncthreads();
-  if (q != 0 || !valid) return;
+  if (q != 0) return;
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
-    float a = 0.f, b = 0.f;
+    float r = 0.f;
+    if (valid) {
+      float a = 0.f, b = 0.f;
 #pragma unroll
-    for (int sg = 0; sg < SEG; ++sg) {
-      const float2 v = red[vw][sg][i][lane];
-      a += v.x;
-      b += v.y;
+      for (int sg = 0; sg < SEG; ++sg) {
+        const float2 v = red[vw][sg][i][lane];
+        a += v.x;
+        b += v.y;
+      }
+      r = fmaf(Lc, a, Ly32 * b);
+      if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
+      out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
     }
-    float r = fmaf(Lc, a, Ly32 * b);
-    if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
-    out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
+    fwd_view_max(rmaxv, (size_t)(bz0 + i) * V_r + k, vk, valid, r);
   }
 }
 
@@ -346,7 +361,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
                                                                  const int* __restrict__ sel, int n_sel,
                                                                  const float2* __restrict__ pairs, size_t pair_stride,
                                                                  int nc, const float* __restrict__ bsino,
-                                                                 float* __restrict__ out) {
+                                                                 float* __restrict__ out, unsigned* __restrict__ rmaxv) {
   constexpr int SPLIT = 2, VPB = kFwdWarps / SPLIT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = warp % SPLIT;
@@ -428,19 +443,23 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
 #pragma unroll
   for (int i = 0; i < NB; ++i) red[warp][i][lane] = make_float2(sa[i], sb[i]);
   __syncthreads();
-  if (q != 0 || !valid) return;
+  if (q != 0) return;
 #pragma unroll
   for (int i = 0; i < NB; ++i) {
-    float a = 0.f, b = 0.f;
+    float r = 0.f;
+    if (valid) {
+      float a = 0.f, b = 0.f;
 #pragma unroll
-    for (int j = 0; j < SPLIT; ++j) {
-      const float2 v = red[warp + j][i][lane];
-      a += v.x;
-      b += v.y;
+      for (int j = 0; j < SPLIT; ++j) {
+        const float2 v = red[warp + j][i][lane];
+        a += v.x;
+        b += v.y;
+      }
+      r = fmaf(Lc, a, Ly32 * b);
+      if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
+      out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
     }
-    float r = fmaf(Lc, a, Ly32 * b);
-    if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
-    out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
+    fwd_view_max(rmaxv, (size_t)(bz0 + i) * V_r + k, vk, valid, r);
   }
 }
 
@@ -456,10 +475,10 @@ static void fwd_launch_batch(int n_sel, int batch, cudaStream_t s, ms2g_plan* p,
   static const bool il_on = getenv("MS2G_FWD_INTERLEAVE") != nullptr;
   if (!il_on)
     (void)launch_k(k_forward_batch<NB, false>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
-                   (const float2*)p->w_pair, p->pair_stride, f.nc, b, out);
+                   (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, p->w_rmaxv);
   else
     (void)launch_k(k_forward_batch<NB, true>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
-                   (const float2*)p->w_pair, p->pair_stride, f.nc, b, out);
+                   (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, p->w_rmaxv);
 }
 
 template <int NB, int SPLIT, int SEG>
@@ -476,7 +495,7 @@ static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, cons
   // experiment / test switch: every warp on the clamped path (bitwise equal)
   static const int allow_fast = getenv("MS2G_FWD_NO_FAST") ? 0 : 1;
   (void)launch_k(k_forward<NB, SPLIT, SEG>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
-                 (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, order, allow_fast);
+                 (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, order, allow_fast, p->w_rmaxv);
 }
 
 // views per block of the single-image forward kernel for a launch of n_sel
@@ -627,7 +646,7 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
 // The adjoint's steps over one round of <= 32 ray records (one broadcast
 // LDS.128 each): per step the lane's end coordinate, the two weights and two
 // shared read-modify-writes, the lower row at a compile-time offset.
-template <bool MIR, int H>
+template <bool MIR, int H, bool FX = false>
 __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, int nrays, int lane, unsigned sbase,
                                          unsigned acc0, unsigned acc1) {
   constexpr int kStride = MIR ? -4 * kBT : 4 * kBT;   // bytes per row step of u
@@ -646,6 +665,12 @@ __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, int nray
     const float mu = (float)m, ml = (float)(S - m);
     const unsigned adu = sbase + min(u, (unsigned)(H + 2)) * (unsigned)kStride;
     MS2G_DASSERT(adu >= acc0 && adu < acc1 && adu - kStride >= acc0 && adu - kStride < acc1);
+    if (FX) {
+      const int up = __float_as_int(fmaf(mu, a.w, 12582912.f)) - 0x4B400000;
+      const int dn = __float_as_int(fmaf(ml, a.w, 12582912.f)) - 0x4B400000;
+      if (MIR) asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.add.u32 [%0+128], %2;" :: "r"(adu), "r"(up), "r"(dn) : "memory");
+      else asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.add.u32 [%0+-128], %2;" :: "r"(adu), "r"(up), "r"(dn) : "memory");
+    } else
     if (MIR)
       asm volatile("{\n\t.reg .f32 c0, c1;\n\t"
                    "ld.shared.f32 c0, [%0];\n\t"
@@ -668,13 +693,15 @@ __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, int nray
   }
 }
 
-template <int H>
+template <int H, bool FX>
 __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(const RayBp* __restrict__ rays,
                                                           const int4* __restrict__ ranges, int V_r, int B,
                                                           const int* __restrict__ sel, int n_sel,
                                                           const float* __restrict__ sino, float* __restrict__ part,
                                                           int nc, int tmaj, int per, int chx, int vpcx, int vpcy,
-                                                          const int* __restrict__ order) {
+                                                          const int* __restrict__ order,
+                                                          const float* __restrict__ bpw, float lc_max,
+                                                          const unsigned* __restrict__ rmaxv) {
   extern __shared__ float4 dyn_smem[];
   float* acc = reinterpret_cast<float*>(dyn_smem);   // kAccRows x kBT (dynamic: may exceed 48 KB)
   constexpr int kBH = H, kWinR = BpShape<H>::kWinR, kAccRows = BpShape<H>::kAccRows;
@@ -738,6 +765,45 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     return true;
   };
 
+  // Fixed-point accumulation (FX): each warp window accumulates integers
+  // round(w r sigma) with the native shared-memory integer add (ATOMS.ADD:
+  // one instead of two shared wavefronts per update, and order-independent).
+  // sigma = 2^e per warp, the largest power of two with
+  //   sum over the warp's views of W_v * max|r|  < 2^31  (no overflow: W_v
+  //     bounds the weight a pixel receives from one view, plan_bp_bounds)
+  //   Lc_max * max|r|                            < 2^22  (every contribution
+  //     fits the FFMA-against-1.5*2^23 rounding trick)
+  // from the per-view bounds of the warp's views.  A non-finite residual
+  // makes the warp's window NaN (the solve's divergence check).
+  __shared__ float s_inv[kBW];
+  __shared__ int s_bad[kBW];
+  float sig = 1.f;
+  if (FX) {
+    // the warp's views are kb + warp + kBW j: W and max |r| per view (the
+    // forward's epilogue wrote rmaxv; a caller's sinogram got launch_view_absmax)
+    unsigned rbits = 0;
+    float wsum = 0.f;
+    for (int kk = kb + warp + kBW * lane; kk < ke; kk += 32 * kBW) {
+      const int gg = sel ? __ldg(sel + kk) : kk;
+      wsum += __ldg(bpw + (size_t)fam * V_r + gg);
+      rbits = max(rbits, __ldcg(rmaxv + (size_t)bz * V_r + kk));
+    }
+    rbits = __reduce_max_sync(0xffffffffu, rbits);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    int e = 0;
+    const bool bad = rbits >= 0x7f800000u;   // inf / nan
+    if (!bad && rbits != 0u) {
+      const double rm = (double)__uint_as_float(rbits);
+      const double t = fmin(2.1e9 / ((double)wsum * rm), 4.19e6 / ((double)lc_max * rm));   // < 2^31, < 2^22
+      e = min(126, max(-126, ilogb(t)));
+    }
+    sig = ldexpf(1.f, e);      // a power of two: the conversion back is exact
+    if (lane == 0) {
+      s_inv[warp] = ldexpf(1.f, -e);
+      s_bad[warp] = bad ? 1 : 0;
+    }
+  }
   run = 0; nr = 0; te = -1; tb = 0;
   bool have = next_round();
   RayBp Rn;
@@ -759,7 +825,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
       const int mb = mir ? nc - m0 - kBH : m0;
       const long long Et = Rn.F0 + (long long)c0 * (long long)Rn.S + (long long)Rn.S - ((long long)(mb - 1) << 32);
       st4[warp][lane] = make_float4(__uint_as_float((unsigned)Et), __uint_as_float((unsigned)(Et >> 32)),
-                                    __uint_as_float(Rn.S), Rn.Ly32 * rn);
+                                    __uint_as_float(Rn.S), FX ? Rn.Ly32 * (rn * sig) : Rn.Ly32 * rn);
     }
     __syncwarp();
     // fetch the next round while this one is processed
@@ -774,8 +840,8 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     //   plain:  phys row = u - 1      (sbase at row -1)
     //   mirror: phys row = kBH - u    (sbase at row kBH, negative stride)
     const int nrays = min(32, cte - ctb + 1);
-    if (mir) bp_steps<true, kBH>(st4[warp], nrays, lane, tbase + 4u * kBT * kBH, acc0, acc1);
-    else bp_steps<false, kBH>(st4[warp], nrays, lane, tbase - 4u * kBT, acc0, acc1);
+    if (mir) bp_steps<true, kBH, FX>(st4[warp], nrays, lane, tbase + 4u * kBT * kBH, acc0, acc1);
+    else bp_steps<false, kBH, FX>(st4[warp], nrays, lane, tbase - 4u * kBT, acc0, acc1);
     __syncwarp();
   }
   __syncthreads();
@@ -787,7 +853,11 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     const int idx = threadIdx.x + i * 32 * kBW;   // row idx / 32, lane idx % 32
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < kBW; ++w) s += acc[(kPadR + w * kWinR) * kBT + idx];
+    for (int w = 0; w < kBW; ++w) {
+      const float v = acc[(kPadR + w * kWinR) * kBT + idx];
+      if (FX) s += s_bad[w] ? __int_as_float(0x7fc00000) : (float)__float_as_int(v) * s_inv[w];
+      else s += v;
+    }
     sum[i] = s;
   }
   const size_t np = (size_t)nc * nc;
@@ -1051,12 +1121,40 @@ int launch_reduce_up_step(const float* part, int nplanes, int nc, int batch, flo
   return check_launch("k_reduce_up_step");
 }
 
+// max |sino| of each view (float bits), one block per (view, image): the
+// fixed-point adjoint's scale for a sinogram that did not come from
+// launch_forward (ms2g_back_project)
+__global__ void __launch_bounds__(256) k_view_absmax(const float* __restrict__ sino, int n_sel, int B, int V_r,
+                                                     unsigned* __restrict__ rmaxv) {
+  __shared__ unsigned wm[8];
+  const int k = blockIdx.x, bz = blockIdx.y;
+  const float* row = sino + ((size_t)bz * n_sel + k) * B;
+  unsigned m = 0;
+  for (int t = threadIdx.x; t < B; t += 256) m = max(m, __float_as_uint(fabsf(row[t])));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
+    rmaxv[(size_t)bz * V_r + k] = max(m, wm[0]);
+  }
+}
+
+int launch_view_absmax(ms2g_plan* p, const float* sino, int n_sel, int batch, cudaStream_t s) {
+  if (n_sel <= 0) return MS2G_OK;
+  MS2G_CUDA(launch_k(k_view_absmax, dim3(n_sel, batch), dim3(256), 0, s, sino, n_sel, p->B, p->V_r, p->w_rmaxv));
+  return check_launch("k_view_absmax");
+}
+
 int launch_reduce_power(ms2g_plan* p, const float* part, int nplanes, size_t np, float* w_out, const float* v,
                         double* red, int red_blocks, unsigned* ticket, double* pw, double* L_out, double* eta_out,
-                        float* etaf_out, cudaStream_t st) {
+                        float* etaf_out, cudaStream_t st, int tile_planes) {
   // one pass over nplanes x np floats: as many blocks as the buffer allows
   // (the fixed-order last-block reduction handles any grid size)
-  const int G = plane_groups(np, nplanes);
+  // the plane rule (and with it the tiling, hence the fp64 dot order) of the
+  // backprojection's plane count: an exchange path passes its one summed
+  // plane with the count it came from, so every path gives the same bits
+  const int G = plane_groups(np, std::max(nplanes, tile_planes));
   const int blocks = plane_blocks(np, G, red_blocks);
   MS2G_CUDA(launch_k(k_reduce_power, dim3(blocks), dim3(32, kPlaneGroups), 0, st, part, nplanes, np, w_out, v, red,
                      ticket, pw, L_out, eta_out, etaf_out, G));
@@ -1075,12 +1173,22 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
   MS2G_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_devices.load() & bit)) {
-    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_devices.fetch_or(bit);
   }
-  MS2G_CUDA(launch_k(k_backward<H>, grid, dim3(32 * kBW), smem, s, f.d_rays_bp, (const int4*)f.d_bpr, p->V_r, p->B,
-                     d_sel, n_sel, sino, p->w_part, f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order));
+  // experiment / test switch: the fp32 read-modify-write accumulation
+  static const bool fp32 = getenv("MS2G_BP_FP32") != nullptr;
+  if (fp32)
+    MS2G_CUDA(launch_k(k_backward<H, false>, grid, dim3(32 * kBW), smem, s, f.d_rays_bp, (const int4*)f.d_bpr, p->V_r,
+                       p->B, d_sel, n_sel, sino, p->w_part, f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order,
+                       (const float*)f.d_bpw, f.lc_max, (const unsigned*)p->w_rmaxv));
+  else
+    MS2G_CUDA(launch_k(k_backward<H, true>, grid, dim3(32 * kBW), smem, s, f.d_rays_bp, (const int4*)f.d_bpr, p->V_r,
+                       p->B, d_sel, n_sel, sino, p->w_part, f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order,
+                       (const float*)f.d_bpw, f.lc_max, (const unsigned*)p->w_rmaxv));
   return MS2G_OK;
 }
 

@@ -577,12 +577,37 @@ constexpr int kPadR = 2;
 #define MS2G_BH96_MIN_NC 1024
 #endif
 int bp_height(int nc) { return nc >= MS2G_BH96_MIN_NC ? 96 : 64; }
-template <int H>
+// Warps per block and accumulator windows: the fp32 form needs one window
+// per warp (plain read-modify-writes); the fixed-point form's integer adds
+// are atomic, so at H = 96 two warps share a window -- twice the warps
+// (latency hiding: the step is a chain of dependent integer / FMA
+// operations) in the same shared memory: C4 s=1 1.17 -> 1.13 ms.  At H = 64
+// 8 warps (or 2 windows) measured slower (0.60 against 0.58 ms at C4 s=2).
+#ifndef MS2G_FX96_W
+#define MS2G_FX96_W 8
+#endif
+#ifndef MS2G_FX96_WIN
+#define MS2G_FX96_WIN 4
+#endif
+#ifndef MS2G_FX64_W
+#define MS2G_FX64_W 4
+#endif
+#ifndef MS2G_FX64_WIN
+#define MS2G_FX64_WIN 4
+#endif
+template <bool FX, int H>
+struct BpWarps {
+  static constexpr int kW = FX ? (H >= 96 ? MS2G_FX96_W : MS2G_FX64_W) : kBW;        // warps per block
+  static constexpr int kWin = FX ? (H >= 96 ? MS2G_FX96_WIN : MS2G_FX64_WIN) : kBW;  // accumulator windows
+};
+template <int H, bool FX = false>
 struct BpShape {
-  static constexpr int kWinR = H + kPadR;                // rows per warp window (+ shared pads)
-  static constexpr int kAccRows = kPadR + kBW * kWinR;
+  static constexpr int kWinR = H + kPadR;                // rows per window (+ shared pads)
+  static constexpr int kAccRows = kPadR + BpWarps<FX, H>::kWin * kWinR;
   static constexpr size_t kSmem = sizeof(float) * kAccRows * kBT;
-  static constexpr int kMinBlocks = (H <= 64 ? 24 : 16) / kBW;   // resident warps: 24 (H = 64) / 16 (H = 96)
+  // resident blocks per SM: 24 (H = 64) / 16 (H = 96) warps of the fp32 form; the
+  // fixed-point form keeps the block count (shared memory) at twice the warps
+  static constexpr int kMinBlocks = (FX && H >= 96) ? 32 / BpWarps<FX, H>::kW : (H <= 64 ? 24 : 16) / kBW;
 };
 
 struct BpTiling {
@@ -694,7 +719,7 @@ __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, int nray
 }
 
 template <int H, bool FX>
-__global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(const RayBp* __restrict__ rays,
+__global__ void __launch_bounds__(32 * BpWarps<FX, H>::kW, BpShape<H, FX>::kMinBlocks) k_backward(const RayBp* __restrict__ rays,
                                                           const int4* __restrict__ ranges, int V_r, int B,
                                                           const int* __restrict__ sel, int n_sel,
                                                           const float* __restrict__ sino, float* __restrict__ part,
@@ -704,8 +729,9 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
                                                           const unsigned* __restrict__ rmaxv) {
   extern __shared__ float4 dyn_smem[];
   float* acc = reinterpret_cast<float*>(dyn_smem);   // kAccRows x kBT (dynamic: may exceed 48 KB)
-  constexpr int kBH = H, kWinR = BpShape<H>::kWinR, kAccRows = BpShape<H>::kAccRows;
-  __shared__ float4 st4[kBW][33];   // entry 32 is a pipeline pad
+  constexpr int kBH = H, kWinR = BpShape<H, FX>::kWinR, kAccRows = BpShape<H, FX>::kAccRows;
+  constexpr int NW = BpWarps<FX, H>::kW, NWIN = BpWarps<FX, H>::kWin;   // warps, windows (warp w -> window w % NWIN)
+  __shared__ float4 st4[NW][33];   // entry 32 is a pipeline pad
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // blockIdx.x = (family, view chunk, tile): X-family blocks first
   const int bx = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x, bz = blockIdx.z;
@@ -717,8 +743,9 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   const int vpc = fam ? vpcy : vpcx;
   const int plane = fam ? chx + chunk : chunk;
   const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * kBH;   // major / minor origin
-  float* T = acc + (kPadR + warp * kWinR) * kBT;
-  for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * kBW) acc[i] = 0.f;
+  const int win = warp % NWIN;
+  float* T = acc + (kPadR + win * kWinR) * kBT;
+  for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * NW) acc[i] = 0.f;
   __syncthreads();
   pdl_wait();      // the residual sinogram comes from the forward
   pdl_release();
@@ -727,7 +754,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   const int4* trange = ranges + (size_t)tile * V_r;
 
   // ---- round iterator: (view k, run, [tb, te]) of this warp ----
-  int vbase = kb + warp - 32 * kBW;     // first view of the current 32-view batch
+  int vbase = kb + warp - 32 * NW;      // first view of the current 32-view batch
   int g_lane = 0;                       // rank-local view held by this lane for the batch
   int4 rr_lane = make_int4(0, 0, 0, 0); // its range record
   int j = 31;                           // index of the current view within the batch
@@ -740,14 +767,14 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
       if (run >= nr) {
         ++j;
         if (j == 32) {                    // load the next batch of 32 views (lane j <-> view)
-          vbase += 32 * kBW;
+          vbase += 32 * NW;
           if (vbase >= ke) return false;
-          const int kk = vbase + lane * kBW;
+          const int kk = vbase + lane * NW;
           g_lane = (kk < ke) ? (sel ? __ldg(sel + kk) : kk) : 0;
           rr_lane = (kk < ke) ? __ldg(trange + g_lane) : make_int4(0, 0, 0, 0);
           j = 0;
         }
-        k = vbase + j * kBW;
+        k = vbase + j * NW;
         if (k >= ke) return false;
         g = __shfl_sync(0xffffffffu, g_lane, j);
         const int rx = __shfl_sync(0xffffffffu, rr_lane.x, j);
@@ -775,15 +802,18 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   //     fits the FFMA-against-1.5*2^23 rounding trick)
   // from the per-view bounds of the warp's views.  A non-finite residual
   // makes the warp's window NaN (the solve's divergence check).
-  __shared__ float s_inv[kBW];
-  __shared__ int s_bad[kBW];
+  __shared__ float s_inv[NWIN];
+  __shared__ int s_bad[NWIN];
+  __shared__ float s_w[NW];
+  __shared__ unsigned s_r[NW];
   float sig = 1.f;
   if (FX) {
-    // the warp's views are kb + warp + kBW j: W and max |r| per view (the
-    // forward's epilogue wrote rmaxv; a caller's sinogram got launch_view_absmax)
+    // the warp's views are kb + warp + NW j: W and max |r| per view (the
+    // forward's epilogue wrote rmaxv; a caller's sinogram got launch_view_absmax),
+    // combined over the warps sharing the window
     unsigned rbits = 0;
     float wsum = 0.f;
-    for (int kk = kb + warp + kBW * lane; kk < ke; kk += 32 * kBW) {
+    for (int kk = kb + warp + NW * lane; kk < ke; kk += 32 * NW) {
       const int gg = sel ? __ldg(sel + kk) : kk;
       wsum += __ldg(bpw + (size_t)fam * V_r + gg);
       rbits = max(rbits, __ldcg(rmaxv + (size_t)bz * V_r + kk));
@@ -791,6 +821,17 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     rbits = __reduce_max_sync(0xffffffffu, rbits);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if (lane == 0) {
+      s_w[warp] = wsum;
+      s_r[warp] = rbits;
+    }
+    __syncthreads();
+    wsum = 0.f;
+    rbits = 0;
+    for (int w = win; w < NW; w += NWIN) {     // fixed order
+      wsum += s_w[w];
+      rbits = max(rbits, s_r[w]);
+    }
     int e = 0;
     const bool bad = rbits >= 0x7f800000u;   // inf / nan
     if (!bad && rbits != 0u) {
@@ -799,9 +840,9 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
       e = min(126, max(-126, ilogb(t)));
     }
     sig = ldexpf(1.f, e);      // a power of two: the conversion back is exact
-    if (lane == 0) {
-      s_inv[warp] = ldexpf(1.f, -e);
-      s_bad[warp] = bad ? 1 : 0;
+    if (lane == 0 && warp < NWIN) {
+      s_inv[win] = ldexpf(1.f, -e);
+      s_bad[win] = bad ? 1 : 0;
     }
   }
   run = 0; nr = 0; te = -1; tb = 0;
@@ -846,14 +887,14 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   }
   __syncthreads();
   // Sum the warp windows in fixed order: element (row l, lane) of the tile.
-  constexpr int kPer = kBT * kBH / (32 * kBW);
+  constexpr int kPer = kBT * kBH / (32 * NW);
   float sum[kPer];
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
-    const int idx = threadIdx.x + i * 32 * kBW;   // row idx / 32, lane idx % 32
+    const int idx = threadIdx.x + i * 32 * NW;    // row idx / 32, lane idx % 32
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < kBW; ++w) {
+    for (int w = 0; w < NWIN; ++w) {
       const float v = acc[(kPadR + w * kWinR) * kBT + idx];
       if (FX) s += s_bad[w] ? __int_as_float(0x7fc00000) : (float)__float_as_int(v) * s_inv[w];
       else s += v;
@@ -867,7 +908,7 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
   if (!fam) {       // X-tile: row l = y - m0, lane = x - c0 (coalesced)
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int idx = threadIdx.x + i * 32 * kBW;
+      const int idx = threadIdx.x + i * 32 * NW;
       const int yy = m0 + (idx >> 5), xx = c0 + (idx & 31);
       if (yy < nc && xx < nc) dst[(size_t)yy * nc + xx] = sum[i];
     }
@@ -875,13 +916,13 @@ __global__ void __launch_bounds__(32 * kBW, BpShape<H>::kMinBlocks) k_backward(c
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int idx = threadIdx.x + i * 32 * kBW;
+      const int idx = threadIdx.x + i * 32 * NW;
       acc[(idx & 31) * (kBH + 1) + (idx >> 5)] = sum[i];
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const int idx = threadIdx.x + i * 32 * kBW;   // y = idx / kBH, x = idx % kBH (tile-relative)
+      const int idx = threadIdx.x + i * 32 * NW;    // y = idx / kBH, x = idx % kBH (tile-relative)
       const int ly = idx / kBH, lx = idx % kBH;
       const int yy = c0 + ly, xx = m0 + lx;
       if (yy < nc && xx < nc) dst[(size_t)yy * nc + xx] = acc[ly * (kBH + 1) + lx];
@@ -1165,7 +1206,7 @@ template <int H>
 static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTables& f, const float* sino,
                       const int* d_sel, int n_sel, const int* ch, const int* vpc, const BpTiling& t,
                       const int* order) {
-  constexpr size_t smem = BpShape<H>::kSmem;
+  constexpr size_t smem = BpShape<H, false>::kSmem, smem_fx = BpShape<H, true>::kSmem;
   // several blocks of 36-51 KB per SM need the maximum shared-memory carveout;
   // function attributes are per device, so remember which devices have them
   static std::atomic<uint64_t> attr_devices{0};
@@ -1173,7 +1214,7 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
   MS2G_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_devices.load() & bit)) {
-    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fx));
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MS2G_CUDA(cudaFuncSetAttribute(k_backward<H, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -1186,7 +1227,8 @@ static int bwd_launch(dim3 grid, cudaStream_t s, ms2g_plan* p, const FactorTable
                        p->B, d_sel, n_sel, sino, p->w_part, f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order,
                        (const float*)f.d_bpw, f.lc_max, (const unsigned*)p->w_rmaxv));
   else
-    MS2G_CUDA(launch_k(k_backward<H, true>, grid, dim3(32 * kBW), smem, s, f.d_rays_bp, (const int4*)f.d_bpr, p->V_r,
+    MS2G_CUDA(launch_k(k_backward<H, true>, grid, dim3(32 * BpWarps<true, H>::kW), smem_fx, s, f.d_rays_bp,
+                       (const int4*)f.d_bpr, p->V_r,
                        p->B, d_sel, n_sel, sino, p->w_part, f.nc, t.maj, t.per, ch[0], vpc[0], vpc[1], order,
                        (const float*)f.d_bpw, f.lc_max, (const unsigned*)p->w_rmaxv));
   return MS2G_OK;

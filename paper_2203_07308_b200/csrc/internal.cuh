@@ -88,6 +88,7 @@ struct FactorTables {
   float lc_max = 0.f;
   ViewEntry* d_views = nullptr;   // [V_r]
   int bp_chunks[2] = {1, 1};      // view chunks of the backprojector per tile family (X, Y)
+  int bp_h = 64;                  // minor extent of the adjoint's tiles (bp_height)
   // step size cached per factor by the last power iteration on this plan:
   // d_Lcache = {L, eta} (double), then eta as float; L_iters = its iteration
   // count as enqueued (0 = none yet).  L depends on the geometry only.
@@ -396,7 +397,8 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
 // built for this view list (subset_orders in ms2g_api.cu); NULL = grid order
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s, const int* order_sel = nullptr);
-int bp_tile_count(int nc);   // adjoint tiles (both families) of an n_c grid
+int bp_tile_count(int nc, int H);   // adjoint tiles (both families) of an n_c grid, minor extent H
+int bp_height(int nc, int V_r);      // that minor extent for a plan's factor
 int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch);
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
 // publish: 0 = img = scale A_s^T sino (+ img), 1 = write scale * A_s^T sino

@@ -91,7 +91,7 @@ static int upload_order(const std::vector<long long>& cost, int** out) {
 
 static int upload_bp_order(const ms2g_plan* p, const FactorTables& f, const std::vector<int>& views, int** out) {
   const int n_sel = (int)views.size(), V_r = p->V_r;
-  const int per_t = bp_tile_count(f.nc) / 2;
+  const int per_t = bp_tile_count(f.nc, f.bp_h) / 2;
   int ch[2];
   bp_launch_chunks(p, f, n_sel, ch);
   const int n_items = per_t * (ch[0] + ch[1]);
@@ -303,7 +303,8 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   MS2G_CUDA(cudaMemset(f.d_Lcache, 0, 3 * sizeof(double)));
   {  // adjoint tile/view bin ranges (geometry only, once per plan)
     int* d_err = nullptr;
-    MS2G_CUDA(cudaMalloc(&f.d_bpr, sizeof(int4) * (size_t)bp_tile_count(nc) * V_r));
+    f.bp_h = bp_height(nc, V_r);
+    MS2G_CUDA(cudaMalloc(&f.d_bpr, sizeof(int4) * (size_t)bp_tile_count(nc, f.bp_h) * V_r));
     MS2G_CUDA(cudaMalloc(&d_err, sizeof(int)));
     MS2G_CUDA(cudaMemset(d_err, 0, sizeof(int)));
     int rc = launch_bp_ranges(f, V_r, B, f.d_bpr, d_err, 0);
@@ -323,7 +324,7 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   // The X- and Y-tile families only see the views with major-x / major-y
   // rays; a contiguous view shard (e.g. 45 degrees at P = 8) is almost all
   // one class, so each family gets view chunks in proportion to its views.
-  const long long tiles = (long long)bp_tile_count(nc) * d.batch;
+  const long long tiles = (long long)bp_tile_count(nc, f.bp_h) * d.batch;
   const long long per = tiles / 2;
   const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : 24;
   const long long target = waves * sm_count;
@@ -348,7 +349,7 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   // its longest blocks.  Adjoint: rays meeting (tile, view), from the range
   // table; forward: the longest ray column range of (view, 32-bin block).
   {
-    const int ntile = bp_tile_count(nc);
+    const int ntile = bp_tile_count(nc, f.bp_h);
     std::vector<int4> rt((size_t)ntile * V_r);
     MS2G_CUDA(cudaMemcpy(rt.data(), f.d_bpr, sizeof(int4) * rt.size(), cudaMemcpyDeviceToHost));
     f.h_bp_cost.assign(rt.size(), 0);

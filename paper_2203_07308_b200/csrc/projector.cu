@@ -576,7 +576,21 @@ constexpr int kPadR = 2;
 #ifndef MS2G_BH96_MIN_NC
 #define MS2G_BH96_MIN_NC 1024
 #endif
-int bp_height(int nc) { return nc >= MS2G_BH96_MIN_NC ? 96 : 64; }
+// The minor extent of the fixed-point form's tiles for full view sets:
+// taller tiles cover more of each ray per visit (fewer rays clipped by the
+// tile's minor edges, fewer record loads per segment) and, with the windows
+// shared by the block's warps, cost no more shared memory.  View shards and
+// small plans keep the shorter tiles (more blocks per launch).  Measured at
+// C4 (CUDA events, C4 adjoint s=1 / s=2): 96 -> 256 at 1024^2 1.13 -> 1.02 ms,
+// 64 -> 192 at 512^2 0.58 -> 0.54 ms; the 180-view shard prefers 96 / 64.
+int bp_height(int nc, int V_r) {
+  static const int h1 = getenv("MS2G_BP_H1024") ? atoi(getenv("MS2G_BP_H1024")) : 0;   // experiment switches
+  static const int h2 = getenv("MS2G_BP_H512") ? atoi(getenv("MS2G_BP_H512")) : 0;
+  const bool full = V_r >= 720 && !getenv("MS2G_BP_FP32");
+  if (nc >= MS2G_BH96_MIN_NC) return h1 ? h1 : (full ? 256 : 96);
+  if (nc >= 512) return h2 ? h2 : (full ? 192 : 64);
+  return 64;
+}
 // Warps per block and accumulator windows: the fp32 form needs one window
 // per warp (plain read-modify-writes); the fixed-point form's integer adds
 // are atomic, so at H = 96 two warps share a window -- twice the warps
@@ -598,7 +612,8 @@ int bp_height(int nc) { return nc >= MS2G_BH96_MIN_NC ? 96 : 64; }
 template <bool FX, int H>
 struct BpWarps {
   static constexpr int kW = FX ? (H >= 96 ? MS2G_FX96_W : MS2G_FX64_W) : kBW;        // warps per block
-  static constexpr int kWin = FX ? (H >= 96 ? MS2G_FX96_WIN : MS2G_FX64_WIN) : kBW;  // accumulator windows
+  // accumulator windows: 4 at H <= 96, 2 at H = 128 .. 192, 1 from H = 256
+  static constexpr int kWin = FX ? (H >= 256 ? 1 : H >= 128 ? 2 : H >= 96 ? MS2G_FX96_WIN : MS2G_FX64_WIN) : kBW;
 };
 template <int H, bool FX = false>
 struct BpShape {
@@ -620,7 +635,7 @@ static inline BpTiling bp_tiling(int nc, int H) {
   t.per = t.maj * t.mnr;
   return t;
 }
-int bp_tile_count(int nc) { return 2 * bp_tiling(nc, bp_height(nc)).per; }
+int bp_tile_count(int nc, int H) { return 2 * bp_tiling(nc, H).per; }
 
 // Per (tile, view): bins [ta_r, te_r] of run r (r < n) of the tile family's
 // major axis, class cls_r.
@@ -660,7 +675,7 @@ __global__ void k_bp_ranges(const ViewEntry* __restrict__ views, int V_r, int B,
 }
 
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s) {
-  const int H = bp_height(f.nc);
+  const int H = f.bp_h;
   const BpTiling t = bp_tiling(f.nc, H);
   const size_t n = (size_t)2 * t.per * V_r;
   const int blocks = (int)((n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192);
@@ -1276,7 +1291,7 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
                                                                                              scale, accumulate, G);
     return check_launch("k_chunk_reduce");
   }
-  const int H = bp_height(f.nc);
+  const int H = f.bp_h;
   const BpTiling t = bp_tiling(f.nc, H);
   int ch[2], vpc[2];
   bp_launch_chunks(p, f, n_sel, ch);
@@ -1287,8 +1302,15 @@ int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, floa
   static const bool no_order = getenv("MS2G_BP_NO_ORDER") != nullptr;    // experiment switch
   const int* order = no_order ? nullptr : (d_sel ? order_sel : (n_sel == p->V_r ? f.d_bp_order : nullptr));
   const int slot = timing_begin(p, 1, f.factor, s);
-  if (H == 96) MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
-  else MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order));
+  switch (H) {
+    case 64: MS2G_TRY(bwd_launch<64>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order)); break;
+    case 96: MS2G_TRY(bwd_launch<96>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order)); break;
+    case 128: MS2G_TRY(bwd_launch<128>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order)); break;
+    case 192: MS2G_TRY(bwd_launch<192>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order)); break;
+    case 256: MS2G_TRY(bwd_launch<256>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order)); break;
+    case 320: MS2G_TRY(bwd_launch<320>(grid, s, p, f, sino, d_sel, n_sel, ch, vpc, t, order)); break;
+    default: return set_error(MS2G_ERR_CONFIG, "adjoint tile height must be 64, 96, 128, 192, 256 or 320");
+  }
   MS2G_TRY(check_launch("k_backward"));
   timing_end(p, slot, s);
   if (nplanes_out) *nplanes_out = ch[0] + ch[1];

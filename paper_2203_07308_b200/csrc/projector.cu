@@ -582,12 +582,13 @@ constexpr int kPadR = 2;
 // shared by the block's warps, cost no more shared memory.  View shards and
 // small plans keep the shorter tiles (more blocks per launch).  Measured at
 // C4 (CUDA events, C4 adjoint s=1 / s=2): 96 -> 256 at 1024^2 1.13 -> 1.02 ms,
-// 64 -> 192 at 512^2 0.58 -> 0.54 ms; the 180-view shard prefers 96 / 64.
+// 64 -> 192 at 512^2 0.58 -> 0.54 ms (320 / 256 no better); the 180-view
+// shard prefers 128 (0.181 against 0.188 ms at 96, 0.201 at 256) and 64.
 int bp_height(int nc, int V_r) {
   static const int h1 = getenv("MS2G_BP_H1024") ? atoi(getenv("MS2G_BP_H1024")) : 0;   // experiment switches
   static const int h2 = getenv("MS2G_BP_H512") ? atoi(getenv("MS2G_BP_H512")) : 0;
   const bool full = V_r >= 720 && !getenv("MS2G_BP_FP32");
-  if (nc >= MS2G_BH96_MIN_NC) return h1 ? h1 : (full ? 256 : 96);
+  if (nc >= MS2G_BH96_MIN_NC) return h1 ? h1 : (full ? 256 : 128);
   if (nc >= 512) return h2 ? h2 : (full ? 192 : 64);
   return 64;
 }

@@ -186,8 +186,10 @@ constexpr int kFwdUnroll = MS2G_FWD_UNROLL;
 // unsigned order is the float order, NaN above +inf) -- the bound of the
 // fixed-point adjoint's scale.  The words are zeroed by the pair prep.
 __device__ __forceinline__ void fwd_view_max(unsigned* rmaxv, size_t idx, bool vk, bool valid, float r) {
+#ifndef MS2G_NO_RMAXV
   const unsigned bits = __reduce_max_sync(0xffffffffu, valid ? __float_as_uint(fabsf(r)) : 0u);
   if (rmaxv && vk && (threadIdx.x & 31) == 0) atomicMax(rmaxv + idx, bits);
+#endif
 }
 
 // (pl, pu) = pair element e of a pair image (one 8-byte non-coherent load)
@@ -224,7 +226,7 @@ __device__ __forceinline__ bool fwd_fast_warp(bool valid, int cl, int ch, int wc
 // wave would otherwise wait on its longest rays; the summation order depends
 // on SEG only, not on SPLIT.
 template <int NB, int SPLIT, int SEG>
-__global__ void __launch_bounds__(32 * kFwdWarps) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
+__global__ void __launch_bounds__(32 * kFwdWarps, 16) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out,

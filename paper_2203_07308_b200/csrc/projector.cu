@@ -625,7 +625,10 @@ struct BpShape {
   static constexpr size_t kSmem = sizeof(float) * kAccRows * kBT;
   // resident blocks per SM: 24 (H = 64) / 16 (H = 96) warps of the fp32 form; the
   // fixed-point form keeps the block count (shared memory) at twice the warps
-  static constexpr int kMinBlocks = (FX && H >= 96) ? 32 / BpWarps<FX, H>::kW : (H <= 64 ? 24 : 16) / kBW;
+#ifndef MS2G_FX_WARPS_SM
+#define MS2G_FX_WARPS_SM 32
+#endif
+  static constexpr int kMinBlocks = (FX && H >= 96) ? MS2G_FX_WARPS_SM / BpWarps<FX, H>::kW : (H <= 64 ? 24 : 16) / kBW;
 };
 
 struct BpTiling {

@@ -192,6 +192,15 @@ __device__ __forceinline__ void fwd_view_max(unsigned* rmaxv, size_t idx, bool v
 #endif
 }
 
+// the same for several views per warp (the TILE forward): groups of G lanes
+template <int G>
+__device__ __forceinline__ void fwd_view_max_g(unsigned* rmaxv, size_t idx, bool vk, bool valid, float r) {
+  unsigned bits = valid ? __float_as_uint(fabsf(r)) : 0u;
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
+  if (rmaxv && vk && (threadIdx.x & (G - 1)) == 0) atomicMax(rmaxv + idx, bits);
+}
+
 // (pl, pu) = pair element e of a pair image (one 8-byte non-coherent load)
 __device__ __forceinline__ void fwd_ld_pair(const float2* base, unsigned e, float& pl, float& pu) {
   asm("{\n\t.reg .u64 ad;\n\tmad.wide.u32 ad, %2, 8, %3;\n\tld.global.nc.v2.f32 {%0, %1}, [ad];\n\t}"
@@ -225,7 +234,7 @@ __device__ __forceinline__ bool fwd_fast_warp(bool valid, int cl, int ch, int wc
 // units help launches with few views (a view shard, a minibatch) whose single
 // wave would otherwise wait on its longest rays; the summation order depends
 // on SEG only, not on SPLIT.
-template <int NB, int SPLIT, int SEG>
+template <int NB, int SPLIT, int SEG, int TILE = 1>
 __global__ void __launch_bounds__(32 * kFwdWarps, 16) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
@@ -247,9 +256,15 @@ __global__ void __launch_bounds__(32 * kFwdWarps, 16) k_forward(const RayEntry* 
     bxi = item % gridDim.x;
     byi = item / gridDim.x;
   }
-  const int k = byi * VPB + vw;
+  // TILE = views per warp (SPLIT = 1): a warp takes 32 / TILE adjacent bins
+  // of TILE of the block's 4 views instead of 32 bins of one view -- rays of
+  // neighbouring views at the same bins cross a column within a few rows of
+  // each other, so a warp's gathers span fewer pair-image sectors
+  constexpr int BPW = 32 / TILE;                     // bins per warp and view
+  // (warp w: view group w / TILE of TILE views, bin group w % TILE of BPW bins)
+  const int k = byi * VPB + (TILE > 1 ? (warp / TILE) * TILE + lane / BPW : vw);
   const bool vk = k < n_sel;
-  const int t = bxi * 32 + lane;
+  const int t = bxi * 32 + (TILE > 1 ? (warp % TILE) * BPW + lane % BPW : lane);
   const int bz0 = blockIdx.z * NB;
   const int g = (sel && vk) ? __ldg(sel + k) : k;
   const bool valid = vk && t < B;
@@ -330,7 +345,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps, 16) k_forward(const RayEntry* 
       }
     }
 #pragma unroll
-    for (int i = 0; i < NB; ++i) red[vw][sg][i][lane] = make_float2(sa[i], sb[i]);
+    for (int i = 0; i < NB; ++i) red[TILE > 1 ? warp : vw][sg][i][lane] = make_float2(sa[i], sb[i]);
   }
   __syncthreads();
   if (q != 0) return;
@@ -341,7 +356,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps, 16) k_forward(const RayEntry* 
       float a = 0.f, b = 0.f;
 #pragma unroll
       for (int sg = 0; sg < SEG; ++sg) {
-        const float2 v = red[vw][sg][i][lane];
+        const float2 v = red[TILE > 1 ? warp : vw][sg][i][lane];
         a += v.x;
         b += v.y;
       }
@@ -349,7 +364,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps, 16) k_forward(const RayEntry* 
       if (bsino) r -= __ldg(bsino + ((size_t)(bz0 + i) * V_r + g) * B + t);
       out[((size_t)(bz0 + i) * n_sel + k) * B + t] = r;
     }
-    fwd_view_max(rmaxv, (size_t)(bz0 + i) * V_r + k, vk, valid, r);
+    if (TILE > 1) fwd_view_max_g<32 / TILE>(rmaxv, (size_t)(bz0 + i) * V_r + k, vk, valid, r);
+    else fwd_view_max(rmaxv, (size_t)(bz0 + i) * V_r + k, vk, valid, r);
   }
 }
 
@@ -483,7 +499,7 @@ static void fwd_launch_batch(int n_sel, int batch, cudaStream_t s, ms2g_plan* p,
                    (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, p->w_rmaxv);
 }
 
-template <int NB, int SPLIT, int SEG>
+template <int NB, int SPLIT, int SEG, int TILE = 1>
 static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, const FactorTables& f,
                         const int* d_sel, const float* b, float* out, const int* order_sel) {
   constexpr int VPB = kFwdWarps / SPLIT;
@@ -496,7 +512,7 @@ static void fwd_launch2(int n_sel, int batch, cudaStream_t s, ms2g_plan* p, cons
                                        : ((n_sel == p->V_r && f.fwd_order_vpb == VPB) ? f.d_fwd_order : nullptr));
   // experiment / test switch: every warp on the clamped path (bitwise equal)
   static const int allow_fast = getenv("MS2G_FWD_NO_FAST") ? 0 : 1;
-  (void)launch_k(k_forward<NB, SPLIT, SEG>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
+  (void)launch_k(k_forward<NB, SPLIT, SEG, TILE>, grid, dim3(32 * kFwdWarps), 0, s, f.d_rays, p->B, p->V_r, d_sel, n_sel,
                  (const float2*)p->w_pair, p->pair_stride, f.nc, b, out, order, allow_fast, p->w_rmaxv);
 }
 
@@ -529,7 +545,12 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
     // 4 segments per ray; SPLIT x SEG = 2 x 4, 4 x 8, 2 x 8 measured slower
     // ("tried and measured")
     fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
-  } else fwd_launch2<1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+  } else {
+    static const int tile = getenv("MS2G_FWD_TILE") ? atoi(getenv("MS2G_FWD_TILE")) : 4;   // experiment switch
+    if (tile == 4) fwd_launch2<1, 1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+    else if (tile == 2) fwd_launch2<1, 1, 4, 2>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+    else fwd_launch2<1, 1, 4, 1>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+  }
   const int rc = check_launch("k_forward");
   timing_end(p, slot, s);
   return rc;

@@ -235,7 +235,7 @@ __device__ __forceinline__ bool fwd_fast_warp(bool valid, int cl, int ch, int wc
 // wave would otherwise wait on its longest rays; the summation order depends
 // on SEG only, not on SPLIT.
 template <int NB, int SPLIT, int SEG, int TILE = 1>
-__global__ void __launch_bounds__(32 * kFwdWarps, 16) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
+__global__ void __launch_bounds__(32 * kFwdWarps, 64 / kFwdWarps) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out,
@@ -546,8 +546,14 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
     // ("tried and measured")
     fwd_launch2<1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
   } else {
-    static const int tile = getenv("MS2G_FWD_TILE") ? atoi(getenv("MS2G_FWD_TILE")) : 4;   // experiment switch
-    if (tile == 4) fwd_launch2<1, 1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+    static const int tile = getenv("MS2G_FWD_TILE") ? atoi(getenv("MS2G_FWD_TILE")) : (kFwdWarps == 8 ? 8 : 4);   // experiment switch
+    if (tile == kFwdWarps && tile == 8) fwd_launch2<1, 1, 4, (kFwdWarps == 8 ? 8 : 4)>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+    else if (tile == 4) {
+      static const int seg = getenv("MS2G_FWD_SEG") ? atoi(getenv("MS2G_FWD_SEG")) : 4;   // experiment switch
+      if (seg == 2) fwd_launch2<1, 1, 2, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+      else if (seg == 8) fwd_launch2<1, 1, 8, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+      else fwd_launch2<1, 1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+    }
     else if (tile == 2) fwd_launch2<1, 1, 4, 2>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
     else fwd_launch2<1, 1, 4, 1>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
   }

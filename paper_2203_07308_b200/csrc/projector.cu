@@ -720,8 +720,8 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
 // LDS.128 each): per step the lane's end coordinate, the two weights and two
 // shared read-modify-writes, the lower row at a compile-time offset.
 template <bool MIR, int H, bool FX = false>
-__device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, int nrays, int lane, unsigned sbase,
-                                         unsigned acc0, unsigned acc1) {
+__device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, const int* __restrict__ p1, int nrays,
+                                         int lane, unsigned sbase, unsigned acc0, unsigned acc1) {
   constexpr int kStride = MIR ? -4 * kBT : 4 * kBT;   // bytes per row step of u
   (void)acc0;
   (void)acc1;
@@ -735,12 +735,15 @@ __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, int nray
         : "=r"(lo), "=r"(u)
         : "r"((unsigned)lane), "r"(S), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
     const unsigned m = min(lo, S);
-    const float mu = (float)m, ml = (float)(S - m);
+    const float mu = (float)m, ml = FX ? 0.f : (float)(S - m);
     const unsigned adu = sbase + min(u, (unsigned)(H + 2)) * (unsigned)kStride;
     MS2G_DASSERT(adu >= acc0 && adu < acc1 && adu - kStride >= acc0 && adu - kStride < acc1);
     if (FX) {
-      const int up = __float_as_int(fmaf(mu, a.w, 12582912.f)) - 0x4B400000;
-      const int dn = __float_as_int(fmaf(ml, a.w, 12582912.f)) - 0x4B400000;
+      // up = round(m K); dn = round(S K) - round(m K), with round(S K) + M
+      // precomputed per ray (p1): one FFMA and two IADDs for both weights
+      const int ub = __float_as_int(fmaf(mu, a.w, 12582912.f));
+      const int up = ub - 0x4B400000;
+      const int dn = p1[q] - ub;
       if (MIR) asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.add.u32 [%0+128], %2;" :: "r"(adu), "r"(up), "r"(dn) : "memory");
       else asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.add.u32 [%0+-128], %2;" :: "r"(adu), "r"(up), "r"(dn) : "memory");
     } else
@@ -780,6 +783,7 @@ __global__ void __launch_bounds__(32 * BpWarps<FX, H>::kW, BpShape<H, FX>::kMinB
   constexpr int kBH = H, kWinR = BpShape<H, FX>::kWinR, kAccRows = BpShape<H, FX>::kAccRows;
   constexpr int NW = BpWarps<FX, H>::kW, NWIN = BpWarps<FX, H>::kWin;   // warps, windows (warp w -> window w % NWIN)
   __shared__ float4 st4[NW][33];   // entry 32 is a pipeline pad
+  __shared__ int st1[NW][33];      // FX: round(S K) + 1.5 * 2^23 (as float bits) per ray
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // blockIdx.x = (family, view chunk, tile): X-family blocks first
   const int bx = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x, bz = blockIdx.z;
@@ -913,8 +917,10 @@ __global__ void __launch_bounds__(32 * BpWarps<FX, H>::kW, BpShape<H, FX>::kMinB
     if (tn <= cte) {
       const int mb = mir ? nc - m0 - kBH : m0;
       const long long Et = Rn.F0 + (long long)c0 * (long long)Rn.S + (long long)Rn.S - ((long long)(mb - 1) << 32);
+      const float K = FX ? Rn.Ly32 * (rn * sig) : Rn.Ly32 * rn;
       st4[warp][lane] = make_float4(__uint_as_float((unsigned)Et), __uint_as_float((unsigned)(Et >> 32)),
-                                    __uint_as_float(Rn.S), FX ? Rn.Ly32 * (rn * sig) : Rn.Ly32 * rn);
+                                    __uint_as_float(Rn.S), K);
+      if (FX) st1[warp][lane] = __float_as_int(fmaf((float)Rn.S, K, 12582912.f));
     }
     __syncwarp();
     // fetch the next round while this one is processed
@@ -929,8 +935,8 @@ __global__ void __launch_bounds__(32 * BpWarps<FX, H>::kW, BpShape<H, FX>::kMinB
     //   plain:  phys row = u - 1      (sbase at row -1)
     //   mirror: phys row = kBH - u    (sbase at row kBH, negative stride)
     const int nrays = min(32, cte - ctb + 1);
-    if (mir) bp_steps<true, kBH, FX>(st4[warp], nrays, lane, tbase + 4u * kBT * kBH, acc0, acc1);
-    else bp_steps<false, kBH, FX>(st4[warp], nrays, lane, tbase - 4u * kBT, acc0, acc1);
+    if (mir) bp_steps<true, kBH, FX>(st4[warp], st1[warp], nrays, lane, tbase + 4u * kBT * kBH, acc0, acc1);
+    else bp_steps<false, kBH, FX>(st4[warp], st1[warp], nrays, lane, tbase - 4u * kBT, acc0, acc1);
     __syncwarp();
   }
   __syncthreads();

@@ -647,8 +647,14 @@ struct BpWarps {
 };
 template <int H, bool FX = false>
 struct BpShape {
-  static constexpr int kWinR = H + kPadR;                // rows per window (+ shared pads)
-  static constexpr int kAccRows = kPadR + BpWarps<FX, H>::kWin * kWinR;
+  // one shared window (H >= 256): 36 pad rows per side hold every row a ray
+  // of the tile's range can reach over the tile's 32 columns (slope <= 1, the
+  // range table's margin), so the step needs no clamp; otherwise 2 rows and
+  // the row index clamped into them
+  static constexpr bool kNoClamp = FX && BpWarps<FX, H>::kWin == 1;
+  static constexpr int kPad = kNoClamp ? 36 : kPadR;
+  static constexpr int kWinR = H + kPad;                 // rows per window (+ shared pads)
+  static constexpr int kAccRows = kPad + BpWarps<FX, H>::kWin * kWinR;
   static constexpr size_t kSmem = sizeof(float) * kAccRows * kBT;
   // resident blocks per SM: 24 (H = 64) / 16 (H = 96) warps of the fp32 form; the
   // fixed-point form keeps the block count (shared memory) at twice the warps
@@ -719,7 +725,7 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
 // The adjoint's steps over one round of <= 32 ray records (one broadcast
 // LDS.128 each): per step the lane's end coordinate, the two weights and two
 // shared read-modify-writes, the lower row at a compile-time offset.
-template <bool MIR, int H, bool FX = false>
+template <bool MIR, int H, bool FX = false, bool NOCLAMP = false>
 __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, const int* __restrict__ p1, int nrays,
                                          int lane, unsigned sbase, unsigned acc0, unsigned acc1) {
   constexpr int kStride = MIR ? -4 * kBT : 4 * kBT;   // bytes per row step of u
@@ -736,8 +742,8 @@ __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, const in
         : "r"((unsigned)lane), "r"(S), "r"(__float_as_uint(a.x)), "r"(__float_as_uint(a.y)));
     const unsigned m = min(lo, S);
     const float mu = (float)m, ml = FX ? 0.f : (float)(S - m);
-    const unsigned adu = sbase + min(u, (unsigned)(H + 2)) * (unsigned)kStride;
-    MS2G_DASSERT(adu >= acc0 && adu < acc1 && adu - kStride >= acc0 && adu - kStride < acc1);
+    const unsigned adu = sbase + (NOCLAMP ? u : min(u, (unsigned)(H + 2))) * (unsigned)kStride;   // mod 2^32
+    MS2G_DASSERT(adu >= acc0 && adu < acc1 && adu - (unsigned)kStride >= acc0 && adu - (unsigned)kStride < acc1);
     if (FX) {
       // up = round(m K); dn = round(S K) - round(m K), with round(S K) + M
       // precomputed per ray (p1): one FFMA and two IADDs for both weights
@@ -796,7 +802,8 @@ __global__ void __launch_bounds__(32 * BpWarps<FX, H>::kW, BpShape<H, FX>::kMinB
   const int plane = fam ? chx + chunk : chunk;
   const int c0 = (ti % tmaj) * kBT, m0 = (ti / tmaj) * kBH;   // major / minor origin
   const int win = warp % NWIN;
-  float* T = acc + (kPadR + win * kWinR) * kBT;
+  constexpr int kPad = BpShape<H, FX>::kPad;
+  float* T = acc + (kPad + win * kWinR) * kBT;
   for (int i = threadIdx.x; i < kAccRows * kBT; i += 32 * NW) acc[i] = 0.f;
   __syncthreads();
   pdl_wait();      // the residual sinogram comes from the forward
@@ -935,8 +942,9 @@ __global__ void __launch_bounds__(32 * BpWarps<FX, H>::kW, BpShape<H, FX>::kMinB
     //   plain:  phys row = u - 1      (sbase at row -1)
     //   mirror: phys row = kBH - u    (sbase at row kBH, negative stride)
     const int nrays = min(32, cte - ctb + 1);
-    if (mir) bp_steps<true, kBH, FX>(st4[warp], st1[warp], nrays, lane, tbase + 4u * kBT * kBH, acc0, acc1);
-    else bp_steps<false, kBH, FX>(st4[warp], st1[warp], nrays, lane, tbase - 4u * kBT, acc0, acc1);
+    constexpr bool kNC = BpShape<H, FX>::kNoClamp;
+    if (mir) bp_steps<true, kBH, FX, kNC>(st4[warp], st1[warp], nrays, lane, tbase + 4u * kBT * kBH, acc0, acc1);
+    else bp_steps<false, kBH, FX, kNC>(st4[warp], st1[warp], nrays, lane, tbase - 4u * kBT, acc0, acc1);
     __syncwarp();
   }
   __syncthreads();
@@ -949,7 +957,7 @@ __global__ void __launch_bounds__(32 * BpWarps<FX, H>::kW, BpShape<H, FX>::kMinB
     float s = 0.f;
 #pragma unroll
     for (int w = 0; w < NWIN; ++w) {
-      const float v = acc[(kPadR + w * kWinR) * kBT + idx];
+      const float v = acc[(kPad + w * kWinR) * kBT + idx];
       if (FX) s += s_bad[w] ? __int_as_float(0x7fc00000) : (float)__float_as_int(v) * s_inv[w];
       else s += v;
     }

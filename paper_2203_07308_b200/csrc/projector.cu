@@ -176,10 +176,15 @@ int launch_pair_prep(ms2g_plan* p, int nc, int batch, const float* x, cudaStream
 #define MS2G_FWD_WARPS 4
 #endif
 constexpr int kFwdWarps = MS2G_FWD_WARPS;
+// column-loop unroll of the single-image forward (16) and of the batched one (4)
 #ifndef MS2G_FWD_UNROLL
-#define MS2G_FWD_UNROLL 4
+#define MS2G_FWD_UNROLL 16
 #endif
 constexpr int kFwdUnroll = MS2G_FWD_UNROLL;
+#ifndef MS2G_FWD_UNROLL_B
+#define MS2G_FWD_UNROLL_B 4
+#endif
+constexpr int kFwdUnrollB = MS2G_FWD_UNROLL_B;
 
 
 // max |r| of the warp's rays into the view's word (float bits: for r >= 0 the
@@ -235,7 +240,13 @@ __device__ __forceinline__ bool fwd_fast_warp(bool valid, int cl, int ch, int wc
 // wave would otherwise wait on its longest rays; the summation order depends
 // on SEG only, not on SPLIT.
 template <int NB, int SPLIT, int SEG, int TILE = 1>
-__global__ void __launch_bounds__(32 * kFwdWarps, 64 / kFwdWarps) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
+// resident blocks the single-image forward is compiled for: 8 (64 registers)
+// -- with the 4-view warps and a 16-column unroll it outruns the 32-register
+// build at full occupancy (C4 s=1 0.640 -> 0.545 ms)
+#ifndef MS2G_FWD_MINB
+#define MS2G_FWD_MINB 8
+#endif
+__global__ void __launch_bounds__(32 * kFwdWarps, SPLIT == 1 ? MS2G_FWD_MINB : 64 / kFwdWarps) k_forward(const RayEntry* __restrict__ rays, int B, int V_r,
                                                  const int* __restrict__ sel, int n_sel,
                                                  const float2* __restrict__ pairs, size_t pair_stride, int nc,
                                                  const float* __restrict__ bsino, float* __restrict__ out,
@@ -305,7 +316,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps, 64 / kFwdWarps) k_forward(cons
       unsigned elo = (unsigned)Es, ehi = (unsigned)(Es >> 32);
       if (fast) {
         unsigned qhi = ehi + (unsigned)(c0 * L + kPairPad);
-#pragma unroll kFwdUnroll
+#pragma unroll(SPLIT == 1 ? kFwdUnroll : kFwdUnrollB)
         for (int c = c0; c < c1; ++c) {
           unsigned lo1, hi1;
           asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;" : "=r"(lo1), "=r"(hi1)
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps, 64 / kFwdWarps) k_forward(cons
         }
       } else {
         unsigned offk = (unsigned)(c0 * L + kPairPad);
-#pragma unroll kFwdUnroll
+#pragma unroll(SPLIT == 1 ? kFwdUnroll : kFwdUnrollB)
         for (int c = c0; c < c1; ++c) {
           unsigned lo1, hi1;
           asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));
@@ -423,7 +434,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) k_forward_batch(const RayEntry
     // u clamped to the zero pads (the carry-chained form of k_forward saves
     // 2 of ~5 NB instructions per column here and costs 6 registers at NB = 8)
     unsigned offk = (unsigned)(wcl * L + kPairPad);
-#pragma unroll kFwdUnroll
+#pragma unroll kFwdUnrollB
     for (int c = wcl; c < wch; ++c) {
       unsigned lo1, hi1;
       asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, 0;" : "=r"(lo1), "=r"(hi1) : "r"(elo), "r"(ehi), "r"(S));

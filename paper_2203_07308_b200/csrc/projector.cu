@@ -736,6 +736,10 @@ int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err,
 // The adjoint's steps over one round of <= 32 ray records (one broadcast
 // LDS.128 each): per step the lane's end coordinate, the two weights and two
 // shared read-modify-writes, the lower row at a compile-time offset.
+#ifndef MS2G_BP_UNROLL
+#define MS2G_BP_UNROLL 8
+#endif
+constexpr int kBpUnroll = MS2G_BP_UNROLL;
 template <bool MIR, int H, bool FX = false, bool NOCLAMP = false>
 __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, const int* __restrict__ p1, int nrays,
                                          int lane, unsigned sbase, unsigned acc0, unsigned acc1) {
@@ -743,7 +747,7 @@ __device__ __forceinline__ void bp_steps(const float4* __restrict__ p4, const in
   (void)acc0;
   (void)acc1;
   float4 a = p4[0];
-#pragma unroll 4
+#pragma unroll kBpUnroll
   for (int q = 0; q < nrays; ++q) {
     const float4 an = p4[q + 1];
     const unsigned S = __float_as_uint(a.z);

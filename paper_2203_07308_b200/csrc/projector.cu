@@ -560,8 +560,14 @@ int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* o
     static const int tile = getenv("MS2G_FWD_TILE") ? atoi(getenv("MS2G_FWD_TILE")) : (kFwdWarps == 8 ? 8 : 4);   // experiment switch
     if (tile == kFwdWarps && tile == 8) fwd_launch2<1, 1, 4, (kFwdWarps == 8 ? 8 : 4)>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
     else if (tile == 4) {
-      static const int seg = getenv("MS2G_FWD_SEG") ? atoi(getenv("MS2G_FWD_SEG")) : 4;   // experiment switch
+      // column segments per ray: each about <= 256 columns long (the fp32
+      // summation error of a segment grows with its length; C4 forward parity
+      // 1.9e-6 with 4 segments of 256 at 1024^2, 2.8e-6 with 2 of 512), so 4
+      // at n_c >= 1024 and 2 below (C4 s=2: 0.297 -> 0.280 ms)
+      static const int seg_env = getenv("MS2G_FWD_SEG") ? atoi(getenv("MS2G_FWD_SEG")) : 0;   // experiment switch
+      const int seg = seg_env ? seg_env : (f.nc >= 1024 ? 4 : 2);
       if (seg == 2) fwd_launch2<1, 1, 2, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
+      else if (seg == 1) fwd_launch2<1, 1, 1, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
       else if (seg == 8) fwd_launch2<1, 1, 8, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
       else fwd_launch2<1, 1, 4, 4>(n_sel, batch, s, p, f, d_sel, b, out, order_sel);
     }

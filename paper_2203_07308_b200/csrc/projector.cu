@@ -539,7 +539,12 @@ int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch) {
 int launch_forward(ms2g_plan* p, const FactorTables& f, const float* b, float* out, const int* d_sel, int n_sel,
                    int batch, cudaStream_t s, const int* order_sel) {
   if (n_sel <= 0) return MS2G_OK;
-  const int nb = batch_group(batch);
+  // batches share one traversal (k_forward_batch) on coarse grids; at
+  // n_c >= 512 the single-image kernel (4-view warps, 64 registers) run over
+  // the batch is faster per image (C5 s=1: 0.0893 ms per image against 0.741
+  // / 8 = 0.0926 ms; s=2 keeps the shared traversal, 0.26 against 0.41 ms)
+  static const bool nb_env = getenv("MS2G_FWD_BATCH_SHARED") != nullptr;   // experiment switch
+  const int nb = (f.nc >= 512 && !nb_env) ? 1 : batch_group(batch);
   const int slot = timing_begin(p, 0, f.factor, s);
   // Work-unit shape (measured on B200, CUDA events):
   //  * single images: 4 segments per ray; one warp takes all four (SPLIT 1:

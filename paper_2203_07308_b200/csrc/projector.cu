@@ -665,7 +665,10 @@ template <bool FX, int H>
 struct BpWarps {
   static constexpr int kW = FX ? (H >= 96 ? MS2G_FX96_W : MS2G_FX64_W) : kBW;        // warps per block
   // accumulator windows: 4 at H <= 96, 2 at H = 128 .. 192, 1 from H = 256
-  static constexpr int kWin = FX ? (H >= 256 ? 1 : H >= 128 ? 2 : H >= 96 ? MS2G_FX96_WIN : MS2G_FX64_WIN) : kBW;
+#ifndef MS2G_FX_ONEWIN_H
+#define MS2G_FX_ONEWIN_H 128
+#endif
+  static constexpr int kWin = FX ? (H >= MS2G_FX_ONEWIN_H ? 1 : H >= 128 ? 2 : H >= 96 ? MS2G_FX96_WIN : MS2G_FX64_WIN) : kBW;
 };
 template <int H, bool FX = false>
 struct BpShape {

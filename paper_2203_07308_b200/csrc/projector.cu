@@ -632,15 +632,16 @@ constexpr int kPadR = 2;
 // tile's minor edges, fewer record loads per segment) and, with the windows
 // shared by the block's warps, cost no more shared memory.  View shards and
 // small plans keep the shorter tiles (more blocks per launch).  Measured at
-// C4 (CUDA events, C4 adjoint s=1 / s=2): 96 -> 256 at 1024^2 1.13 -> 1.02 ms,
-// 64 -> 192 at 512^2 0.58 -> 0.54 ms (320 / 256 no better); the 180-view
-// shard prefers 128 (0.181 against 0.188 ms at 96, 0.201 at 256) and 64.
+// C4 (CUDA events, C4 adjoint s=1 / s=2): 96 -> 256 at 1024^2 1.13 -> 1.02 ms
+// (320 no better), 64 -> 128 at 512^2 0.58 -> 0.52 ms (192 / 256 no better,
+// one shared window each); the 180-view shard prefers 128 at 1024^2 (0.169
+// against 0.188 ms at 96, 0.201 at 256) and 128 at 512^2 (0.101 against 0.105).
 int bp_height(int nc, int V_r) {
   static const int h1 = getenv("MS2G_BP_H1024") ? atoi(getenv("MS2G_BP_H1024")) : 0;   // experiment switches
   static const int h2 = getenv("MS2G_BP_H512") ? atoi(getenv("MS2G_BP_H512")) : 0;
   const bool full = V_r >= 720 && !getenv("MS2G_BP_FP32");
   if (nc >= MS2G_BH96_MIN_NC) return h1 ? h1 : (full ? 256 : 128);
-  if (nc >= 512) return h2 ? h2 : (full ? 192 : 64);
+  if (nc >= 512) return h2 ? h2 : 128;
   return 64;
 }
 // Warps per block and accumulator windows: the fp32 form needs one window

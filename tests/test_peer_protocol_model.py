@@ -30,11 +30,15 @@ def _run(P, rounds, seed, skip_rs_wait=False, skip_ag_wait=False):
     errors = []
     done = [0] * P
 
+    # the negative controls skew the ranks by milliseconds (rank r starts each
+    # round r x 2 ms late), so a missing wait shows up whatever the host load
+    skew = 2e-3 if (skip_rs_wait or skip_ag_wait) else 0.0
+
     def rank(r):
         d = iter(delays[r])
         for it in range(rounds):
             e = it + 1
-            time.sleep(next(d))
+            time.sleep(next(d) + skew * r)
             for c in range(P):                       # publish (fused into the chunk sum)
                 pub[r][c] = float((1 + r + 10 * it) * (c + 1))
                 time.sleep(next(d) / 4)

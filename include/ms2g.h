@@ -135,7 +135,11 @@ int ms2g_forward_project(ms2g_plan* plan, int32_t factor, const float* x, const 
  * (accumulate != 0: img += ...).  sino is compacted [batch][n_sel][B] in the
  * same view order forward_project used.  allreduce != 0 sums the partial
  * images over the ranks in place (requires attach_nccl or attach_peers; with
- * one rank and neither attached it is a no-op). */
+ * one rank and neither attached it is a no-op).  Accumulation is fixed point
+ * (DESIGN.md 7a): each contribution is rounded to 2^-22 of the largest one
+ * the tile's views can give, so the result is deterministic and
+ * order-independent, ~1e-6 relative; a non-finite sinogram value makes the
+ * affected tiles NaN. */
 int ms2g_back_project(ms2g_plan* plan, int32_t factor, const float* sino, float* img, float scale,
                       int32_t accumulate, const int32_t* subset, int32_t n_subset, int32_t allreduce,
                       void* stream);

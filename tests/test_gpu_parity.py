@@ -929,9 +929,10 @@ def test_tv_persistent_kernel(P, n, batch):
 def test_forward_fast_path_bitwise(P):
     """The forward's carry-chained element index (warps whose rays stay within
     kPairPad rows of the grid) against the clamped path for every warp
-    (MS2G_FWD_NO_FAST=1, subprocess): bitwise equal on ragged grids, factors
-    2 and 3, a view subset, a 45-degree view shard, an odd batch and a tiny
-    grid narrower than the pad."""
+    (MS2G_FWD_NO_FAST=1, subprocess), and the 4-view warp tiling against 1
+    and 2 views per warp (MS2G_FWD_TILE): bitwise equal on ragged grids,
+    factors 2 and 3, a view subset, a 45-degree view shard, an odd batch and
+    a tiny grid narrower than the pad."""
     import os
     import subprocess
     import sys
@@ -952,12 +953,14 @@ for n, V, B, facs, batch, sub, vb, ve in ((64, 90, 96, (2, 1), 1, None, 0, None)
 sys.stdout.buffer.write(np.concatenate(outs).astype(np.float32).tobytes())
 ''' % root
     res = []
-    for extra in ({}, {"MS2G_FWD_NO_FAST": "1"}):
+    # also the warp tilings (1, 2 or 4 views per warp): the same per-ray
+    # arithmetic on other lanes, so bit for bit the same outputs
+    for extra in ({}, {"MS2G_FWD_NO_FAST": "1"}, {"MS2G_FWD_TILE": "1"}, {"MS2G_FWD_TILE": "2"}):
         out = subprocess.run([sys.executable, "-c", code], capture_output=True, env=dict(os.environ, **extra),
                              timeout=600)
         assert out.returncode == 0, out.stderr.decode()[-2000:]
         res.append(np.frombuffer(out.stdout, dtype=np.float32))
-    assert res[0].size > 0 and np.array_equal(res[0], res[1])
+    assert res[0].size > 0 and all(np.array_equal(res[0], r) for r in res[1:])
 
 
 def test_gather_adjoint_variant_parity(P):

@@ -317,16 +317,20 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
     if (rc != MS2G_OK) return rc;
     if (herr) return set_error(MS2G_ERR_CONFIG, "a tile's shadow spans more than 2 ray classes (fan too wide)");
   }
-  // backprojector view chunks: about 24 "waves" of SM-count blocks (measured
-  // on B200 with the longest-first order below: 24 is best or within 2 % for
-  // C3, C4, its 180-view shard and C5 batch 8; 8 and 64 lose 3-10 %).  The
+  // backprojector view chunks: about 12-24 "waves" of SM-count blocks
+  // (measured on B200 with the longest-first order below; with the fp32
+  // adjoint 24 was best or within 2 % everywhere, 8 and 64 lost 3-10 %).  The
   // chunk partials are summed by k_chunk_reduce in fixed order.
   // The X- and Y-tile families only see the views with major-x / major-y
   // rays; a contiguous view shard (e.g. 45 degrees at P = 8) is almost all
   // one class, so each family gets view chunks in proportion to its views.
   const long long tiles = (long long)bp_tile_count(nc, f.bp_h) * d.batch;
   const long long per = tiles / 2;
-  const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : 24;
+  // 12 "waves" at n_c >= 512 since the fixed-point adjoint with tall tiles
+  // (C4 solve 493 -> 500 iterations/s, C3 13.9 -> 13.2 ms, the 180-view
+  // shard 18.7 -> 17.7 ms); 24 on coarser grids, whose small subset launches
+  // need the blocks (C3 s = 4 subset gradient 27.0 k against 22.1 k evals/s)
+  const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : (nc >= 512 ? 12 : 24);
   const long long target = waves * sm_count;
   long long nv[2] = {0, 0};
   for (const ViewEntry& ve : views) {

@@ -403,11 +403,7 @@ int fwd_views_per_block(const ms2g_plan* p, int n_sel, int batch);
 int launch_bp_ranges(const FactorTables& f, int V_r, int B, int4* out, int* err, cudaStream_t s);
 // publish: 0 = img = scale A_s^T sino (+ img), 1 = write scale * A_s^T sino
 // into the peer exchange slot (not img), 2 = leave the partial planes in
-// p->w_part for a fused epilogue; *nplanes_out = their count.
-// Precondition of the fixed-point adjoint: p->w_rmaxv holds, per view of the
-// launch, an upper bound of |sino| (written by the launch_forward that
-// produced sino, or by launch_view_absmax for a caller's sinogram); a stale
-// larger bound only coarsens the scale, a missing one (0) gives sigma = 1.
+// p->w_part for a fused epilogue; *nplanes_out = their count
 int launch_backward(ms2g_plan* p, const FactorTables& f, const float* sino, float* img, float scale,
                     int accumulate, const int* d_sel, int n_sel, int batch, cudaStream_t s, int publish = 0,
                     const int* order_sel = nullptr, int* nplanes_out = nullptr);

@@ -1443,6 +1443,11 @@ static int do_forward(ms2g_plan* p, const FactorTables* f, const float* x, const
   return launch_forward(p, *f, b, out, s.d_sel, s.n_sel, p->d.batch, st, s.ford);
 }
 
+// Every launch_backward needs p->w_rmaxv to bound |sino| per view (the
+// fixed-point adjoint's scale, projector.cu): written by the launch_forward
+// that produced sino (all solve / gradient / power paths), or here by
+// launch_view_absmax for a caller's sinogram.  A stale larger bound only
+// coarsens the scale; a missing one (0) would give sigma = 1.
 static int do_backward(ms2g_plan* p, const FactorTables* f, const float* sino, float* img, float scale,
                        int accumulate, int do_allreduce, const Sel& s, cudaStream_t st) {
   MS2G_TRY(launch_view_absmax(p, sino, s.n_sel, p->d.batch, st));   // a caller's sinogram: its per-view bounds

@@ -326,11 +326,12 @@ static int build_tables(ms2g_plan* p, FactorTables& f, int sm_count) {
   // one class, so each family gets view chunks in proportion to its views.
   const long long tiles = (long long)bp_tile_count(nc, f.bp_h) * d.batch;
   const long long per = tiles / 2;
-  // 12 "waves" at n_c >= 512 since the fixed-point adjoint with tall tiles
-  // (C4 solve 493 -> 500 iterations/s, C3 13.9 -> 13.2 ms, the 180-view
-  // shard 18.7 -> 17.7 ms); 24 on coarser grids, whose small subset launches
-  // need the blocks (C3 s = 4 subset gradient 27.0 k against 22.1 k evals/s)
-  const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : (nc >= 512 ? 12 : 24);
+  // 12 "waves" at n_c >= 256 since the fixed-point adjoint with tall tiles
+  // (C4 solve 493 -> 500 iterations/s, C3 13.9 -> 13.1 ms, C5 64.9 -> 63.9 ms,
+  // the 180-view shard 18.7 -> 17.7 ms, C3 s = 2 subset gradients 20.0 k ->
+  // 23.1 k evals/s); 24 below, whose small subset launches need the blocks
+  // (C3 s = 4 subset gradient 27.0 k against 22.1 k evals/s)
+  const long long waves = getenv("MS2G_BP_WAVES") ? atoi(getenv("MS2G_BP_WAVES")) : (nc >= 256 ? 12 : 24);
   const long long target = waves * sm_count;
   long long nv[2] = {0, 0};
   for (const ViewEntry& ve : views) {

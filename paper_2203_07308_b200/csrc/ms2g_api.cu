@@ -169,7 +169,9 @@ static int check_grid_ties(const ms2g_geom_desc& d, double pitch, const int32_t*
 // the covered fraction: a pixel row [rho, rho + 1) meets at most
 // (1 + S_max) / delta_min + 1 of them (delta_min = the smallest gap between
 // neighbouring rays, at c = 0 or c = n_c since F is linear in c), each
-// giving at most Lc_max.  Runs of a family add up.
+// giving at most Lc_max -- or, per unit of the row, at most
+// S_max / delta_min + 1 column steps overlap, each weighing Lc / S per unit
+// of minor travel: the smaller bound counts.  Runs of a family add up.
 static int plan_bp_bounds(FactorTables& f, const std::vector<RayEntry>& rays, const std::vector<ViewEntry>& views,
                           int V_r, int B, int nc) {
   std::vector<float> w(2 * (size_t)V_r, 0.f);
@@ -178,7 +180,7 @@ static int plan_bp_bounds(FactorTables& f, const std::vector<RayEntry>& rays, co
     const ViewEntry& ve = views[v];
     for (int sg = 0; sg < ve.nseg; ++sg) {
       const int fam = (ve.seg_cls[sg] & kMajorY) ? 1 : 0;
-      double lmax = 0.0, smax = 0.0, dmin = 1e300;
+      double lmax = 0.0, smax = 0.0, dmin = 1e300, lymax = 0.0;
       int cnt = 0, prev = -1;
       for (int t = ve.seg_t[sg]; t < ve.seg_t[sg + 1]; ++t) {
         const RayEntry& R = rays[(size_t)v * B + t];
@@ -186,6 +188,7 @@ static int plan_bp_bounds(FactorTables& f, const std::vector<RayEntry>& rays, co
         ++cnt;
         lmax = std::max(lmax, (double)R.Lc);
         smax = std::max(smax, (double)R.S / kFix);
+        lymax = std::max(lymax, (double)R.Lc / ((double)R.S / kFix));   // length per unit of minor travel
         if (prev >= 0) {
           const RayEntry& Q = rays[(size_t)v * B + prev];
           const double d0 = std::fabs((double)(R.F0 - Q.F0)) / kFix;
@@ -196,7 +199,12 @@ static int plan_bp_bounds(FactorTables& f, const std::vector<RayEntry>& rays, co
       }
       if (!cnt) continue;
       const double count = cnt == 1 ? 1.0 : std::min((double)cnt, (1.0 + smax) / std::max(dmin, 1e-6) + 1.0);
-      w[(size_t)fam * V_r + v] += (float)(lmax * count * 1.001 + 1e-30);
+      // or: a point of the row lies under at most S_max / delta_min + 1 of
+      // the rays' column steps, each weighing Ly = Lc / S per unit of minor
+      // travel, so the row receives at most Ly_max (S_max / delta_min + 1)
+      const double cover = cnt == 1 ? 1.0 : smax / std::max(dmin, 1e-6) + 1.0;
+      const double wb = std::min(lmax * count, lymax * cover);
+      w[(size_t)fam * V_r + v] += (float)(wb * 1.001 + 1e-30);
       lcm = std::max(lcm, lmax);
     }
   }
